@@ -1,0 +1,266 @@
+/*
+ * rinshan.h — C ABI of the B200-native batched Riichi-Mahjong environment step.
+ *
+ * This is the drop-in boundary for the reference's Pgx-style env path
+ * (mjsim.init / mjsim.step / mjsim.observe + the random-policy rollout
+ * harness).  Every entry point takes plain pointers and sizes; device
+ * pointers are CUDA global-memory addresses (e.g. torch tensor data_ptr()),
+ * `stream` is a cudaStream_t passed as void*.  No torch types cross this ABI.
+ *
+ * Reference interfaces each entry point replaces (paths under the
+ * reference's pkg/src/mjsim/):
+ *   rs_tables_build   hand/tables.py:212-224   build_tables()   (+ get_tables :278-291)
+ *   rs_tables_load    hand/tables.py:243-265   load_tables(path) blob format
+ *   rs_create         env/core.py:41-61        EnvConfig -> GameConfig (batched)
+ *   rs_init           env/core.py:97-98        init(seed, config) for n envs
+ *   rs_init_indexed   bench/runner.py:25-33,76-84  env_game_seed/env_policy_state + init
+ *   rs_step           env/core.py:101-110      step(state, action) for n envs
+ *                     (engine/engine.py:405-422 apply_action, :105-122 _finish)
+ *   rs_observe        env/observe.py:191-234   observe(state, seat)
+ *   rs_policy_random  env/policies.py:17-22    random_policy(legal, rng)
+ *   rs_rollout        bench/runner.py:97-121   run_shard.one_pass (auto-reset +
+ *                                              random_policy + step), fused
+ *   rs_export_env     engine/state.py:191-242  serialize_state (projection record)
+ *   rs_import_env     tests/engine_helpers.py:58-105 craft() (crafted states)
+ *
+ * Error convention: every function returns 0 on success, a negative RS_E*
+ * code on contract violations and a positive cudaError_t value when a CUDA
+ * call fails; rs_last_error() gives a message.  Per-env contract outcomes
+ * (illegal action, stepping a finished env) are reported in the per-env
+ * status byte, never as a global error (reference env/core.py:101-110).
+ */
+#ifndef RINSHAN_H
+#define RINSHAN_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define RS_ABI_VERSION 1
+
+#define RS_NUM_TILES 136
+#define RS_NUM_KINDS 34
+#define RS_NUM_ACTIONS 115
+#define RS_EVENT_WINDOW 64
+#define RS_MAX_RIVER 40
+#define RS_MAX_QUEUE 8
+#define RS_MASK_WORDS 4
+
+/* rules / modes / schemes (reference tiles.py:18-19, engine/types.py:12-14) */
+#define RS_RULE_RED 0
+#define RS_RULE_NO_RED 1
+#define RS_MODE_SINGLE 0
+#define RS_MODE_EAST 1
+#define RS_MODE_HALF 2
+#define RS_REWARD_SCORE_DELTA 0
+#define RS_REWARD_RANK 1
+
+/* per-env status bits written by rs_step (reference env/core.py:101-110) */
+#define RS_STATUS_ILLEGAL 1u  /* masked-off action: penalty, episode ends   */
+#define RS_STATUS_CONTRACT 2u /* stepped a finished env: state unchanged   */
+
+/* error codes */
+#define RS_OK 0
+#define RS_E_ARG (-1)
+#define RS_E_TABLES (-2)
+#define RS_E_STATE (-3)
+#define RS_E_CORRUPT (-4)
+
+typedef struct rs_config {
+  int32_t rule;           /* RS_RULE_*                                       */
+  int32_t mode;           /* RS_MODE_*                                       */
+  int32_t reward_scheme;  /* RS_REWARD_*                                     */
+  float illegal_penalty;  /* <= 0                                            */
+  int32_t max_steps;      /* truncation (engine/types.py:56)                 */
+  int32_t kazoe;          /* engine/types.py:53                              */
+  int32_t double_yakuman; /* engine/types.py:54                              */
+  int32_t agari_yame;     /* engine/types.py:55                              */
+  int32_t renchan_cap;    /* engine/types.py:57                              */
+} rs_config;
+
+/* ---- projection records (host side, import/export, parity harness) ---- */
+
+typedef struct rs_meld_rec {
+  int8_t type;        /* 0 chi 1 pon 2 kan_open 3 kan_closed 4 kan_added   */
+  int8_t n_tiles;
+  int8_t from_seat;   /* -1 for closed kan                                 */
+  int8_t pad0;
+  uint8_t tiles[4];   /* sorted tile ids                                   */
+  int16_t called_tile;
+  int16_t pad1;
+} rs_meld_rec;
+
+#define RS_RIVER_TSUMOGIRI 1u
+#define RS_RIVER_RIICHI 2u
+#define RS_RIVER_CALLED 4u
+
+typedef struct rs_hand_rec {
+  uint8_t concealed[14]; /* sorted tile ids                                */
+  uint8_t n_concealed;
+  uint8_t n_melds;
+  rs_meld_rec melds[4];
+  uint8_t river_tile[RS_MAX_RIVER];
+  uint8_t river_flags[RS_MAX_RIVER];
+  int32_t n_river;
+  int8_t riichi;       /* 0 / 1 / 2 (double)                               */
+  int8_t riichi_index;
+  int8_t ippatsu;
+  int8_t temp_furiten;
+  int8_t perm_furiten;
+  int8_t shanten;
+  int16_t pad;
+  uint64_t waits;      /* bit k: kind k completes the hand                 */
+} rs_hand_rec;
+
+/* kyoku result kinds (engine/engine.py: "tsumo", "ron", "exhaustive",
+ * "abort_nine_terminals", "abort_triple_ron", "abort_four_riichi",
+ * "abort_four_kan") */
+#define RS_RES_TSUMO 0
+#define RS_RES_RON 1
+#define RS_RES_EXHAUSTIVE 2
+#define RS_RES_ABORT_NINE 3
+#define RS_RES_ABORT_TRIPLE_RON 4
+#define RS_RES_ABORT_FOUR_RIICHI 5
+#define RS_RES_ABORT_FOUR_KAN 6
+
+#define RS_FORM_STANDARD 0
+#define RS_FORM_SEVEN_PAIRS 1
+#define RS_FORM_KOKUSHI 2
+
+typedef struct rs_win_rec {
+  int8_t yaku_han[40]; /* han (or yakuman multiplicity) per yaku id, 0 = absent */
+  int32_t yakuman;     /* yakuman count                                     */
+  int32_t han, fu, base, dora, ura, reds, form;
+} rs_win_rec;
+
+typedef struct rs_result_rec {
+  int32_t kyoku, honba, kind;
+  int32_t n_winners;
+  int8_t winners[4];
+  int32_t loser;
+  int32_t n_settlements;
+  int32_t deltas[3][4];
+  int32_t honba_component[3];
+  int32_t deposits_claimed[3];
+  rs_win_rec wins[3];
+  int32_t tenpai_mask; /* exhaustive draw: bit s = seat s tenpai            */
+  int32_t scores_after[4];
+} rs_result_rec;
+
+typedef struct rs_env_rec {
+  int32_t abi_version;
+  rs_config cfg;
+  uint8_t wall[RS_NUM_TILES];
+  int32_t cursor, kan_draws, dora_count;
+  rs_hand_rec hands[4];
+  int32_t scores[4];
+  int32_t kyoku, honba, deposits, repeats, phase, actor, drawn;
+  int32_t riichi_pending, rinshan_pending, call_tile, call_from;
+  int32_t n_queue;
+  int8_t queue_seat[RS_MAX_QUEUE];
+  int8_t queue_stage[RS_MAX_QUEUE];
+  int32_t n_rons;
+  int8_t rons[4];
+  int32_t call_chankan, kakan_kind, pending_dora, four_kan_pending, any_call_made;
+  uint64_t rng_key, rng_counter;
+  int32_t step_count, terminated, truncated;
+  int32_t events_len;          /* total events emitted so far            */
+  int16_t events[RS_EVENT_WINDOW][3]; /* last min(64, len), oldest first  */
+  int32_t n_results;
+  rs_result_rec last_result;
+  uint32_t legal_mask[RS_MASK_WORDS];
+  /* env wrapper (env/core.py:64-79) */
+  int32_t current_player;
+  int32_t env_terminated, env_truncated;
+  int32_t status;
+  float rewards[4];
+  /* rollout bookkeeping (bench/runner.py:25-33, 80-82) */
+  uint64_t env_key, policy_key, policy_counter;
+  int32_t resets;
+  int32_t pad;
+} rs_env_rec;
+
+/* ---- device buffers supplied by the caller ---- */
+
+typedef struct rs_step_out {
+  uint8_t* legal_mask;   /* [n][115] bool, may be NULL                      */
+  uint32_t* legal_bits;  /* [n][4] packed mask, may be NULL                 */
+  int8_t* current_player;/* [n]                                             */
+  float* rewards;        /* [n][4]                                          */
+  uint8_t* terminated;   /* [n]                                             */
+  uint8_t* truncated;    /* [n]                                             */
+  uint8_t* status;       /* [n] RS_STATUS_* bits, may be NULL               */
+} rs_step_out;
+
+/* observation tensors (reference docs/formats.md:32-52, env/observe.py:159-172) */
+typedef struct rs_obs_out {
+  uint8_t* hand_tokens;  /* [n][14]                                         */
+  uint8_t* event_tokens; /* [n][64][3]                                      */
+  int8_t* shanten;       /* [n]                                             */
+  int16_t* scores;       /* [n][4] points // 100, observer first            */
+  uint8_t* round_wind;   /* [n]                                             */
+  uint8_t* seat_wind;    /* [n]                                             */
+  uint8_t* kyoku;        /* [n]                                             */
+  int16_t* honba;        /* [n]                                             */
+  int16_t* deposits;     /* [n]                                             */
+  uint8_t* dora_tokens;  /* [n][5]                                          */
+  uint8_t* live_wall;    /* [n]                                             */
+  uint8_t* riichi_flags; /* [n][4]                                          */
+} rs_obs_out;
+
+typedef struct rs_rollout_stats {
+  /* accumulated on device over a rollout (reduced over envs by the host)  */
+  uint64_t steps;
+  uint64_t games_completed;
+  uint64_t illegal;
+} rs_rollout_stats;
+
+typedef struct rs_handle rs_handle;
+
+const char* rs_last_error(void);
+int rs_abi_version(void);
+
+/* tables (host-built once per process, uploaded per handle) */
+int rs_tables_build(void);
+int rs_tables_load(const uint8_t* blob, int64_t size);
+int rs_tables_blob(uint8_t* out, int64_t cap, int64_t* size);
+int rs_tables_crc(uint32_t* crc);
+int rs_tables_info(int32_t* n_suit_classes, int32_t* n_honor_classes,
+                   int32_t* n_pair_mp, int32_t* n_pair_sz);
+/* host-side query of the re-encoded tables (unit tests of the encoding) */
+int rs_tables_shanten_std(uint32_t cm, uint32_t cp, uint32_t cs, uint32_t cz,
+                          int32_t melds, int32_t* out);
+
+int rs_create(rs_handle** out, int64_t n_envs, const rs_config* cfg, int32_t device);
+int rs_destroy(rs_handle* h);
+int64_t rs_num_envs(const rs_handle* h);
+int64_t rs_state_bytes(const rs_handle* h);
+
+/* seeds_dev: device u64[n] game seeds; policy streams are derived from them */
+int rs_init(rs_handle* h, const uint64_t* seeds_dev, const rs_step_out* out, void* stream);
+/* bench seeding: env i uses env_game_seed(seed, index_base + i, 0) and
+ * env_policy_state(seed, index_base + i) */
+int rs_init_indexed(rs_handle* h, uint64_t seed, int64_t index_base,
+                    const rs_step_out* out, void* stream);
+int rs_step(rs_handle* h, const int32_t* actions_dev, const rs_step_out* out, void* stream);
+/* seats_dev: device int8[n] or NULL for each env's current player */
+int rs_observe(rs_handle* h, const int8_t* seats_dev, const rs_obs_out* obs, void* stream);
+/* random policy over each env's legal list using its policy stream */
+int rs_policy_random(rs_handle* h, int32_t* actions_dev, void* stream);
+/* fused rollout: `steps` iterations of {auto-reset, random policy, step}
+ * per env; obs (may be NULL) receives each env's final observation of its
+ * current player; actions_log (may be NULL) is [steps][n] int16; stats_dev
+ * (may be NULL) is a device rs_rollout_stats accumulated atomically;
+ * digests_dev (may be NULL) is u64[n] per-env trajectory digests.        */
+int rs_rollout(rs_handle* h, int32_t steps, const rs_obs_out* obs, int16_t* actions_log,
+               rs_rollout_stats* stats_dev, uint64_t* digests_dev, void* stream);
+
+int rs_export_env(rs_handle* h, int64_t env, rs_env_rec* out);
+int rs_import_env(rs_handle* h, int64_t env, const rs_env_rec* in);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* RINSHAN_H */
