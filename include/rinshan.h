@@ -249,16 +249,24 @@ int rs_step(rs_handle* h, const int32_t* actions_dev, const rs_step_out* out, vo
 int rs_observe(rs_handle* h, const int8_t* seats_dev, const rs_obs_out* obs, void* stream);
 /* random policy over each env's legal list using its policy stream */
 int rs_policy_random(rs_handle* h, int32_t* actions_dev, void* stream);
-/* fused rollout: `steps` iterations of {auto-reset, random policy, step}
- * per env; obs (may be NULL) receives each env's final observation of its
- * current player; actions_log (may be NULL) is [steps][n] int16; stats_dev
- * (may be NULL) is a device rs_rollout_stats accumulated atomically;
- * digests_dev (may be NULL) is u64[n] per-env trajectory digests.        */
-int rs_rollout(rs_handle* h, int32_t steps, const rs_obs_out* obs, int16_t* actions_log,
-               rs_rollout_stats* stats_dev, uint64_t* digests_dev, void* stream);
+/* fused rollout: `steps` iterations of {auto-reset, random policy, step,
+ * observe} per env (bench/runner.py:97-121).  obs (may be NULL) receives
+ * the current player's observation: obs_slots = 1 keeps only the final
+ * one, obs_slots = steps writes slot t of [steps][n] every step (a
+ * trajectory buffer).  actions_log (may be NULL) is [steps][n] int16;
+ * stats_dev (may be NULL) is a device rs_rollout_stats accumulated
+ * atomically; digests_dev (may be NULL) is u64[n] per-env trajectory
+ * digests chained across calls; out (may be NULL) gets the final step's
+ * outputs. */
+int rs_rollout(rs_handle* h, int32_t steps, const rs_obs_out* obs, int32_t obs_slots,
+               int16_t* actions_log, rs_rollout_stats* stats_dev, uint64_t* digests_dev,
+               const rs_step_out* out, void* stream);
 
 int rs_export_env(rs_handle* h, int64_t env, rs_env_rec* out);
 int rs_import_env(rs_handle* h, int64_t env, const rs_env_rec* in);
+/* sizeof of the records above, for binding checks: config, meld, hand,
+ * win, result, env */
+int rs_record_sizes(int32_t* out /*[6]*/);
 
 #ifdef __cplusplus
 }

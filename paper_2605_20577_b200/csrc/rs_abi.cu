@@ -1,0 +1,507 @@
+// rs_abi.cu — sm_100a kernels and the extern "C" boundary (include/rinshan.h).
+//
+// Kernels (one thread per env, 128-thread CTAs; the pre-merged shanten
+// tables are staged into shared memory at CTA start):
+//   k_init      init(seed)                         env/core.py:97-98
+//   k_step      step(state, action) + legal mask   env/core.py:101-110
+//   k_observe   observe(state, seat)               env/observe.py:191-234
+//   k_policy    random_policy(legal, rng)          env/policies.py:17-22
+//   k_rollout   fused {auto-reset, random policy, step, observe} x K
+//               (bench/runner.py:97-121 one_pass)
+//   k_expand    packed legal bits -> bool[n][115] (coalesced)
+//   k_export / k_import  projection records for the parity harness
+#include <cuda_runtime.h>
+#include <stdarg.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <mutex>
+#include <string>
+
+#include "rs_io.cuh"
+
+using namespace rs;
+
+namespace {
+
+constexpr int BLOCK = 128;
+
+thread_local std::string g_err;
+int set_err(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+#define CUDA_TRY(expr)                                                                  \
+  do {                                                                                  \
+    cudaError_t _e = (expr);                                                            \
+    if (_e != cudaSuccess) return set_err((int)_e, "%s: %s", #expr, cudaGetErrorString(_e)); \
+  } while (0)
+
+struct DevTables {
+  const uint8_t* suit_cls;
+  const uint8_t* honor_cls;
+  const uint8_t* t1;
+  const uint8_t* t2;
+  const uint32_t* t3;
+  int ns, nh, na, nb;
+  int smem;  // bytes of the staged copy
+};
+
+// one copy of the tables per device, shared by every handle on it (the
+// class-map pointers live in __constant__ memory of the module)
+struct DeviceTables {
+  void* mem = nullptr;
+  DevTables D{};
+};
+std::mutex g_dev_mu;
+DeviceTables g_dev_tables[64];
+
+int device_tables(int device, DevTables* out) {
+  std::lock_guard<std::mutex> lk(g_dev_mu);
+  if (device < 0 || device >= 64) return set_err(RS_E_ARG, "device id out of range");
+  DeviceTables& dt = g_dev_tables[device];
+  if (!dt.mem) {
+    const HostTables& H = host_tables();
+    // block layout: t3 | t1 | t2 (exactly the shared-memory image) | suit | honor
+    const size_t blk = ((size_t)SMEM_TABLE_BYTES + 255) & ~(size_t)255;
+    const size_t sz = blk + H.suit_cls.size() + 256 + H.honor_cls.size();
+    void* mem = nullptr;
+    CUDA_TRY(cudaMalloc(&mem, sz));
+    uint8_t* base = (uint8_t*)mem;
+    uint8_t* suit = base + blk;
+    uint8_t* honor = suit + ((H.suit_cls.size() + 255) & ~(size_t)255);
+    CUDA_TRY(cudaMemset(base, 0, blk));
+    CUDA_TRY(cudaMemcpy(base, H.t3.data(), H.t3.size() * 4, cudaMemcpyHostToDevice));
+    CUDA_TRY(cudaMemcpy(base + T1_OFF, H.t1.data(), H.t1.size(), cudaMemcpyHostToDevice));
+    CUDA_TRY(cudaMemcpy(base + T2_OFF, H.t2.data(), H.t2.size(), cudaMemcpyHostToDevice));
+    CUDA_TRY(cudaMemcpy(suit, H.suit_cls.data(), H.suit_cls.size(), cudaMemcpyHostToDevice));
+    CUDA_TRY(cudaMemcpy(honor, H.honor_cls.data(), H.honor_cls.size(), cudaMemcpyHostToDevice));
+    const uint8_t* sp = suit;
+    const uint8_t* hp = honor;
+    CUDA_TRY(cudaMemcpyToSymbol(c_suit_cls, &sp, sizeof(sp)));
+    CUDA_TRY(cudaMemcpyToSymbol(c_honor_cls, &hp, sizeof(hp)));
+    dt.D.suit_cls = suit;
+    dt.D.honor_cls = honor;
+    dt.D.t3 = reinterpret_cast<const uint32_t*>(base);
+    dt.D.t1 = base + T1_OFF;
+    dt.D.t2 = base + T2_OFF;
+    dt.D.ns = NS; dt.D.nh = NH; dt.D.na = NA; dt.D.nb = NB;
+    dt.D.smem = SMEM_TABLE_BYTES;
+    dt.mem = mem;
+  }
+  *out = dt.D;
+  return 0;
+}
+
+struct StepOut {
+  uint32_t* legal_bits;
+  int8_t* current_player;
+  float* rewards;
+  uint8_t* terminated;
+  uint8_t* truncated;
+  uint8_t* status;
+};
+
+// stage the packed t3 | t1 | t2 block (SMEM_TABLE_BYTES, a multiple of 2)
+// into shared memory with 16-byte vector copies; the engine reads it at
+// compile-time offsets (rs_hand.cuh t1_at / t2_at / t3_at)
+__device__ __forceinline__ Tabs stage_tables(const DevTables& D) {
+  const uint4* src = reinterpret_cast<const uint4*>(D.t3);
+  uint4* dst = reinterpret_cast<uint4*>(g_smem);
+  constexpr int n16 = (SMEM_TABLE_BYTES + 15) / 16;
+  for (int i = threadIdx.x; i < n16; i += blockDim.x) dst[i] = __ldg(src + i);
+  __syncthreads();
+  return Tabs{};
+}
+
+__device__ __forceinline__ void write_step_out(const StepOut& o, int e, const Engine& E, const Mask115& m,
+                                               const float* r, int status) {
+  if (o.legal_bits) {
+    reinterpret_cast<uint4*>(o.legal_bits)[e] = make_uint4(m.m[0], m.m[1], m.m[2], m.m[3]);
+  }
+  if (o.current_player) o.current_player[e] = (int8_t)E.g.current_player;
+  if (o.rewards) reinterpret_cast<float4*>(o.rewards)[e] = make_float4(r[0], r[1], r[2], r[3]);
+  if (o.terminated) o.terminated[e] = (uint8_t)E.g.env_terminated;
+  if (o.truncated) o.truncated[e] = (uint8_t)E.g.env_truncated;
+  if (o.status) o.status[e] = (uint8_t)status;
+}
+
+__global__ void __launch_bounds__(BLOCK) k_init(const __grid_constant__ Soa S, const __grid_constant__ DevTables D,
+    const __grid_constant__ Cfg C, const uint64_t* seeds, uint64_t seed,
+                                                int64_t base, int indexed, StepOut out) {
+  const Tabs T = stage_tables(D);
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= S.n) return;
+  Engine E(S, T, C, e);
+  uint64_t game_seed;
+  if (indexed) {
+    // bench/runner.py:25-33
+    E.g.env_key = derive_key(mix64(seed), (uint64_t)(base + e));
+    E.g.policy_key = derive_key(E.g.env_key, 1);
+    game_seed = derive_key(E.g.env_key, 2);
+  } else {
+    game_seed = seeds[e];
+    E.g.env_key = game_seed;
+    E.g.policy_key = derive_key(game_seed, 1);
+  }
+  E.g.policy_counter = 0;
+  E.g.resets = 0;
+  float r[4];
+  E.init_game(game_seed, r);
+  E.store();
+  write_step_out(out, e, E, E.load_legal(), r, 0);
+}
+
+__global__ void __launch_bounds__(BLOCK) k_step(const __grid_constant__ Soa S, const __grid_constant__ DevTables D,
+    const __grid_constant__ Cfg C, const int32_t* actions, StepOut out) {
+  const Tabs T = stage_tables(D);
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= S.n) return;
+  Engine E(S, T, C, e);
+  E.load();
+  Mask115 m;
+  float r[4];
+  const int st = E.step(actions[e], m, r);
+  if (st != RS_STATUS_CONTRACT) E.store();
+  write_step_out(out, e, E, m, r, st);
+}
+
+__global__ void __launch_bounds__(BLOCK) k_policy(const __grid_constant__ Soa S, const __grid_constant__ DevTables D,
+    const __grid_constant__ Cfg C, int32_t* actions) {
+  const Tabs T = stage_tables(D);
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= S.n) return;
+  Engine E(S, T, C, e);
+  E.load();
+  if (E.g.env_terminated || E.g.env_truncated) { actions[e] = -1; return; }
+  actions[e] = E.random_action(E.load_legal());
+  E.store();
+}
+
+__global__ void __launch_bounds__(BLOCK) k_observe(const __grid_constant__ Soa S, const __grid_constant__ DevTables D,
+    const __grid_constant__ Cfg C, const int8_t* seats, rs_obs_out obs) {
+  const Tabs T = stage_tables(D);
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= S.n) return;
+  Engine E(S, T, C, e);
+  E.load();
+  write_obs(E, seats ? (int)seats[e] : E.g.current_player, obs, e);
+}
+
+// the fused rollout: the packed header stays in registers for all K steps
+__global__ void __launch_bounds__(BLOCK) k_rollout(const __grid_constant__ Soa S, const __grid_constant__ DevTables D,
+    const __grid_constant__ Cfg C, int steps, rs_obs_out obs,
+                                                   int obs_slots, int16_t* actions_log, rs_rollout_stats* stats,
+                                                   uint64_t* digests, StepOut out) {
+  const Tabs T = stage_tables(D);
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  unsigned long long games = 0;
+  if (e < S.n) {
+    Engine E(S, T, C, e);
+    E.load();
+    uint64_t d = digests ? digests[e] : 0ull;
+    float r[4] = {0.f, 0.f, 0.f, 0.f};
+    Mask115 m;
+    int st = 0;
+    for (int t = 0; t < steps; t++) {
+      if (E.g.env_terminated || E.g.env_truncated) {  // runner.py:107-109
+        E.g.resets++;
+        E.init_game(derive_key(E.g.env_key, 2 + (uint64_t)E.g.resets), r);
+      }
+      const int a = E.random_action(E.load_legal());
+      st = E.step(a, m, r);
+      if (actions_log) actions_log[(size_t)t * S.n + e] = (int16_t)a;
+      if (E.g.env_terminated || E.g.env_truncated) games++;
+      if (digests) d = digest_step(d, a, E, m, r);
+      if (obs_slots > 0 && (obs_slots > 1 || t == steps - 1)) {
+        const int slot = obs_slots > 1 ? t % obs_slots : 0;
+        write_obs(E, E.g.current_player, obs, (int64_t)slot * S.n + e);
+      }
+    }
+    E.store();
+    if (digests) digests[e] = d;
+    write_step_out(out, e, E, m, r, st);
+  }
+  if (stats) {
+    unsigned long long g = games;
+    for (int off = 16; off > 0; off >>= 1) g += __shfl_down_sync(0xffffffffu, g, off);
+    const int lane = threadIdx.x & 31;
+    const int active = min(32, max(0, S.n - (int)(blockIdx.x * blockDim.x + (threadIdx.x & ~31))));
+    if (lane == 0 && active > 0) {
+      atomicAdd(reinterpret_cast<unsigned long long*>(&stats->games_completed), g);
+      atomicAdd(reinterpret_cast<unsigned long long*>(&stats->steps), (unsigned long long)active * steps);
+    }
+  }
+}
+
+__global__ void k_expand(const uint32_t* bits, uint8_t* bools, int n) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= (int64_t)n * RS_NUM_ACTIONS) return;
+  const int64_t e = i / RS_NUM_ACTIONS;
+  const int a = (int)(i - e * RS_NUM_ACTIONS);
+  bools[i] = (uint8_t)((bits[e * 4 + (a >> 5)] >> (a & 31)) & 1u);
+}
+
+__global__ void k_export(const __grid_constant__ Soa S, const __grid_constant__ DevTables D,
+    const __grid_constant__ Cfg C, int e, rs_env_rec* out) {
+  const Tabs T = stage_tables(D);
+  if (threadIdx.x != 0) return;
+  Engine E(S, T, C, e);
+  export_env(E, C, *out);
+}
+
+__global__ void k_import(const __grid_constant__ Soa S, const __grid_constant__ DevTables D,
+    const __grid_constant__ Cfg C, int e, const rs_env_rec* in) {
+  const Tabs T = stage_tables(D);
+  if (threadIdx.x != 0) return;
+  Engine E(S, T, C, e);
+  E.load();
+  import_env(E, *in);
+}
+
+}  // namespace
+
+struct rs_handle {
+  int device;
+  int n;
+  Cfg cfg;
+  Soa S;
+  DevTables D;
+  void* mem;
+  size_t mem_bytes;
+  uint32_t* legal_bits_tmp;  // step output when the caller asks only for bools
+  rs_env_rec* rec_dev;
+};
+
+namespace {
+
+Cfg to_cfg(const rs_config* c) {
+  return Cfg{c->rule, c->mode, c->reward_scheme, c->illegal_penalty, c->max_steps,
+             c->kazoe, c->double_yakuman, c->agari_yame, c->renchan_cap};
+}
+int grid_of(int n) { return (n + BLOCK - 1) / BLOCK; }
+
+StepOut step_out(rs_handle* h, const rs_step_out* o) {
+  StepOut s{};
+  if (!o) return s;
+  s.legal_bits = o->legal_bits ? o->legal_bits : (o->legal_mask ? h->legal_bits_tmp : nullptr);
+  s.current_player = o->current_player;
+  s.rewards = o->rewards;
+  s.terminated = o->terminated;
+  s.truncated = o->truncated;
+  s.status = o->status;
+  return s;
+}
+int finish_step_out(rs_handle* h, const rs_step_out* o, cudaStream_t st) {
+  if (o && o->legal_mask) {
+    const uint32_t* bits = o->legal_bits ? o->legal_bits : h->legal_bits_tmp;
+    const int64_t total = (int64_t)h->n * RS_NUM_ACTIONS;
+    k_expand<<<(unsigned)((total + 255) / 256), 256, 0, st>>>(bits, o->legal_mask, h->n);
+  }
+  CUDA_TRY(cudaGetLastError());
+  return 0;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* rs_last_error(void) { return g_err.c_str(); }
+int rs_abi_version(void) { return RS_ABI_VERSION; }
+
+int rs_tables_build(void) {
+  host_tables();
+  return 0;
+}
+int rs_tables_load(const uint8_t* blob, int64_t size) {
+  const int rc = host_tables_load(blob, size);
+  return rc ? set_err(rc, "suit-table blob rejected (magic, cardinality or crc)") : 0;
+}
+int rs_tables_blob(uint8_t* out, int64_t cap, int64_t* size) {
+  const int64_t s = host_tables_blob(out, cap);
+  if (size) *size = s;
+  return 0;
+}
+int rs_tables_crc(uint32_t* crc) {
+  *crc = host_tables().crc;
+  return 0;
+}
+int rs_tables_info(int32_t* ns, int32_t* nh, int32_t* na, int32_t* nb) {
+  const HostTables& T = host_tables();
+  if (ns) *ns = T.ns;
+  if (nh) *nh = T.nh;
+  if (na) *na = T.na;
+  if (nb) *nb = T.nb;
+  return 0;
+}
+int rs_tables_shanten_std(uint32_t cm, uint32_t cp, uint32_t cs, uint32_t cz, int32_t melds, int32_t* out) {
+  const HostTables& H = host_tables();
+  if (cm >= (uint32_t)SUIT_CODES || cp >= (uint32_t)SUIT_CODES || cs >= (uint32_t)SUIT_CODES ||
+      cz >= (uint32_t)HONOR_CODES || melds < 0 || melds > 4)
+    return set_err(RS_E_ARG, "code or meld count out of range");
+  Tabs T{H.suit_cls.data(), H.honor_cls.data(), H.t1.data(), H.t2.data(), H.t3.data()};
+  const uint32_t cls = (uint32_t)H.suit_cls[cm] | ((uint32_t)H.suit_cls[cp] << 8) | ((uint32_t)H.suit_cls[cs] << 16) |
+                       ((uint32_t)H.honor_cls[cz] << 24);
+  *out = std_shanten_cls(T, cls, melds);
+  return 0;
+}
+
+int64_t rs_state_bytes(const rs_handle* h) { return h ? (int64_t)h->mem_bytes : bytes_per_env(); }
+int64_t rs_num_envs(const rs_handle* h) { return h ? h->n : 0; }
+
+int rs_create(rs_handle** out, int64_t n_envs, const rs_config* cfg, int32_t device) {
+  if (!out || !cfg || n_envs <= 0 || n_envs > (1 << 26)) return set_err(RS_E_ARG, "bad rs_create arguments");
+  if (cfg->rule != RS_RULE_RED && cfg->rule != RS_RULE_NO_RED) return set_err(RS_E_ARG, "bad rule");
+  if (cfg->mode < 0 || cfg->mode > 2) return set_err(RS_E_ARG, "bad mode");
+  if (cfg->illegal_penalty > 0.f) return set_err(RS_E_ARG, "illegal penalty must be <= 0");
+  if (cfg->max_steps <= 0 || cfg->max_steps > 65535) return set_err(RS_E_ARG, "max_steps out of range");
+  const HostTables& H = host_tables();
+  CUDA_TRY(cudaSetDevice(device));
+  rs_handle* h = new rs_handle();
+  h->device = device;
+  h->n = (int)n_envs;
+  h->cfg = to_cfg(cfg);
+  const size_t n = (size_t)n_envs;
+  struct Part { void** p; size_t bytes; };
+  Soa& S = h->S;
+  S.n = (int)n;
+  const int trc = device_tables(device, &h->D);
+  if (trc) {
+    delete h;
+    return trc;
+  }
+  Part parts[] = {
+      {(void**)&S.hdr, 16 * 4 * n},          {(void**)&S.scores, 16 * n},
+      {(void**)&S.wall, (size_t)WALL_STRIDE * n}, {(void**)&S.hmask, 4 * 20 * n},
+      {(void**)&S.hcode, 4 * 16 * n},        {(void**)&S.hcls, 16 * n},
+      {(void**)&S.hinfo, 16 * n},            {(void**)&S.hwaits, 32 * n},
+      {(void**)&S.hrkind, 32 * n},           {(void**)&S.mtiles, 64 * n},
+      {(void**)&S.minfo, 64 * n},            {(void**)&S.river, 4 * RS_MAX_RIVER * 2 * n},
+      {(void**)&S.events, 64 * 2 * n},       {(void**)&S.legal, 16 * n},
+      {(void**)&S.results, sizeof(rs_result_rec) * n},
+      {(void**)&h->legal_bits_tmp, 16 * n},  {(void**)&h->rec_dev, sizeof(rs_env_rec)},
+  };
+  size_t total = 0;
+  for (auto& p : parts) total += (p.bytes + 255) & ~(size_t)255;
+  cudaError_t err = cudaMalloc(&h->mem, total);
+  if (err != cudaSuccess) {
+    delete h;
+    return set_err((int)err, "cudaMalloc(%zu): %s", total, cudaGetErrorString(err));
+  }
+  h->mem_bytes = total;
+  size_t off = 0;
+  for (auto& p : parts) {
+    *p.p = (char*)h->mem + off;
+    off += (p.bytes + 255) & ~(size_t)255;
+  }
+  auto cleanup = [&](cudaError_t e2, const char* what) {
+    cudaFree(h->mem);
+    delete h;
+    return set_err((int)e2, "%s: %s", what, cudaGetErrorString(e2));
+  };
+  if ((err = cudaMemset(h->mem, 0, total))) return cleanup(err, "state clear");
+  const void* kernels[] = {(const void*)k_init, (const void*)k_step, (const void*)k_policy,
+                           (const void*)k_observe, (const void*)k_rollout, (const void*)k_export,
+                           (const void*)k_import};
+  for (const void* k : kernels)
+    if ((err = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, h->D.smem)))
+      return cleanup(err, "cudaFuncSetAttribute");
+  *out = h;
+  return 0;
+}
+
+int rs_destroy(rs_handle* h) {
+  if (!h) return 0;
+  cudaSetDevice(h->device);
+  cudaFree(h->mem);
+  delete h;
+  return 0;
+}
+
+int rs_init(rs_handle* h, const uint64_t* seeds_dev, const rs_step_out* out, void* stream) {
+  if (!h || !seeds_dev) return set_err(RS_E_ARG, "rs_init: null argument");
+  cudaStream_t st = (cudaStream_t)stream;
+  k_init<<<grid_of(h->n), BLOCK, h->D.smem, st>>>(h->S, h->D, h->cfg, seeds_dev, 0, 0, 0, step_out(h, out));
+  return finish_step_out(h, out, st);
+}
+
+int rs_init_indexed(rs_handle* h, uint64_t seed, int64_t index_base, const rs_step_out* out, void* stream) {
+  if (!h) return set_err(RS_E_ARG, "rs_init_indexed: null handle");
+  cudaStream_t st = (cudaStream_t)stream;
+  k_init<<<grid_of(h->n), BLOCK, h->D.smem, st>>>(h->S, h->D, h->cfg, nullptr, seed, index_base, 1,
+                                                  step_out(h, out));
+  return finish_step_out(h, out, st);
+}
+
+int rs_step(rs_handle* h, const int32_t* actions_dev, const rs_step_out* out, void* stream) {
+  if (!h || !actions_dev) return set_err(RS_E_ARG, "rs_step: null argument");
+  cudaStream_t st = (cudaStream_t)stream;
+  k_step<<<grid_of(h->n), BLOCK, h->D.smem, st>>>(h->S, h->D, h->cfg, actions_dev, step_out(h, out));
+  return finish_step_out(h, out, st);
+}
+
+int rs_observe(rs_handle* h, const int8_t* seats_dev, const rs_obs_out* obs, void* stream) {
+  if (!h || !obs) return set_err(RS_E_ARG, "rs_observe: null argument");
+  cudaStream_t st = (cudaStream_t)stream;
+  k_observe<<<grid_of(h->n), BLOCK, h->D.smem, st>>>(h->S, h->D, h->cfg, seats_dev, *obs);
+  CUDA_TRY(cudaGetLastError());
+  return 0;
+}
+
+int rs_policy_random(rs_handle* h, int32_t* actions_dev, void* stream) {
+  if (!h || !actions_dev) return set_err(RS_E_ARG, "rs_policy_random: null argument");
+  cudaStream_t st = (cudaStream_t)stream;
+  k_policy<<<grid_of(h->n), BLOCK, h->D.smem, st>>>(h->S, h->D, h->cfg, actions_dev);
+  CUDA_TRY(cudaGetLastError());
+  return 0;
+}
+
+int rs_rollout(rs_handle* h, int32_t steps, const rs_obs_out* obs, int32_t obs_slots, int16_t* actions_log,
+               rs_rollout_stats* stats_dev, uint64_t* digests_dev, const rs_step_out* out, void* stream) {
+  if (!h || steps < 0) return set_err(RS_E_ARG, "rs_rollout: bad arguments");
+  if (obs_slots < 0 || (obs_slots > 1 && obs_slots != steps)) return set_err(RS_E_ARG, "obs_slots must be 0, 1 or steps");
+  if (obs_slots > 0 && !obs) return set_err(RS_E_ARG, "obs_slots > 0 needs obs buffers");
+  cudaStream_t st = (cudaStream_t)stream;
+  rs_obs_out o{};
+  if (obs) o = *obs;
+  k_rollout<<<grid_of(h->n), BLOCK, h->D.smem, st>>>(h->S, h->D, h->cfg, steps, o, obs ? obs_slots : 0,
+                                                     actions_log, stats_dev, digests_dev, step_out(h, out));
+  return finish_step_out(h, out, st);
+}
+
+int rs_export_env(rs_handle* h, int64_t env, rs_env_rec* out) {
+  if (!h || !out || env < 0 || env >= h->n) return set_err(RS_E_ARG, "rs_export_env: bad arguments");
+  CUDA_TRY(cudaSetDevice(h->device));
+  k_export<<<1, 32, h->D.smem>>>(h->S, h->D, h->cfg, (int)env, h->rec_dev);
+  CUDA_TRY(cudaGetLastError());
+  CUDA_TRY(cudaMemcpy(out, h->rec_dev, sizeof(rs_env_rec), cudaMemcpyDeviceToHost));
+  return 0;
+}
+
+int rs_import_env(rs_handle* h, int64_t env, const rs_env_rec* in) {
+  if (!h || !in || env < 0 || env >= h->n) return set_err(RS_E_ARG, "rs_import_env: bad arguments");
+  if (in->abi_version != RS_ABI_VERSION) return set_err(RS_E_ARG, "record abi version mismatch");
+  CUDA_TRY(cudaSetDevice(h->device));
+  CUDA_TRY(cudaMemcpy(h->rec_dev, in, sizeof(rs_env_rec), cudaMemcpyHostToDevice));
+  k_import<<<1, 32, h->D.smem>>>(h->S, h->D, h->cfg, (int)env, h->rec_dev);
+  CUDA_TRY(cudaGetLastError());
+  CUDA_TRY(cudaDeviceSynchronize());
+  return 0;
+}
+
+int rs_record_sizes(int32_t* out /*[6]*/) {
+  out[0] = (int32_t)sizeof(rs_config);
+  out[1] = (int32_t)sizeof(rs_meld_rec);
+  out[2] = (int32_t)sizeof(rs_hand_rec);
+  out[3] = (int32_t)sizeof(rs_win_rec);
+  out[4] = (int32_t)sizeof(rs_result_rec);
+  out[5] = (int32_t)sizeof(rs_env_rec);
+  return 0;
+}
+
+}  // extern "C"

@@ -1,0 +1,140 @@
+// rs_common.cuh — shared primitives of the B200 env-step engine.
+//
+// Everything here is __host__ __device__ so the identical engine source can
+// also be compiled by g++ for the test-only host harness (tests/hostcheck),
+// which exercises the transition logic without a GPU; the shipped library
+// is the nvcc sm_100a build.
+#pragma once
+
+#include <stdint.h>
+
+#if defined(__CUDACC__)
+#include <cuda_runtime.h>
+#define RS_HD __host__ __device__ inline
+#define RS_HOT __host__ __device__ __forceinline__
+#define RS_COLD __host__ __device__ __noinline__
+#define RS_DEV_ONLY __device__
+#else
+#define RS_HD inline
+#define RS_HOT inline
+#define RS_COLD
+#define RS_DEV_ONLY
+// host-only build (test harness): the CUDA vector types the state uses
+struct alignas(16) uint4 { uint32_t x, y, z, w; };
+struct alignas(16) int4 { int x, y, z, w; };
+inline uint4 make_uint4(uint32_t x, uint32_t y, uint32_t z, uint32_t w) { return uint4{x, y, z, w}; }
+#endif
+
+namespace rs {
+
+constexpr uint64_t GOLDEN = 0x9E3779B97F4A7C15ull;
+
+// ---------------------------------------------------------------- bit ops
+RS_HD int popc32(uint32_t x) {
+#if defined(__CUDA_ARCH__)
+  return __popc(x);
+#else
+  return __builtin_popcount(x);
+#endif
+}
+RS_HD int popc64(uint64_t x) {
+#if defined(__CUDA_ARCH__)
+  return __popcll(x);
+#else
+  return __builtin_popcountll(x);
+#endif
+}
+RS_HD int ctz32(uint32_t x) {  // x != 0
+#if defined(__CUDA_ARCH__)
+  return __ffs((int)x) - 1;
+#else
+  return __builtin_ctz(x);
+#endif
+}
+RS_HD int ctz64(uint64_t x) {  // x != 0
+#if defined(__CUDA_ARCH__)
+  return __ffsll((long long)x) - 1;
+#else
+  return __builtin_ctzll(x);
+#endif
+}
+RS_HD uint64_t umulhi64(uint64_t a, uint64_t b) {
+#if defined(__CUDA_ARCH__)
+  return __umul64hi(a, b);
+#else
+  return (uint64_t)(((unsigned __int128)a * b) >> 64);
+#endif
+}
+
+// ---------------------------------------------- counter RNG (rng.py:18-65)
+// SplitMix64 finalizer; key/counter streams; randbelow = high word of x*n.
+RS_HD uint64_t mix64(uint64_t x) {
+  x ^= x >> 30;
+  x *= 0xBF58476D1CE4E5B9ull;
+  x ^= x >> 27;
+  x *= 0x94D049BB133111EBull;
+  x ^= x >> 31;
+  return x;
+}
+RS_HD uint64_t derive_key(uint64_t key, uint64_t stream) {
+  return mix64((key ^ GOLDEN) + mix64(stream));
+}
+// value number `c` (1-based) of stream `key`
+RS_HD uint64_t stream_value(uint64_t key, uint64_t c) { return mix64(key + c * GOLDEN); }
+RS_HD uint32_t randbelow_from(uint64_t x, uint32_t n) { return (uint32_t)umulhi64(x, (uint64_t)n); }
+
+// --------------------------------------- per-nibble tile-count arithmetic
+// A hand is a 136-bit set of tile ids held in five 32-bit words; kind k owns
+// the nibble (k & 7) of word k >> 3.  SWAR turns words into per-kind counts.
+RS_HD uint32_t nib_counts(uint32_t x) {  // 8 nibbles of 4 bits -> 8 counts 0..4
+  uint32_t v = x - ((x >> 1) & 0x55555555u);
+  return (v & 0x33333333u) + ((v >> 2) & 0x33333333u);
+}
+// gather bit 0 of each nibble (positions 0,4,...,28) into bits 0..7
+RS_HD uint32_t nib_gather(uint32_t x) {
+  x &= 0x11111111u;
+  x = (x | (x >> 3)) & 0x03030303u;
+  x = (x | (x >> 6)) & 0x000F000Fu;
+  x = (x | (x >> 12)) & 0xFFu;
+  return x;
+}
+// bit i of the result set iff nibble count i >= t (t in 1..4)
+RS_HD uint32_t nib_ge(uint32_t counts, int t) {
+  uint32_t add = (uint32_t)(8 - t) * 0x11111111u;
+  return nib_gather(((counts + add) & 0x88888888u) >> 3);
+}
+RS_HD uint32_t nib_eq(uint32_t counts, int t) {
+  return t >= 4 ? nib_ge(counts, 4) : (nib_ge(counts, t) & ~nib_ge(counts, t + 1));
+}
+
+// ------------------------------------------------------------ tile facts
+RS_HD bool is_orphan(int k) { return k >= 27 || k % 9 == 0 || k % 9 == 8; }
+RS_HD bool is_terminal(int k) { return k < 27 && (k % 9 == 0 || k % 9 == 8); }
+constexpr uint64_t ORPHAN_MASK = (1ull << 0) | (1ull << 8) | (1ull << 9) | (1ull << 17) | (1ull << 18) |
+                                 (1ull << 26) | (0x7Full << 27);
+constexpr uint64_t GREEN_MASK = (1ull << 19) | (1ull << 20) | (1ull << 21) | (1ull << 23) | (1ull << 25) |
+                                (1ull << 32);
+constexpr uint64_t HONOR_MASK = 0x7Full << 27;
+constexpr uint64_t TERMINAL_MASK = ORPHAN_MASK & ~HONOR_MASK;
+constexpr uint64_t KINDS_MASK = (1ull << 34) - 1;
+
+RS_HD int dora_kind(int ind) {  // tiles.py:108-115
+  if (ind < 27) return ind - ind % 9 + (ind % 9 + 1) % 9;
+  if (ind < 31) return 27 + (ind - 27 + 1) % 4;
+  return 31 + (ind - 31 + 1) % 3;
+}
+RS_HD bool is_red_tile(int t) { return t == 16 || t == 52 || t == 88; }
+RS_HD int red_index_of_kind(int k) { return k == 4 ? 0 : (k == 13 ? 1 : (k == 22 ? 2 : -1)); }
+
+RS_HD uint32_t pow5(int i) {  // 5^i, i in 0..8, without memory
+  uint32_t p = 1;
+  for (int j = 0; j < i; j++) p *= 5u;
+  return p;
+}
+// code delta of one tile of kind k, and the suit slot (0 m, 1 p, 2 s, 3 z)
+RS_HD uint32_t kind_pow(int k) {
+  return k < 27 ? pow5(8 - k % 9) : pow5(6 - (k - 27));
+}
+RS_HD int kind_suit(int k) { return k < 27 ? k / 9 : 3; }
+
+}  // namespace rs

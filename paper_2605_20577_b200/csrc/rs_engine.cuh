@@ -1,0 +1,981 @@
+// rs_engine.cuh — the kyoku/game state machine, one thread per env.
+//
+// Mirrors the reference transition function (engine/engine.py:105-891) and
+// env facade (env/core.py:65-110) over the SoA state of rs_state.cuh.  The
+// game scalars live in registers (`Game`) for the whole step; per-seat
+// hands are loaded into registers (`Hand`) where a transition reads or
+// rewrites them and stored back once.
+#pragma once
+
+#include "rs_hand.cuh"
+#include "rs_score.cuh"
+
+namespace rs {
+
+enum : int { PH_ACT = 0, PH_CALL = 1, PH_GAME_END = 2 };
+enum : int { ST_RON = 0, ST_PONKAN = 1, ST_CHI = 2 };
+enum : int {
+  EV_DRAW = 0, EV_DISCARD, EV_CHI, EV_PON, EV_KAN_OPEN, EV_KAN_CLOSED, EV_KAN_ADDED,
+  EV_RIICHI, EV_RON, EV_TSUMO, EV_DRAW_END, EV_NEW_DORA
+};
+enum : int {
+  A_RIICHI = 37, A_TSUMO = 38, A_RON = 39, A_PON = 40, A_CHI_LOW = 41, A_CHI_MID = 42,
+  A_CHI_HIGH = 43, A_KAN_OPEN = 44, A_KAN_CLOSED = 45, A_KAN_ADDED = 79, A_PASS = 113, A_NINE = 114
+};
+enum : int { M_CHI = 0, M_PON = 1, M_KAN_OPEN = 2, M_KAN_CLOSED = 3, M_KAN_ADDED = 4 };
+
+struct Mask115 {
+  uint32_t m[4];
+  RS_HD void clear() { m[0] = m[1] = m[2] = m[3] = 0; }
+  RS_HD void set(int a) {
+    const uint32_t b = 1u << (a & 31);
+    if ((a >> 5) == 0) m[0] |= b;
+    else if ((a >> 5) == 1) m[1] |= b;
+    else if ((a >> 5) == 2) m[2] |= b;
+    else m[3] |= b;
+  }
+  RS_HD bool test(int a) const {
+    const uint32_t w = (a >> 5) == 0 ? m[0] : (a >> 5) == 1 ? m[1] : (a >> 5) == 2 ? m[2] : m[3];
+    return (w >> (a & 31)) & 1u;
+  }
+  RS_HD int count() const { return popc32(m[0]) + popc32(m[1]) + popc32(m[2]) + popc32(m[3]); }
+  // the i-th set bit (ascending ids, engine.py:258)
+  RS_HD int nth(int i) const {
+    for (int w = 0; w < 4; w++) {
+      uint32_t x = w == 0 ? m[0] : w == 1 ? m[1] : w == 2 ? m[2] : m[3];
+      const int c = popc32(x);
+      if (i < c) {
+        for (int j = 0; j < i; j++) x &= x - 1;
+        return 32 * w + ctz32(x);
+      }
+      i -= c;
+    }
+    return -1;
+  }
+};
+
+struct Engine {
+  const Soa& S;
+  const Tabs& T;
+  const Cfg& C;
+  int e;
+  Game g;
+
+  RS_HD Engine(const Soa& s, const Tabs& t, const Cfg& c, int env) : S(s), T(t), C(c), e(env) {}
+
+  // ------------------------------------------------------------- memory
+  RS_HD size_t at(int f) const { return (size_t)f * S.n + e; }
+  RS_HD void load() {
+    g.unpack(S.hdr[at(0)], S.hdr[at(1)], S.hdr[at(2)], S.hdr[at(3)], S.scores[e]);
+  }
+  RS_HD void store() const {
+    uint4 a, b, c, d;
+    int4 sc;
+    g.pack(a, b, c, d, sc);
+    S.hdr[at(0)] = a; S.hdr[at(1)] = b; S.hdr[at(2)] = c; S.hdr[at(3)] = d;
+    S.scores[e] = sc;
+  }
+  RS_HD int wall(int pos) const { return S.wall[(size_t)e * WALL_STRIDE + pos]; }
+  RS_HD uint32_t info(int s) const { return S.hinfo[at(s)]; }
+  RS_HD void set_info(int s, uint32_t v) const { S.hinfo[at(s)] = v; }
+  RS_HD uint64_t waits(int s) const { return S.hwaits[at(s)]; }
+  RS_HD int count_of(int s, int k) const {
+    return popc32((S.hmask[at(s * 5 + (k >> 3))] >> ((k & 7) * 4)) & 0xFu);
+  }
+  RS_HD uint32_t meld_info(int s, int i) const { return S.minfo[at(s * 4 + i)]; }
+  RS_HD uint32_t meld_tiles(int s, int i) const { return S.mtiles[at(s * 4 + i)]; }
+
+  // engine.py:100-102 (64-slot ring; the full history is reconstructed by
+  // the host while stepping)
+  RS_HD void emit(int type, int actor, int tile) {
+    S.events[at((int)(g.events_len & 63))] =
+        (uint16_t)(type | ((actor + 1) << 4) | ((tile + 1) << 7));
+    g.events_len++;
+  }
+
+  // ------------------------------------------------------ rng / dealing
+  // engine.py:139-164 (_start_kyoku) with tiles.py:142-144 / rng.py:59-65
+  RS_COLD void start_kyoku() {
+    uint8_t w[WALL_STRIDE];
+#pragma unroll 8
+    for (int i = 0; i < 136; i++) w[i] = (uint8_t)i;
+    for (int i = 136; i < WALL_STRIDE; i++) w[i] = 0;
+    uint64_t c = g.rng_counter;
+    for (int i = 135; i > 0; i--) {
+      c++;
+      const int j = (int)randbelow_from(stream_value(g.rng_key, c), (uint32_t)(i + 1));
+      const uint8_t t = w[i];
+      w[i] = w[j];
+      w[j] = t;
+    }
+    g.rng_counter = (uint32_t)c;
+    uint4* dst = reinterpret_cast<uint4*>(S.wall + (size_t)e * WALL_STRIDE);
+    const uint4* src = reinterpret_cast<const uint4*>(w);
+#pragma unroll
+    for (int i = 0; i < WALL_STRIDE / 16; i++) dst[i] = src[i];
+    const int dealer = g.dealer();
+    // deal 4-4-4 then 1 from the dealer (engine.py:142-151): seat s at
+    // offset i = (s - dealer) & 3 receives positions 16r + 4i .. +3 and 48 + i
+    for (int s = 0; s < 4; s++) {
+      const int i = (s - dealer) & 3;
+      Hand h;
+      h.w0 = h.w1 = h.w2 = h.w3 = h.w4 = 0;
+      h.cm = h.cp = h.cs = h.cz = 0;
+      for (int r = 0; r < 3; r++)
+        for (int j = 0; j < 4; j++) {
+          const int t = w[16 * r + 4 * i + j];
+          h.set_word(t >> 5, h.word(t >> 5) | (1u << (t & 31)));
+          const int k = t >> 2;
+          h.set_code(kind_suit(k), h.code(kind_suit(k)) + kind_pow(k));
+        }
+      {
+        const int t = w[48 + i];
+        h.set_word(t >> 5, h.word(t >> 5) | (1u << (t & 31)));
+        const int k = t >> 2;
+        h.set_code(kind_suit(k), h.code(kind_suit(k)) + kind_pow(k));
+      }
+      h.cls = class_of(T, 0, h.cm) | (class_of(T, 1, h.cp) << 8) | (class_of(T, 2, h.cs) << 16) |
+              (class_of(T, 3, h.cz) << 24);
+      h.info = hi::set_nconc(hi::set_riichi_index(0u, -1), 13);
+      finish_hand(T, h);
+      store_hand(S, e, s, h);
+      S.hrkind[at(s)] = 0ull;
+    }
+    g.cursor = 52;
+    g.kan_draws = 0;
+    g.dora_count = 1;
+    g.riichi_pending = 0;
+    g.rinshan_pending = 0;
+    g.call_tile = -1;
+    g.call_from = -1;
+    g.queue = 0;
+    g.rons = 0;
+    g.call_chankan = 0;
+    g.kakan_kind = -1;
+    g.pending_dora = 0;
+    g.four_kan_pending = 0;
+    g.any_call_made = 0;
+    draw(dealer);
+  }
+
+  // engine.py:167-178
+  RS_HD void draw(int seat) {
+    Hand h = load_hand(S, e, seat);
+    h.info = hi::set_temp(h.info, 0);
+    const int tile = wall(g.cursor);
+    g.cursor++;
+    hand_put(T, h, tile);
+    finish_hand(T, h);
+    store_hand(S, e, seat, h);
+    g.drawn = tile;
+    g.rinshan_pending = 0;
+    g.phase = PH_ACT;
+    g.actor = seat;
+    emit(EV_DRAW, seat, tile);
+  }
+  // engine.py:181-189 (temp furiten is NOT cleared here)
+  RS_HD void rinshan_draw(int seat, Hand& h) {
+    const int tile = wall(135 - g.kan_draws);
+    g.kan_draws++;
+    hand_put(T, h, tile);
+    finish_hand(T, h);
+    store_hand(S, e, seat, h);
+    g.drawn = tile;
+    g.rinshan_pending = 1;
+    g.phase = PH_ACT;
+    g.actor = seat;
+    emit(EV_DRAW, seat, tile);
+  }
+
+  // ------------------------------------------------------ win evaluation
+  // engine.py:345-375 (_win_context)
+  RS_HD void win_input(int seat, const Hand& h, int win_tile, bool tsumo, bool chankan, WinIn& w) const {
+    const uint32_t inf = h.info;
+    w.conc.c[0] = nib_counts(h.w0);
+    w.conc.c[1] = nib_counts(h.w1);
+    w.conc.c[2] = nib_counts(h.w2);
+    w.conc.c[3] = nib_counts(h.w3);
+    w.conc.c[4] = nib_counts(h.w4);
+    if (!tsumo) w.conc.add(win_tile >> 2, 1);
+    w.nmelds = hi::nmelds(inf);
+    w.closed = true;
+    Counts all = w.conc;
+    int reds = 0;
+    if (C.rule == RS_RULE_RED) {
+      reds = (int)h.has(16) + (int)h.has(52) + (int)h.has(88);
+      if (!tsumo && is_red_tile(win_tile)) reds++;
+    }
+    for (int i = 0; i < 4; i++) {
+      if (i < w.nmelds) {
+        const uint32_t mf = meld_info(seat, i), mt = meld_tiles(seat, i);
+        w.mtype[i] = mi::type(mf);
+        w.mbase[i] = (mt & 255) >> 2;
+        if (w.mtype[i] != M_KAN_CLOSED) w.closed = false;
+        const int nt = mi::ntiles(mf);
+        for (int j = 0; j < 4; j++)
+          if (j < nt) {
+            const int t = (mt >> (8 * j)) & 255;
+            all.add(t >> 2, 1);
+            if (C.rule == RS_RULE_RED && is_red_tile(t)) reds++;
+          }
+      }
+    }
+    w.win_kind = win_tile >> 2;
+    w.tsumo = tsumo;
+    w.seat_wind = g.seat_wind(seat);
+    w.round_wind = g.round_wind();
+    w.riichi = hi::riichi(inf);
+    w.ippatsu = hi::ippatsu(inf);
+    if (tsumo) {
+      w.last_tile = g.live() == 0 && !g.rinshan_pending;
+      w.rinshan = g.rinshan_pending;
+      w.first_draw = hi::nriver(inf) == 0 && !g.any_call_made && w.nmelds == 0 && !w.rinshan;
+      w.chankan = false;
+    } else {
+      w.last_tile = g.live() == 0 && !chankan;
+      w.rinshan = false;
+      w.first_draw = false;
+      w.chankan = chankan;
+    }
+    // dora.py:9-26
+    int dora = 0, ura = 0;
+    for (int i = 0; i < 5; i++)
+      if (i < g.dora_count) {
+        dora += all.get(dora_kind(wall(122 + 2 * i) >> 2));
+        if (w.riichi) ura += all.get(dora_kind(wall(123 + 2 * i) >> 2));
+      }
+    w.dora = dora;
+    w.ura = ura;
+    w.reds = reds;
+    w.double_yakuman = C.double_yakuman != 0;
+    w.kazoe = C.kazoe != 0;
+  }
+
+  // engine.py:386-390
+  RS_COLD bool can_tsumo(int seat, const Hand& h) const {
+    if (hi::shanten(h.info) != -1) return false;
+    WinIn w;
+    win_input(seat, h, g.drawn, true, false, w);
+    Reading r;
+    return score_win(w, r, true);
+  }
+  // engine.py:393-399 + types.py:93-100 (furiten)
+  RS_COLD bool can_ron(int seat, int tile, bool chankan) const {
+    const uint32_t inf = info(seat);
+    if (hi::shanten(inf) != 0) return false;
+    const uint64_t wt = waits(seat);
+    if (!((wt >> (tile >> 2)) & 1)) return false;
+    if (hi::temp(inf) || hi::perm(inf)) return false;
+    if (wt & S.hrkind[at(seat)]) return false;
+    const Hand h = load_hand(S, e, seat);
+    WinIn w;
+    win_input(seat, h, tile, false, chankan, w);
+    Reading r;
+    return score_win(w, r, true);
+  }
+
+  // --------------------------------------------------------- legality
+  RS_HD bool kan_draw_ok() const { return g.live() >= 1 && g.kan_draws < 4; }
+
+  // engine.py:230-246
+  RS_HD void discard_bits(const Hand& h, bool only_tenpai, Mask115& m) const {
+    uint64_t present = h.kinds_ge(1);
+    if (only_tenpai) {
+      uint64_t keep = 0, p = present;
+      while (p) {
+        const int k = ctz64(p);
+        p &= p - 1;
+        if (shanten_minus_kind(T, h, k) == 0) keep |= 1ull << k;
+      }
+      present = keep;
+    }
+    uint64_t kinds = present;
+    if (C.rule == RS_RULE_RED) {
+      const int reds[3] = {16, 52, 88};
+      for (int i = 0; i < 3; i++) {
+        const int k = reds[i] >> 2;
+        if (((present >> k) & 1) && h.has(reds[i])) {
+          m.set(34 + i);
+          if (h.count(k) <= 1) kinds &= ~(1ull << k);
+        }
+      }
+    }
+    m.m[0] |= (uint32_t)kinds;
+    m.m[1] |= (uint32_t)(kinds >> 32) & 3u;
+  }
+
+  // engine.py:331-339
+  RS_COLD bool kan_keeps_waits(const Hand& h, int kind) const {
+    const int melds = hi::nmelds(h.info);
+    Hand before = h;
+    hand_take(T, before, before.lowest_of_kind(kind));
+    const uint64_t old = compute_waits(T, before, melds);
+    Hand after = h;
+    for (int j = 0; j < 4; j++) hand_take(T, after, after.lowest_of_kind(kind));
+    const uint64_t nw = compute_waits(T, after, melds + 1);
+    return old == nw && !((old >> kind) & 1);
+  }
+
+  // engine.py:265-306
+  RS_HD void legal_act(Mask115& m) const {
+    const int seat = g.actor;
+    const Hand h = load_hand(S, e, seat);
+    if (g.riichi_pending) { discard_bits(h, true, m); return; }
+    if (hi::riichi(h.info)) {
+      if (can_tsumo(seat, h)) m.set(A_TSUMO);
+      const int kind = g.drawn >> 2;
+      if (C.rule == RS_RULE_RED && is_red_tile(g.drawn)) m.set(34 + red_index_of_kind(kind));
+      else m.set(kind);
+      if (h.count(kind) == 4 && kan_draw_ok() && kan_keeps_waits(h, kind)) m.set(A_KAN_CLOSED + kind);
+      return;
+    }
+    discard_bits(h, false, m);
+    if (g.drawn < 0) return;
+    const int nm = hi::nmelds(h.info);
+    bool closed = true;
+    uint64_t pon_kinds = 0;
+    for (int i = 0; i < 4; i++)
+      if (i < nm) {
+        const uint32_t mf = meld_info(seat, i);
+        if (mi::type(mf) != M_KAN_CLOSED) closed = false;
+        if (mi::type(mf) == M_PON) pon_kinds |= 1ull << ((meld_tiles(seat, i) & 255) >> 2);
+      }
+    if (closed && g.scores[seat] >= 1000 && g.live() >= 4 && hi::shanten(h.info) <= 0) m.set(A_RIICHI);
+    if (can_tsumo(seat, h)) m.set(A_TSUMO);
+    if (kan_draw_ok()) {
+      uint64_t quads = h.kinds_ge(4);
+      while (quads) { const int k = ctz64(quads); quads &= quads - 1; m.set(A_KAN_CLOSED + k); }
+      uint64_t adds = pon_kinds & h.kinds_ge(1);
+      while (adds) { const int k = ctz64(adds); adds &= adds - 1; m.set(A_KAN_ADDED + k); }
+    }
+    if (C.rule == RS_RULE_RED && !g.any_call_made && hi::nriver(h.info) == 0 && nm == 0 &&
+        popc64(h.kinds_ge(1) & ORPHAN_MASK) >= 9)
+      m.set(A_NINE);
+  }
+
+  // engine.py:309-328
+  RS_COLD void legal_call(Mask115& m) const {
+    const int seat = g.qseat(0), stage = g.qstage(0);
+    const int kind = g.call_tile >> 2;
+    m.set(A_PASS);
+    if (stage == ST_RON) {
+      m.set(A_RON);
+    } else if (stage == ST_PONKAN) {
+      m.set(A_PON);
+      if (count_of(seat, kind) >= 3 && kan_draw_ok()) m.set(A_KAN_OPEN);
+    } else {
+      const int n = kind % 9;
+      if (n <= 6 && count_of(seat, kind + 1) && count_of(seat, kind + 2)) m.set(A_CHI_LOW);
+      if (n >= 1 && n <= 7 && count_of(seat, kind - 1) && count_of(seat, kind + 1)) m.set(A_CHI_MID);
+      if (n >= 2 && count_of(seat, kind - 2) && count_of(seat, kind - 1)) m.set(A_CHI_HIGH);
+    }
+  }
+
+  // engine.py:105-122 + 253-262
+  RS_HD void compute_legal(Mask115& m) const {
+    m.clear();
+    if (g.terminated || g.truncated) return;
+    if (g.phase == PH_CALL) legal_call(m);
+    else legal_act(m);
+  }
+
+  // ------------------------------------------------------ kyoku endings
+  RS_HD rs_result_rec& result() const { return S.results[e]; }
+  RS_HD void begin_result(int kind) const {
+    rs_result_rec& r = result();
+    r.kyoku = g.kyoku;
+    r.honba = g.honba;
+    r.kind = kind;
+    r.n_winners = 0;
+    r.loser = -1;
+    r.n_settlements = 0;
+    r.tenpai_mask = 0;
+  }
+  RS_HD void end_result() const {
+    rs_result_rec& r = result();
+    for (int s = 0; s < 4; s++) r.scores_after[s] = g.scores[s];
+  }
+  RS_COLD void write_win(int i, const Reading& rd, const WinIn& w) const {
+    rs_win_rec& x = result().wins[i];
+    for (int id = 0; id < 40; id++) {
+      int han = 0;
+      if ((rd.mask >> id) & 1) {
+        if (rd.yakuman) han = ((rd.x2 >> id) & 1) ? 2 : 1;
+        else han = yaku_han_of(id, rd.form == 1 ? true : w.closed);
+      }
+      x.yaku_han[id] = (int8_t)han;
+    }
+    x.yakuman = rd.yakuman;
+    x.han = rd.han;
+    x.fu = rd.fu;
+    x.base = rd.base;
+    x.dora = w.dora;
+    x.ura = w.ura;
+    x.reds = w.reds;
+    x.form = rd.form;
+  }
+
+  RS_HD int final_kyoku() const { return C.mode == RS_MODE_SINGLE ? 0 : (C.mode == RS_MODE_EAST ? 3 : 7); }
+  RS_HD void end_game() {
+    g.phase = PH_GAME_END;
+    g.terminated = 1;
+    g.queue = 0;
+  }
+  // engine.py:842-872
+  RS_HD void advance_round(bool dealer_repeat, bool reset_honba) {
+    g.n_results++;
+    g.drawn = -1;
+    if (dealer_repeat && g.repeats >= C.renchan_cap) dealer_repeat = false;
+    if (dealer_repeat) g.repeats++;
+    const bool bankrupt = g.scores[0] < 0 || g.scores[1] < 0 || g.scores[2] < 0 || g.scores[3] < 0;
+    const int next_honba = reset_honba ? 0 : g.honba + 1;
+    if (C.mode == RS_MODE_SINGLE || bankrupt) { end_game(); return; }
+    if (dealer_repeat) {
+      int leader = 0;
+      for (int s = 1; s < 4; s++) if (g.scores[s] > g.scores[leader]) leader = s;
+      if (g.kyoku == final_kyoku() && C.agari_yame && leader == g.dealer()) { end_game(); return; }
+      g.honba = next_honba;
+      start_kyoku();
+      return;
+    }
+    if (g.kyoku + 1 > final_kyoku()) { end_game(); return; }
+    g.kyoku++;
+    g.honba = next_honba;
+    start_kyoku();
+  }
+  RS_HD void clear_call() {
+    g.call_tile = -1;
+    g.call_from = -1;
+    g.queue = 0;
+    g.rons = 0;
+    g.call_chankan = 0;
+    g.kakan_kind = -1;
+  }
+  // engine.py:829-839
+  RS_COLD void abort_kyoku(int kind) {
+    for (int s = 0; s < 4; s++)
+      if (hi::riichi(info(s))) { g.scores[s] += 1000; g.deposits -= 1; }
+    begin_result(kind);
+    end_result();
+    clear_call();
+    advance_round(true, false);
+  }
+  // engine.py:810-826
+  RS_COLD void exhaustive() {
+    emit(EV_DRAW_END, -1, -1);
+    int tmask = 0, n = 0;
+    for (int s = 0; s < 4; s++)
+      if (hi::shanten(info(s)) == 0) { tmask |= 1 << s; n++; }
+    int d[4] = {0, 0, 0, 0};
+    if (n > 0 && n < 4) {
+      const int gain = 3000 / n, loss = 3000 / (4 - n);
+      for (int s = 0; s < 4; s++) d[s] = ((tmask >> s) & 1) ? gain : -loss;
+    }
+    for (int s = 0; s < 4; s++) g.scores[s] += d[s];
+    begin_result(RS_RES_EXHAUSTIVE);
+    rs_result_rec& r = result();
+    r.tenpai_mask = tmask;
+    r.n_settlements = 1;
+    for (int s = 0; s < 4; s++) r.deltas[0][s] = d[s];
+    r.honba_component[0] = 0;
+    r.deposits_claimed[0] = 0;
+    end_result();
+    advance_round((tmask >> g.dealer()) & 1, false);
+  }
+  // engine.py:764-779
+  RS_COLD void apply_tsumo(int seat) {
+    const Hand h = load_hand(S, e, seat);
+    WinIn w;
+    win_input(seat, h, g.drawn, true, false, w);
+    Reading rd;
+    score_win(w, rd, false);
+    begin_result(RS_RES_TSUMO);
+    rs_result_rec& r = result();
+    int deltas[4], hc;
+    settle(true, rd.base, g.dealer(), seat, -1, g.honba, g.deposits, deltas, &hc);
+    for (int s = 0; s < 4; s++) { r.deltas[0][s] = deltas[s]; g.scores[s] += deltas[s]; }
+    r.honba_component[0] = hc;
+    r.deposits_claimed[0] = g.deposits;
+    r.n_winners = 1;
+    r.winners[0] = (int8_t)seat;
+    r.n_settlements = 1;
+    write_win(0, rd, w);
+    g.deposits = 0;
+    emit(EV_TSUMO, seat, g.drawn);
+    end_result();
+    const int dealer = g.dealer();
+    advance_round(seat == dealer, seat != dealer);
+  }
+  // engine.py:782-807
+  RS_COLD void apply_ron_wins() {
+    const int loser = g.call_from;
+    const int nw = g.rn();
+    int w4[3];
+    for (int i = 0; i < nw; i++) w4[i] = g.rseat(i);
+    for (int i = 1; i < nw; i++)
+      for (int j = i; j > 0 && ((w4[j - 1] - loser) & 3) > ((w4[j] - loser) & 3); j--) {
+        const int t = w4[j]; w4[j] = w4[j - 1]; w4[j - 1] = t;
+      }
+    begin_result(RS_RES_RON);
+    rs_result_rec& r = result();
+    r.loser = loser;
+    r.n_winners = nw;
+    r.n_settlements = nw;
+    const int dealer = g.dealer();
+    bool dealer_won = false;
+    for (int i = 0; i < nw; i++) {
+      const int seat = w4[i];
+      r.winners[i] = (int8_t)seat;
+      const Hand h = load_hand(S, e, seat);
+      WinIn w;
+      win_input(seat, h, g.call_tile, false, g.call_chankan, w);
+      Reading rd;
+      score_win(w, rd, false);
+      const int honba = i == 0 ? g.honba : 0, dep = i == 0 ? g.deposits : 0;
+      int deltas[4], hc;
+      settle(false, rd.base, dealer, seat, loser, honba, dep, deltas, &hc);
+      for (int s = 0; s < 4; s++) { r.deltas[i][s] = deltas[s]; g.scores[s] += deltas[s]; }
+      r.honba_component[i] = hc;
+      r.deposits_claimed[i] = dep;
+      write_win(i, rd, w);
+      emit(EV_RON, seat, g.call_tile);
+      if (seat == dealer) dealer_won = true;
+    }
+    g.deposits = 0;
+    end_result();
+    clear_call();
+    advance_round(dealer_won, !dealer_won);
+  }
+
+  // ------------------------------------------------------ call handling
+  // engine.py:580-591
+  RS_HD void mark_passed_furiten(int kind, int discarder) {
+    for (int s = 0; s < 4; s++) {
+      if (s == discarder) continue;
+      const uint32_t inf = info(s);
+      if (hi::shanten(inf) == 0 && ((waits(s) >> kind) & 1))
+        set_info(s, hi::riichi(inf) ? hi::set_perm(inf, 1) : hi::set_temp(inf, 1));
+    }
+  }
+  // engine.py:594-615
+  RS_HD void discard_stands() {
+    const int discarder = g.phase == PH_CALL ? g.call_from : g.actor;
+    g.phase = PH_ACT;
+    const uint32_t inf = info(discarder);
+    if (hi::riichi(inf) && hi::riichi_index(inf) == hi::nriver(inf) - 1 && !hi::ippatsu(inf)) {
+      set_info(discarder, hi::set_ippatsu(inf, 1));
+      if (C.rule == RS_RULE_RED && hi::riichi(info(0)) && hi::riichi(info(1)) && hi::riichi(info(2)) &&
+          hi::riichi(info(3))) {
+        emit(EV_DRAW_END, discarder, -1);
+        abort_kyoku(RS_RES_ABORT_FOUR_RIICHI);
+        return;
+      }
+    }
+    if (g.four_kan_pending && C.rule == RS_RULE_RED) {
+      emit(EV_DRAW_END, discarder, -1);
+      abort_kyoku(RS_RES_ABORT_FOUR_KAN);
+      return;
+    }
+    g.call_tile = -1;
+    g.call_from = -1;
+    g.queue = 0;
+    g.rons = 0;
+    if (g.live() == 0) { exhaustive(); return; }
+    draw((discarder + 1) & 3);
+  }
+  // engine.py:489-495
+  RS_HD void reveal_pending_dora() {
+    while (g.pending_dora > 0 && g.dora_count < 5) {
+      g.dora_count++;
+      g.pending_dora--;
+      emit(EV_NEW_DORA, -1, wall(122 + 2 * (g.dora_count - 1)));
+    }
+    g.pending_dora = 0;
+  }
+  RS_HD bool can_chi(int s, int kind) const {
+    const int n = kind % 9;
+    return (n <= 6 && count_of(s, kind + 1) && count_of(s, kind + 2)) ||
+           (n >= 1 && n <= 7 && count_of(s, kind - 1) && count_of(s, kind + 1)) ||
+           (n >= 2 && count_of(s, kind - 2) && count_of(s, kind - 1));
+  }
+  // engine.py:498-531
+  RS_HD bool begin_call_phase(int tile, int discarder, bool chankan) {
+    const int kind = tile >> 2;
+    int qs[5], qt[5], n = 0;
+    for (int off = 1; off <= 3; off++) {
+      const int s = (discarder + off) & 3;
+      if (can_ron(s, tile, chankan)) { qs[n] = s; qt[n] = ST_RON; n++; }
+    }
+    if (!chankan && g.live() >= 1) {
+      for (int off = 1; off <= 3; off++) {
+        const int s = (discarder + off) & 3;
+        if (hi::riichi(info(s))) continue;
+        if (count_of(s, kind) >= 2) { qs[n] = s; qt[n] = ST_PONKAN; n++; }
+      }
+      const int s = (discarder + 1) & 3;
+      if (kind < 27 && !hi::riichi(info(s)) && can_chi(s, kind)) { qs[n] = s; qt[n] = ST_CHI; n++; }
+    }
+    if (!n) return false;
+    g.phase = PH_CALL;
+    g.call_tile = tile;
+    g.call_from = discarder;
+    g.qset(n, qs, qt);
+    g.rons = 0;
+    g.call_chankan = chankan;
+    g.actor = qs[0];
+    return true;
+  }
+
+  // engine.py:447-455
+  RS_HD int pick_discard(const Hand& h, int action) const {
+    const int kind = action < 34 ? action : (action == 34 ? 4 : action == 35 ? 13 : 22);
+    const bool want_red = action >= 34;
+    const bool red_rule = C.rule == RS_RULE_RED;
+    if (g.drawn >= 0 && (g.drawn >> 2) == kind && (red_rule && is_red_tile(g.drawn)) == want_red) return g.drawn;
+    uint32_t nib = h.nibble(kind);
+    if (red_rule && red_index_of_kind(kind) >= 0) nib = want_red ? (nib & 1u) : (nib & ~1u);
+    return 4 * kind + ctz32(nib);
+  }
+  // engine.py:458-486
+  RS_HD void apply_discard(int seat, int action) {
+    Hand h = load_hand(S, e, seat);
+    const int tile = pick_discard(h, action);
+    const bool tsumogiri = tile == g.drawn;
+    const bool declaring = g.riichi_pending;
+    int riichi_val = hi::riichi(h.info), riichi_index = hi::riichi_index(h.info);
+    const int nriver = hi::nriver(h.info);
+    if (declaring) {
+      riichi_val = (nriver == 0 && !g.any_call_made) ? 2 : 1;
+      riichi_index = nriver;
+      g.riichi_pending = 0;
+    }
+    int ipp = hi::ippatsu(h.info);
+    if (hi::riichi(h.info) && !declaring && ipp) ipp = 0;
+    S.river[at(seat * RS_MAX_RIVER + nriver)] =
+        (uint16_t)(tile | ((tsumogiri ? RS_RIVER_TSUMOGIRI : 0) | (declaring ? RS_RIVER_RIICHI : 0)) << 8);
+    S.hrkind[at(seat)] |= 1ull << (tile >> 2);
+    hand_take(T, h, tile);
+    h.info = hi::set_nriver(h.info, nriver + 1);
+    h.info = hi::set_riichi(h.info, riichi_val);
+    h.info = hi::set_riichi_index(h.info, riichi_index);
+    h.info = hi::set_ippatsu(h.info, ipp);
+    finish_hand(T, h);
+    store_hand(S, e, seat, h);
+    g.drawn = -1;
+    g.rinshan_pending = 0;
+    emit(EV_DISCARD, seat, tile);
+    reveal_pending_dora();
+    if (!begin_call_phase(tile, seat, false)) {
+      mark_passed_furiten(tile >> 2, seat);
+      discard_stands();
+    }
+  }
+
+  RS_HD void clear_all_ippatsu() {
+    for (int s = 0; s < 4; s++) {
+      const uint32_t inf = info(s);
+      if (hi::ippatsu(inf)) set_info(s, hi::set_ippatsu(inf, 0));
+    }
+  }
+  // engine.py:631-636
+  RS_HD void mark_called_tile() {
+    const int d = g.call_from;
+    const int idx = hi::nriver(info(d)) - 1;
+    uint16_t& rt = S.river[at(d * RS_MAX_RIVER + idx)];
+    rt = (uint16_t)(rt | (RS_RIVER_CALLED << 8));
+  }
+  // engine.py:639-644
+  RS_COLD void check_four_kans() {
+    if (C.rule != RS_RULE_RED) return;
+    int total = 0, seats = 0;
+    for (int s = 0; s < 4; s++) {
+      const int nm = hi::nmelds(info(s));
+      int c = 0;
+      for (int i = 0; i < 4; i++)
+        if (i < nm && mi::type(meld_info(s, i)) >= M_KAN_OPEN) c++;
+      total += c;
+      if (c) seats++;
+    }
+    if (total == 4 && seats >= 2) g.four_kan_pending = 1;
+  }
+  // append a meld of sorted ids (melds.py:17-34)
+  RS_HD void add_meld(int seat, Hand& h, int type, const int* ids, int nids, int called, int from) {
+    int t[4];
+    for (int i = 0; i < nids; i++) t[i] = ids[i];
+    for (int i = 1; i < nids; i++)
+      for (int j = i; j > 0 && t[j - 1] > t[j]; j--) { const int x = t[j]; t[j] = t[j - 1]; t[j - 1] = x; }
+    uint32_t packed = 0;
+    for (int i = 0; i < nids; i++) packed |= (uint32_t)t[i] << (8 * i);
+    const int nm = hi::nmelds(h.info);
+    S.mtiles[at(seat * 4 + nm)] = packed;
+    S.minfo[at(seat * 4 + nm)] = mi::make(type, nids, from, called);
+    h.info = hi::set_nmelds(h.info, nm + 1);
+  }
+  // engine.py:696-702
+  RS_HD void finish_meld_call(int seat) {
+    g.any_call_made = 1;
+    clear_all_ippatsu();
+    g.phase = PH_ACT;
+    g.actor = seat;
+    g.drawn = -1;
+    g.rinshan_pending = 0;
+  }
+  // engine.py:647-693 (pon / chi / open kan share the claim prologue)
+  RS_COLD void apply_claim(int seat, int action) {
+    const int kind = g.call_tile >> 2;
+    mark_passed_furiten(kind, g.call_from);
+    mark_called_tile();
+    Hand h = load_hand(S, e, seat);
+    int ids[4], n = 0;
+    if (action == A_PON || action == A_KAN_OPEN) {
+      const int need = action == A_PON ? 2 : 3;
+      uint32_t nib = h.nibble(kind);
+      for (int j = 0; j < need; j++) { const int b = ctz32(nib); nib &= nib - 1; ids[n++] = 4 * kind + b; }
+    } else {
+      int k0, k1;
+      if (action == A_CHI_LOW) { k0 = kind + 1; k1 = kind + 2; }
+      else if (action == A_CHI_MID) { k0 = kind - 1; k1 = kind + 1; }
+      else { k0 = kind - 2; k1 = kind - 1; }
+      ids[n++] = h.lowest_of_kind(k0);
+      ids[n++] = h.lowest_of_kind(k1);
+    }
+    for (int j = 0; j < n; j++) hand_take(T, h, ids[j]);
+    ids[n] = g.call_tile;
+    const int type = action == A_PON ? M_PON : (action == A_KAN_OPEN ? M_KAN_OPEN : M_CHI);
+    add_meld(seat, h, type, ids, n + 1, g.call_tile, g.call_from);
+    finish_hand(T, h);
+    const int called = g.call_tile;
+    if (action == A_KAN_OPEN) {
+      store_hand(S, e, seat, h);
+      g.any_call_made = 1;
+      clear_all_ippatsu();
+      g.pending_dora++;
+      emit(EV_KAN_OPEN, seat, called);
+      clear_call();
+      check_four_kans();
+      h.info = info(seat);  // ippatsu may have been cleared above
+      rinshan_draw(seat, h);
+      return;
+    }
+    store_hand(S, e, seat, h);
+    finish_meld_call(seat);
+    emit(action == A_PON ? EV_PON : EV_CHI, seat, called);
+    clear_call();
+  }
+  // engine.py:714-727
+  RS_COLD void apply_closed_kan(int seat, int kind) {
+    Hand h = load_hand(S, e, seat);
+    int ids[4];
+    uint32_t nib = h.nibble(kind);
+    for (int j = 0; j < 4; j++) { ids[j] = 4 * kind + ctz32(nib); nib &= nib - 1; }
+    for (int j = 0; j < 4; j++) hand_take(T, h, ids[j]);
+    add_meld(seat, h, M_KAN_CLOSED, ids, 4, -1, -1);
+    finish_hand(T, h);
+    store_hand(S, e, seat, h);
+    g.any_call_made = 1;
+    clear_all_ippatsu();
+    g.dora_count = g.dora_count + 1 < 5 ? g.dora_count + 1 : 5;
+    emit(EV_KAN_CLOSED, seat, ids[0]);
+    emit(EV_NEW_DORA, -1, wall(122 + 2 * (g.dora_count - 1)));
+    check_four_kans();
+    h.info = info(seat);
+    rinshan_draw(seat, h);
+  }
+  // engine.py:742-758
+  RS_COLD void complete_added_kan(int seat, int kind) {
+    Hand h = load_hand(S, e, seat);
+    const int tile = h.lowest_of_kind(kind);
+    const int nm = hi::nmelds(h.info);
+    for (int i = 0; i < 4; i++)
+      if (i < nm) {
+        const uint32_t mf = meld_info(seat, i), mt = meld_tiles(seat, i);
+        if (mi::type(mf) == M_PON && ((mt & 255) >> 2) == kind) {
+          int t[4] = {(int)(mt & 255), (int)((mt >> 8) & 255), (int)((mt >> 16) & 255), tile};
+          for (int a = 1; a < 4; a++)
+            for (int b = a; b > 0 && t[b - 1] > t[b]; b--) { const int x = t[b]; t[b] = t[b - 1]; t[b - 1] = x; }
+          S.mtiles[at(seat * 4 + i)] = (uint32_t)t[0] | ((uint32_t)t[1] << 8) | ((uint32_t)t[2] << 16) |
+                                       ((uint32_t)t[3] << 24);
+          S.minfo[at(seat * 4 + i)] = mi::make(M_KAN_ADDED, 4, mi::from(mf), mi::called(mf));
+        }
+      }
+    hand_take(T, h, tile);
+    finish_hand(T, h);
+    store_hand(S, e, seat, h);
+    g.any_call_made = 1;
+    clear_all_ippatsu();
+    g.pending_dora++;
+    clear_call();
+    check_four_kans();
+    h.info = info(seat);
+    rinshan_draw(seat, h);
+  }
+  // engine.py:730-739
+  RS_COLD void apply_added_kan(int seat, int kind) {
+    const int tile = 4 * kind + ctz32((S.hmask[at(seat * 5 + (kind >> 3))] >> ((kind & 7) * 4)) & 0xFu);
+    emit(EV_KAN_ADDED, seat, tile);
+    if (begin_call_phase(tile, seat, true)) { g.kakan_kind = kind; return; }
+    mark_passed_furiten(kind, seat);
+    complete_added_kan(seat, kind);
+  }
+  // engine.py:561-577
+  RS_COLD void resolve_call_end() {
+    if (g.rn()) {
+      if (g.rn() >= 3 && C.rule == RS_RULE_RED) {
+        emit(EV_DRAW_END, g.call_from, -1);
+        abort_kyoku(RS_RES_ABORT_TRIPLE_RON);
+        return;
+      }
+      apply_ron_wins();
+      return;
+    }
+    mark_passed_furiten(g.call_tile >> 2, g.call_from);
+    if (g.call_chankan) {
+      const int seat = g.call_from;
+      g.call_chankan = 0;
+      g.phase = PH_ACT;
+      g.actor = seat;
+      complete_added_kan(seat, g.kakan_kind);
+      return;
+    }
+    discard_stands();
+  }
+  // engine.py:552-558
+  RS_HD void advance_call_queue() {
+    if (g.rn()) {
+      int qs[5], qt[5], n = 0;
+      for (int i = 0; i < g.qn(); i++)
+        if (g.qstage(i) == ST_RON) { qs[n] = g.qseat(i); qt[n] = ST_RON; n++; }
+      g.qset(n, qs, qt);
+    }
+    if (g.qn()) { g.actor = g.qseat(0); return; }
+    resolve_call_end();
+  }
+  // engine.py:534-549
+  RS_HD void apply_call_action(int action) {
+    const int seat = g.qseat(0);
+    g.qpop();
+    if (action == A_RON) { g.rpush(seat); advance_call_queue(); }
+    else if (action == A_PASS) advance_call_queue();
+    else apply_claim(seat, action);
+  }
+  // engine.py:425-444
+  RS_HD void apply_turn_action(int action) {
+    const int seat = g.actor;
+    if (action <= 36) apply_discard(seat, action);
+    else if (action == A_RIICHI) {
+      g.scores[seat] -= 1000;
+      g.deposits += 1;
+      g.riichi_pending = 1;
+      emit(EV_RIICHI, seat, -1);
+    } else if (action == A_TSUMO) apply_tsumo(seat);
+    else if (action < A_KAN_ADDED) apply_closed_kan(seat, action - A_KAN_CLOSED);
+    else if (action < A_PASS) apply_added_kan(seat, action - A_KAN_ADDED);
+    else {
+      emit(EV_DRAW_END, seat, -1);
+      abort_kyoku(RS_RES_ABORT_NINE);
+    }
+  }
+
+  // ------------------------------------------------------------ env API
+  RS_HD void store_legal(const Mask115& m) const {
+    for (int i = 0; i < 4; i++) S.legal[at(i)] = m.m[i];
+  }
+  RS_HD Mask115 load_legal() const {
+    Mask115 m;
+    for (int i = 0; i < 4; i++) m.m[i] = S.legal[at(i)];
+    return m;
+  }
+  // env/core.py:81-94 (_wrap, _terminal_rewards) -> rewards into r[4]
+  RS_HD void wrap(float* r) {
+    g.current_player = g.actor;
+    g.env_terminated = g.terminated;
+    g.env_truncated = g.truncated;
+    if (g.terminated || g.truncated) terminal_rewards(r);
+    else r[0] = r[1] = r[2] = r[3] = 0.0f;
+  }
+  RS_HD void terminal_rewards(float* r) const {
+    if (C.reward_scheme == RS_REWARD_RANK) {
+      const double RR[4] = {1.0, 0.333, -0.333, -1.0};
+      for (int s = 0; s < 4; s++) {
+        int rank = 0;
+        for (int t = 0; t < 4; t++)
+          if (g.scores[t] > g.scores[s] || (g.scores[t] == g.scores[s] && t < s)) rank++;
+        r[s] = (float)RR[rank];
+      }
+    } else {
+      for (int s = 0; s < 4; s++) r[s] = (float)((double)(g.scores[s] - 25000) / 25000.0);
+    }
+  }
+  // current rewards of a stored env (illegal penalty or terminal rewards)
+  RS_HD void current_rewards(float* r) const {
+    if (g.status & RS_STATUS_ILLEGAL) {
+      r[0] = r[1] = r[2] = r[3] = 0.0f;
+      r[g.current_player] = C.illegal_penalty;
+    } else if (g.env_terminated || g.env_truncated) {
+      terminal_rewards(r);
+    } else {
+      r[0] = r[1] = r[2] = r[3] = 0.0f;
+    }
+  }
+
+  // engine.py:128-136 + core.py:97-98: fresh game from `seed`; rollout
+  // keys (env_key, policy stream, resets) are preserved
+  RS_HD void init_game(uint64_t seed, float* r) {
+    g.phase = PH_ACT; g.actor = 0; g.kyoku = 0;
+    g.terminated = g.truncated = 0;
+    g.env_terminated = g.env_truncated = 0;
+    g.status = 0;
+    g.honba = g.deposits = g.repeats = g.n_results = 0;
+    g.step_count = 0;
+    g.events_len = 0;
+    g.drawn = -1;
+    for (int s = 0; s < 4; s++) g.scores[s] = 25000;
+    g.rng_key = mix64(seed);
+    g.rng_counter = 0;
+    start_kyoku();
+    Mask115 m;
+    compute_legal(m);
+    store_legal(m);
+    wrap(r);
+  }
+
+  // env/core.py:101-110 + engine.py:405-422.  Returns status bits.
+  RS_HD int step(int action, Mask115& legal, float* r) {
+    if (g.env_terminated || g.env_truncated) {
+      // contract violation: nothing changes (core.py:103-104 raises)
+      legal.clear();
+      current_rewards(r);
+      return RS_STATUS_CONTRACT;
+    }
+    legal = load_legal();
+    if (action < 0 || action >= RS_NUM_ACTIONS || !legal.test(action)) {
+      r[0] = r[1] = r[2] = r[3] = 0.0f;
+      r[g.current_player] = C.illegal_penalty;
+      g.env_terminated = 1;
+      g.env_truncated = 0;
+      g.status = RS_STATUS_ILLEGAL;
+      legal.clear();
+      // the stored mask is the game's cached list; the env view is empty
+      return RS_STATUS_ILLEGAL;
+    }
+    g.status = 0;
+    g.step_count++;
+    if (g.phase == PH_CALL) apply_call_action(action);
+    else apply_turn_action(action);
+    if (!g.terminated && g.step_count >= (uint32_t)C.max_steps) g.truncated = 1;
+    compute_legal(legal);
+    store_legal(legal);
+    wrap(r);
+    return 0;
+  }
+
+  // env/policies.py:17-22 over the env-view mask
+  RS_HD int random_action(const Mask115& legal) {
+    const int n = legal.count();
+    g.policy_counter++;
+    const int i = (int)randbelow_from(stream_value(g.policy_key, g.policy_counter), (uint32_t)n);
+    return legal.nth(i);
+  }
+};
+
+}  // namespace rs

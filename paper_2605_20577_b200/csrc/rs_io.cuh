@@ -1,0 +1,285 @@
+// rs_io.cuh — observation encoding, trajectory digest and record import /
+// export for one env (device code, also usable on host memory).
+#pragma once
+
+#include "rs_engine.cuh"
+
+namespace rs {
+
+// tile token (observe.py:153-156)
+RS_HD int tile_token(int t, int rule) {
+  if (rule == RS_RULE_RED && is_red_tile(t)) return 34 + red_index_of_kind(t >> 2);
+  return t >> 2;
+}
+RS_HD int ev_token(int type) { return type <= 8 ? type : type - 1; }  // win events merge (observe.py:136-149)
+
+// observe(state, seat) (observe.py:191-234), written into slot `o` of `obs`
+RS_HD void write_obs(const Engine& E, int seat, const rs_obs_out& obs, int64_t o) {
+  const Soa& S = E.S;
+  const Game& g = E.g;
+  const int rule = E.C.rule;
+  const Hand h = load_hand(S, E.e, seat);
+  if (obs.hand_tokens) {
+    uint8_t* ht = obs.hand_tokens + o * 14;
+    int n = 0;
+    for (int k = 0; k < 34; k++) {
+      int c = h.count(k);
+      if (rule == RS_RULE_RED && red_index_of_kind(k) >= 0 && h.has(4 * k)) c--;
+      for (int j = 0; j < c; j++) ht[n++] = (uint8_t)k;
+    }
+    if (rule == RS_RULE_RED) {
+      if (h.has(16)) ht[n++] = 34;
+      if (h.has(52)) ht[n++] = 35;
+      if (h.has(88)) ht[n++] = 36;
+    }
+    for (; n < 14; n++) ht[n] = 37;
+  }
+  if (obs.event_tokens) {
+    // 64 x (type, rel actor, token), oldest first, padded (0,0,37)
+    uint32_t words[48];
+    const uint32_t len = g.events_len;
+    const int cnt = len < 64 ? (int)len : 64, pad = 64 - cnt;
+    for (int i = 0; i < 48; i++) words[i] = 0;
+    for (int i = 0; i < 64; i++) {
+      uint32_t ty = 0, rel = 0, tok = 37;
+      if (i >= pad) {
+        const uint32_t idx = (len - (uint32_t)cnt + (uint32_t)(i - pad)) & 63u;
+        const uint32_t ev = S.events[(size_t)idx * S.n + E.e];
+        const int type = ev & 15, actor = (int)((ev >> 4) & 7) - 1, tile = (int)((ev >> 7) & 255) - 1;
+        ty = (uint32_t)ev_token(type);
+        rel = actor >= 0 ? (uint32_t)((actor - seat) & 3) : 0u;
+        if (type == EV_DRAW && actor != seat) tok = 37;
+        else tok = tile >= 0 ? (uint32_t)tile_token(tile, rule) : 37u;
+      }
+      const int b = 3 * i;
+      words[b >> 2] |= ty << (8 * (b & 3));
+      words[(b + 1) >> 2] |= rel << (8 * ((b + 1) & 3));
+      words[(b + 2) >> 2] |= tok << (8 * ((b + 2) & 3));
+    }
+    uint4* dst = reinterpret_cast<uint4*>(obs.event_tokens + o * 192);
+#pragma unroll
+    for (int i = 0; i < 12; i++) dst[i] = make_uint4(words[4 * i], words[4 * i + 1], words[4 * i + 2], words[4 * i + 3]);
+  }
+  if (obs.shanten) obs.shanten[o] = (int8_t)hi::shanten(h.info);
+  if (obs.scores)
+    for (int i = 0; i < 4; i++) {
+      const int s = g.scores[(seat + i) & 3];
+      obs.scores[o * 4 + i] = (int16_t)(s >= 0 ? s / 100 : -((-s + 99) / 100));  // floor division
+    }
+  if (obs.round_wind) obs.round_wind[o] = (uint8_t)g.round_wind();
+  if (obs.seat_wind) obs.seat_wind[o] = (uint8_t)g.seat_wind(seat);
+  if (obs.kyoku) obs.kyoku[o] = (uint8_t)g.kyoku;
+  if (obs.honba) obs.honba[o] = (int16_t)g.honba;
+  if (obs.deposits) obs.deposits[o] = (int16_t)g.deposits;
+  if (obs.dora_tokens)
+    for (int i = 0; i < 5; i++)
+      obs.dora_tokens[o * 5 + i] = (uint8_t)(i < g.dora_count ? tile_token(E.wall(122 + 2 * i), rule) : 37);
+  if (obs.live_wall) obs.live_wall[o] = (uint8_t)g.live();
+  if (obs.riichi_flags)
+    for (int i = 0; i < 4; i++) obs.riichi_flags[o * 4 + i] = (uint8_t)(hi::riichi(E.info((seat + i) & 3)) ? 1 : 0);
+}
+
+// trajectory digest (identical to oracle/mjoracle.c orc_digest_step)
+RS_HD uint64_t dfold(uint64_t d, uint64_t w) { return mix64((d ^ w) + GOLDEN); }
+RS_HD uint64_t digest_step(uint64_t d, int action, const Engine& E, const Mask115& view, const float* r) {
+  const Game& g = E.g;
+  d = dfold(d, (uint64_t)(uint32_t)action);
+  d = dfold(d, (uint64_t)(uint32_t)g.current_player | ((uint64_t)g.env_terminated << 8) |
+                   ((uint64_t)g.env_truncated << 9) | ((uint64_t)g.phase << 12) |
+                   ((uint64_t)(uint32_t)g.kyoku << 16) | ((uint64_t)(uint32_t)g.honba << 24) |
+                   ((uint64_t)(uint32_t)g.deposits << 40));
+  d = dfold(d, (uint64_t)view.m[0] | ((uint64_t)view.m[1] << 32));
+  d = dfold(d, (uint64_t)view.m[2] | ((uint64_t)view.m[3] << 32));
+  for (int s = 0; s < 4; s += 2)
+    d = dfold(d, (uint64_t)(uint32_t)g.scores[s] | ((uint64_t)(uint32_t)g.scores[s + 1] << 32));
+  uint32_t rb[4];
+  for (int i = 0; i < 4; i++) {
+    union { float f; uint32_t u; } cv;
+    cv.f = r[i];
+    rb[i] = cv.u;
+  }
+  d = dfold(d, (uint64_t)rb[0] | ((uint64_t)rb[1] << 32));
+  d = dfold(d, (uint64_t)rb[2] | ((uint64_t)rb[3] << 32));
+  uint64_t sh = 0;
+  for (int s = 0; s < 4; s++) sh |= (uint64_t)(uint8_t)(int8_t)hi::shanten(E.info(s)) << (8 * s);
+  sh |= (uint64_t)g.events_len << 32;
+  d = dfold(d, sh);
+  d = dfold(d, (uint64_t)(uint32_t)g.cursor | ((uint64_t)(uint32_t)g.kan_draws << 8) |
+                   ((uint64_t)(uint32_t)g.dora_count << 16) | ((uint64_t)g.step_count << 32));
+  return d;
+}
+
+// projection record (include/rinshan.h rs_env_rec) of env e
+RS_COLD void export_env(Engine& E, const Cfg& C, rs_env_rec& r) {
+  const Soa& S = E.S;
+  E.load();
+  const Game& g = E.g;
+  r.abi_version = RS_ABI_VERSION;
+  r.cfg.rule = C.rule; r.cfg.mode = C.mode; r.cfg.reward_scheme = C.reward_scheme;
+  r.cfg.illegal_penalty = C.illegal_penalty; r.cfg.max_steps = C.max_steps; r.cfg.kazoe = C.kazoe;
+  r.cfg.double_yakuman = C.double_yakuman; r.cfg.agari_yame = C.agari_yame; r.cfg.renchan_cap = C.renchan_cap;
+  for (int i = 0; i < 136; i++) r.wall[i] = (uint8_t)E.wall(i);
+  r.cursor = g.cursor; r.kan_draws = g.kan_draws; r.dora_count = g.dora_count;
+  for (int s = 0; s < 4; s++) {
+    const Hand h = load_hand(S, E.e, s);
+    rs_hand_rec& hr = r.hands[s];
+    int n = 0;
+    for (int t = 0; t < 136; t++)
+      if (h.has(t)) hr.concealed[n++] = (uint8_t)t;
+    for (int i = n; i < 14; i++) hr.concealed[i] = 0;
+    hr.n_concealed = (uint8_t)n;
+    const int nm = hi::nmelds(h.info);
+    hr.n_melds = (uint8_t)nm;
+    for (int i = 0; i < 4; i++) {
+      rs_meld_rec& m = hr.melds[i];
+      const uint32_t mf = i < nm ? E.meld_info(s, i) : 0u, mt = i < nm ? E.meld_tiles(s, i) : 0u;
+      m.type = (int8_t)(i < nm ? mi::type(mf) : 0);
+      m.n_tiles = (int8_t)(i < nm ? mi::ntiles(mf) : 0);
+      m.from_seat = (int8_t)(i < nm ? mi::from(mf) : 0);
+      m.pad0 = 0;
+      for (int j = 0; j < 4; j++) m.tiles[j] = (uint8_t)(j < m.n_tiles ? (mt >> (8 * j)) & 255 : 0);
+      m.called_tile = (int16_t)(i < nm ? mi::called(mf) : 0);
+      m.pad1 = 0;
+    }
+    const int nr = hi::nriver(h.info);
+    for (int i = 0; i < RS_MAX_RIVER; i++) {
+      const uint16_t v = i < nr ? S.river[(size_t)(s * RS_MAX_RIVER + i) * S.n + E.e] : (uint16_t)0;
+      hr.river_tile[i] = (uint8_t)(v & 255);
+      hr.river_flags[i] = (uint8_t)(v >> 8);
+    }
+    hr.n_river = nr;
+    hr.riichi = (int8_t)hi::riichi(h.info);
+    hr.riichi_index = (int8_t)hi::riichi_index(h.info);
+    hr.ippatsu = (int8_t)hi::ippatsu(h.info);
+    hr.temp_furiten = (int8_t)hi::temp(h.info);
+    hr.perm_furiten = (int8_t)hi::perm(h.info);
+    hr.shanten = (int8_t)hi::shanten(h.info);
+    hr.pad = 0;
+    hr.waits = h.waits;
+  }
+  for (int s = 0; s < 4; s++) r.scores[s] = g.scores[s];
+  r.kyoku = g.kyoku; r.honba = g.honba; r.deposits = g.deposits; r.repeats = g.repeats;
+  r.phase = g.phase; r.actor = g.actor; r.drawn = g.drawn;
+  r.riichi_pending = g.riichi_pending; r.rinshan_pending = g.rinshan_pending;
+  r.call_tile = g.call_tile; r.call_from = g.call_from;
+  r.n_queue = g.qn();
+  for (int i = 0; i < RS_MAX_QUEUE; i++) {
+    r.queue_seat[i] = (int8_t)(i < r.n_queue ? g.qseat(i) : 0);
+    r.queue_stage[i] = (int8_t)(i < r.n_queue ? g.qstage(i) : 0);
+  }
+  r.n_rons = g.rn();
+  for (int i = 0; i < 4; i++) r.rons[i] = (int8_t)(i < r.n_rons ? g.rseat(i) : 0);
+  r.call_chankan = g.call_chankan; r.kakan_kind = g.kakan_kind; r.pending_dora = g.pending_dora;
+  r.four_kan_pending = g.four_kan_pending; r.any_call_made = g.any_call_made;
+  r.rng_key = g.rng_key; r.rng_counter = g.rng_counter;
+  r.step_count = (int32_t)g.step_count; r.terminated = g.terminated; r.truncated = g.truncated;
+  r.events_len = (int32_t)g.events_len;
+  const int cnt = g.events_len < 64 ? (int)g.events_len : 64;
+  for (int i = 0; i < 64; i++) {
+    if (i < cnt) {
+      const uint32_t idx = (g.events_len - (uint32_t)cnt + (uint32_t)i) & 63u;
+      const uint32_t ev = S.events[(size_t)idx * S.n + E.e];
+      r.events[i][0] = (int16_t)(ev & 15);
+      r.events[i][1] = (int16_t)((int)((ev >> 4) & 7) - 1);
+      r.events[i][2] = (int16_t)((int)((ev >> 7) & 255) - 1);
+    } else {
+      r.events[i][0] = r.events[i][1] = r.events[i][2] = 0;
+    }
+  }
+  r.n_results = g.n_results;
+  r.last_result = S.results[E.e];
+  const bool done = g.env_terminated || g.env_truncated;
+  for (int i = 0; i < 4; i++) r.legal_mask[i] = done ? 0u : S.legal[(size_t)i * S.n + E.e];
+  r.current_player = g.current_player;
+  r.env_terminated = g.env_terminated;
+  r.env_truncated = g.env_truncated;
+  r.status = g.status;
+  float rw[4];
+  E.current_rewards(rw);
+  for (int i = 0; i < 4; i++) r.rewards[i] = rw[i];
+  r.env_key = g.env_key; r.policy_key = g.policy_key; r.policy_counter = g.policy_counter;
+  r.resets = (int32_t)g.resets;
+  r.pad = 0;
+}
+
+// crafted states (tests/engine_helpers.py:58-105 craft()); shanten / waits /
+// codes / classes are derived, the legal mask is recomputed
+RS_COLD void import_env(Engine& E, const rs_env_rec& r) {
+  const Soa& S = E.S;
+  const Tabs& T = E.T;
+  Game& g = E.g;
+  uint8_t* w = S.wall + (size_t)E.e * WALL_STRIDE;
+  for (int i = 0; i < 136; i++) w[i] = r.wall[i];
+  for (int i = 136; i < WALL_STRIDE; i++) w[i] = 0;
+  g.cursor = r.cursor; g.kan_draws = r.kan_draws; g.dora_count = r.dora_count;
+  for (int s = 0; s < 4; s++) {
+    const rs_hand_rec& hr = r.hands[s];
+    Hand h;
+    h.w0 = h.w1 = h.w2 = h.w3 = h.w4 = 0;
+    h.cm = h.cp = h.cs = h.cz = 0;
+    for (int i = 0; i < hr.n_concealed; i++) {
+      const int t = hr.concealed[i], k = t >> 2;
+      h.set_word(t >> 5, h.word(t >> 5) | (1u << (t & 31)));
+      h.set_code(kind_suit(k), h.code(kind_suit(k)) + kind_pow(k));
+    }
+    h.cls = class_of(T, 0, h.cm) | (class_of(T, 1, h.cp) << 8) | (class_of(T, 2, h.cs) << 16) |
+            (class_of(T, 3, h.cz) << 24);
+    uint32_t inf = 0;
+    inf = hi::set_riichi(inf, hr.riichi);
+    inf = hi::set_riichi_index(inf, hr.riichi_index);
+    inf = hi::set_ippatsu(inf, hr.ippatsu);
+    inf = hi::set_temp(inf, hr.temp_furiten);
+    inf = hi::set_perm(inf, hr.perm_furiten);
+    inf = hi::set_nmelds(inf, hr.n_melds);
+    inf = hi::set_nriver(inf, hr.n_river);
+    inf = hi::set_nconc(inf, hr.n_concealed);
+    h.info = inf;
+    for (int i = 0; i < hr.n_melds; i++) {
+      const rs_meld_rec& m = hr.melds[i];
+      uint32_t packed = 0;
+      for (int j = 0; j < m.n_tiles; j++) packed |= (uint32_t)m.tiles[j] << (8 * j);
+      S.mtiles[(size_t)(s * 4 + i) * S.n + E.e] = packed;
+      S.minfo[(size_t)(s * 4 + i) * S.n + E.e] = mi::make(m.type, m.n_tiles, m.from_seat, m.called_tile);
+    }
+    uint64_t rk = 0;
+    for (int i = 0; i < hr.n_river; i++) {
+      S.river[(size_t)(s * RS_MAX_RIVER + i) * S.n + E.e] =
+          (uint16_t)(hr.river_tile[i] | ((uint16_t)hr.river_flags[i] << 8));
+      rk |= 1ull << (hr.river_tile[i] >> 2);
+    }
+    S.hrkind[(size_t)s * S.n + E.e] = rk;
+    finish_hand(T, h);
+    store_hand(S, E.e, s, h);
+  }
+  for (int s = 0; s < 4; s++) g.scores[s] = r.scores[s];
+  g.kyoku = r.kyoku; g.honba = r.honba; g.deposits = r.deposits; g.repeats = r.repeats;
+  g.phase = r.phase; g.actor = r.actor; g.drawn = r.drawn;
+  g.riichi_pending = r.riichi_pending; g.rinshan_pending = r.rinshan_pending;
+  g.call_tile = r.call_tile; g.call_from = r.call_from;
+  int qs[5], qt[5];
+  const int nq = r.n_queue < 5 ? r.n_queue : 5;
+  for (int i = 0; i < nq; i++) { qs[i] = r.queue_seat[i]; qt[i] = r.queue_stage[i]; }
+  g.qset(nq, qs, qt);
+  g.rons = 0;
+  for (int i = 0; i < r.n_rons && i < 3; i++) g.rpush(r.rons[i]);
+  g.call_chankan = r.call_chankan; g.kakan_kind = r.kakan_kind; g.pending_dora = r.pending_dora;
+  g.four_kan_pending = r.four_kan_pending; g.any_call_made = r.any_call_made;
+  g.rng_key = r.rng_key; g.rng_counter = (uint32_t)r.rng_counter;
+  g.step_count = (uint32_t)r.step_count; g.terminated = r.terminated; g.truncated = r.truncated;
+  const int cnt = r.events_len < 64 ? r.events_len : 64;
+  g.events_len = (uint32_t)(r.events_len - cnt);
+  for (int i = 0; i < cnt; i++) E.emit(r.events[i][0], r.events[i][1], r.events[i][2]);
+  g.n_results = r.n_results;
+  S.results[E.e] = r.last_result;
+  g.env_key = r.env_key; g.policy_key = r.policy_key; g.policy_counter = r.policy_counter;
+  g.resets = (uint32_t)r.resets;
+  g.status = 0;
+  Mask115 m;
+  E.compute_legal(m);
+  E.store_legal(m);
+  float rw[4];
+  E.wrap(rw);
+  E.store();
+}
+
+}  // namespace rs

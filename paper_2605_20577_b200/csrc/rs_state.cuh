@@ -1,0 +1,172 @@
+// rs_state.cuh — structure-of-arrays env state in HBM.
+//
+// One thread owns one env; every per-env field is stored field-major
+// ([field][n]) so the 32 lanes of a warp touch 32 consecutive elements of
+// the same field: one 128-byte line per u32 field access.  The hot game
+// scalars are bit-packed into a 64-byte header (4 x uint4 loaded and stored
+// once per step); per-seat hands are 136-bit tile-id sets (5 words) with
+// their base-5 suit codes, table classes and a packed flag word.
+//
+// Field inventory follows the reference GameState / HandState
+// (engine/types.py:72-158); `bytes_per_env()` is the S of the roofline.
+#pragma once
+
+#include <stdint.h>
+
+#include "../../include/rinshan.h"
+#include "rs_common.cuh"
+
+namespace rs {
+
+constexpr int WALL_STRIDE = 144;  // 136 tiles padded to 9 x 16 B
+
+struct Soa {
+  int n;
+  uint4* hdr;        // [4][n]   packed game scalars (see Game::load/store)
+  int4* scores;      // [n]
+  uint8_t* wall;     // [n][144] shuffled tile ids
+  uint32_t* hmask;   // [4 seat][5][n] concealed tile-id set
+  uint32_t* hcode;   // [4 seat][4][n] base-5 codes m, p, s, z
+  uint32_t* hcls;    // [4 seat][n]    table class per suit (4 x u8)
+  uint32_t* hinfo;   // [4 seat][n]    packed HandState flags
+  uint64_t* hwaits;  // [4 seat][n]    34-bit wait mask (13-form tenpai)
+  uint64_t* hrkind;  // [4 seat][n]    kinds present in the river
+  uint32_t* mtiles;  // [4 seat][4 meld][n] tile ids (4 x u8)
+  uint32_t* minfo;   // [4 seat][4 meld][n] type | n | from | called
+  uint16_t* river;   // [4 seat][40][n] tile | flags << 8
+  uint16_t* events;  // [64][n] ring: type | (actor+1) << 4 | (tile+1) << 7
+  uint32_t* legal;   // [4][n] env-view legal mask
+  rs_result_rec* results;  // [n] last kyoku result (written at kyoku end)
+};
+
+inline int64_t bytes_per_env() {
+  return 4 * 16 + 16 + WALL_STRIDE + 4 * 5 * 4 + 4 * 4 * 4 + 4 * 4 + 4 * 4 + 4 * 8 + 4 * 8 +
+         4 * 4 * 4 + 4 * 4 * 4 + 4 * RS_MAX_RIVER * 2 + RS_EVENT_WINDOW * 2 + 4 * 4 +
+         (int64_t)sizeof(rs_result_rec);
+}
+
+struct Cfg {
+  int rule, mode, reward_scheme;
+  float illegal_penalty;
+  int max_steps, kazoe, double_yakuman, agari_yame, renchan_cap;
+};
+
+// --------------------------------------------------------- packed fields
+// HandState flag word (hinfo)
+namespace hi {
+RS_HD int riichi(uint32_t x) { return x & 3; }
+RS_HD int riichi_index(uint32_t x) { return (int)((x >> 2) & 63) - 1; }
+RS_HD int ippatsu(uint32_t x) { return (x >> 8) & 1; }
+RS_HD int temp(uint32_t x) { return (x >> 9) & 1; }
+RS_HD int perm(uint32_t x) { return (x >> 10) & 1; }
+RS_HD int shanten(uint32_t x) { return (int)((x >> 11) & 15) - 1; }
+RS_HD int nmelds(uint32_t x) { return (x >> 15) & 7; }
+RS_HD int nriver(uint32_t x) { return (x >> 18) & 63; }
+RS_HD int nconc(uint32_t x) { return (x >> 24) & 15; }
+RS_HD uint32_t set(uint32_t x, int shift, int width, int v) {
+  uint32_t m = ((1u << width) - 1u) << shift;
+  return (x & ~m) | (((uint32_t)v << shift) & m);
+}
+RS_HD uint32_t set_riichi(uint32_t x, int v) { return set(x, 0, 2, v); }
+RS_HD uint32_t set_riichi_index(uint32_t x, int v) { return set(x, 2, 6, v + 1); }
+RS_HD uint32_t set_ippatsu(uint32_t x, int v) { return set(x, 8, 1, v); }
+RS_HD uint32_t set_temp(uint32_t x, int v) { return set(x, 9, 1, v); }
+RS_HD uint32_t set_perm(uint32_t x, int v) { return set(x, 10, 1, v); }
+RS_HD uint32_t set_shanten(uint32_t x, int v) { return set(x, 11, 4, v + 1); }
+RS_HD uint32_t set_nmelds(uint32_t x, int v) { return set(x, 15, 3, v); }
+RS_HD uint32_t set_nriver(uint32_t x, int v) { return set(x, 18, 6, v); }
+RS_HD uint32_t set_nconc(uint32_t x, int v) { return set(x, 24, 4, v); }
+}  // namespace hi
+
+// meld info word
+namespace mi {
+RS_HD int type(uint32_t x) { return x & 7; }
+RS_HD int ntiles(uint32_t x) { return (x >> 3) & 7; }
+RS_HD int from(uint32_t x) { return (int)((x >> 6) & 7) - 1; }
+RS_HD int called(uint32_t x) { return (int)((x >> 9) & 255) - 1; }
+RS_HD uint32_t make(int type, int n, int from, int called) {
+  return (uint32_t)type | ((uint32_t)n << 3) | ((uint32_t)(from + 1) << 6) | ((uint32_t)(called + 1) << 9);
+}
+}  // namespace mi
+
+// ------------------------------------------------------- game scalars
+// GameState scalars (engine/types.py:124-158) + env wrapper + rollout keys,
+// unpacked into registers for the duration of one step.
+struct Game {
+  int phase, actor, kyoku;
+  int riichi_pending, rinshan_pending, call_chankan, four_kan_pending, any_call_made;
+  int terminated, truncated, env_terminated, env_truncated;
+  int pending_dora, dora_count, kan_draws, call_from, current_player, status;
+  int drawn, call_tile, kakan_kind, cursor;
+  uint32_t queue;  // n (3b) | 5 x (seat 2b, stage 2b) from bit 3
+  uint32_t rons;   // n (2b) | 3 x seat (2b) from bit 2
+  int honba, deposits, repeats, n_results;
+  uint32_t step_count, events_len, rng_counter, resets;
+  uint64_t rng_key, policy_counter, policy_key, env_key;
+  int scores[4];
+
+  RS_HD void unpack(uint4 a, uint4 b, uint4 c, uint4 d, int4 sc) {
+    uint32_t x = a.x;
+    phase = x & 3; actor = (x >> 2) & 3; kyoku = (x >> 4) & 7;
+    riichi_pending = (x >> 7) & 1; rinshan_pending = (x >> 8) & 1; call_chankan = (x >> 9) & 1;
+    four_kan_pending = (x >> 10) & 1; any_call_made = (x >> 11) & 1; terminated = (x >> 12) & 1;
+    truncated = (x >> 13) & 1; env_terminated = (x >> 14) & 1; env_truncated = (x >> 15) & 1;
+    pending_dora = (x >> 16) & 7; dora_count = (x >> 19) & 7; kan_draws = (x >> 22) & 7;
+    call_from = (int)((x >> 25) & 7) - 1; current_player = (x >> 28) & 3; status = (x >> 30) & 3;
+    drawn = (int)(a.y & 255) - 1; call_tile = (int)((a.y >> 8) & 255) - 1;
+    kakan_kind = (int)((a.y >> 16) & 255) - 1; cursor = (a.y >> 24) & 255;
+    queue = a.z & 0x7FFFFFu; rons = a.z >> 23;
+    honba = a.w & 255; deposits = (a.w >> 8) & 255; repeats = (a.w >> 16) & 255; n_results = a.w >> 24;
+    step_count = b.x; events_len = b.y; rng_counter = b.z; resets = b.w;
+    rng_key = (uint64_t)c.x | ((uint64_t)c.y << 32);
+    policy_counter = (uint64_t)c.z | ((uint64_t)c.w << 32);
+    policy_key = (uint64_t)d.x | ((uint64_t)d.y << 32);
+    env_key = (uint64_t)d.z | ((uint64_t)d.w << 32);
+    scores[0] = sc.x; scores[1] = sc.y; scores[2] = sc.z; scores[3] = sc.w;
+  }
+  RS_HD void pack(uint4& a, uint4& b, uint4& c, uint4& d, int4& sc) const {
+    a.x = (uint32_t)phase | ((uint32_t)actor << 2) | ((uint32_t)kyoku << 4) | ((uint32_t)riichi_pending << 7) |
+          ((uint32_t)rinshan_pending << 8) | ((uint32_t)call_chankan << 9) | ((uint32_t)four_kan_pending << 10) |
+          ((uint32_t)any_call_made << 11) | ((uint32_t)terminated << 12) | ((uint32_t)truncated << 13) |
+          ((uint32_t)env_terminated << 14) | ((uint32_t)env_truncated << 15) | ((uint32_t)pending_dora << 16) |
+          ((uint32_t)dora_count << 19) | ((uint32_t)kan_draws << 22) | ((uint32_t)(call_from + 1) << 25) |
+          ((uint32_t)current_player << 28) | ((uint32_t)status << 30);
+    a.y = (uint32_t)(drawn + 1) | ((uint32_t)(call_tile + 1) << 8) | ((uint32_t)(kakan_kind + 1) << 16) |
+          ((uint32_t)cursor << 24);
+    a.z = (queue & 0x7FFFFFu) | (rons << 23);
+    a.w = (uint32_t)honba | ((uint32_t)deposits << 8) | ((uint32_t)repeats << 16) | ((uint32_t)n_results << 24);
+    b.x = step_count; b.y = events_len; b.z = rng_counter; b.w = resets;
+    c.x = (uint32_t)rng_key; c.y = (uint32_t)(rng_key >> 32);
+    c.z = (uint32_t)policy_counter; c.w = (uint32_t)(policy_counter >> 32);
+    d.x = (uint32_t)policy_key; d.y = (uint32_t)(policy_key >> 32);
+    d.z = (uint32_t)env_key; d.w = (uint32_t)(env_key >> 32);
+    sc.x = scores[0]; sc.y = scores[1]; sc.z = scores[2]; sc.w = scores[3];
+  }
+
+  // call queue helpers (engine/types.py:143-144)
+  RS_HD int qn() const { return queue & 7; }
+  RS_HD int qseat(int i) const { return (queue >> (3 + 4 * i)) & 3; }
+  RS_HD int qstage(int i) const { return (queue >> (5 + 4 * i)) & 3; }
+  RS_HD void qset(int n, const int* seats, const int* stages) {
+    uint32_t q = (uint32_t)n;
+    for (int i = 0; i < n; i++) q |= ((uint32_t)seats[i] | ((uint32_t)stages[i] << 2)) << (3 + 4 * i);
+    queue = q;
+  }
+  RS_HD void qpop() {
+    int n = qn();
+    uint32_t entries = (queue >> 7) & 0xFFFFu;
+    queue = (uint32_t)(n - 1) | (entries << 3);
+  }
+  RS_HD int rn() const { return rons & 3; }
+  RS_HD int rseat(int i) const { return (rons >> (2 + 2 * i)) & 3; }
+  RS_HD void rpush(int s) {
+    int n = rn();
+    rons = (rons & ~3u) | (uint32_t)(n + 1) | ((uint32_t)s << (2 + 2 * n));
+  }
+  RS_HD int dealer() const { return kyoku % 4; }
+  RS_HD int round_wind() const { return kyoku >= 4 ? 28 : 27; }
+  RS_HD int seat_wind(int s) const { return 27 + ((s - dealer()) & 3); }
+  RS_HD int live() const { return 122 - kan_draws - cursor; }
+};
+
+}  // namespace rs

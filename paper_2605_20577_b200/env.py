@@ -1,0 +1,221 @@
+"""Batched Pgx-style env on B200: `BatchEnv`.
+
+The batched counterpart of the reference env facade (env/core.py:41-110,
+env/observe.py:159-234, env/policies.py:17-22, bench/runner.py:25-33,97-121).
+State lives on the GPU in the library's structure-of-arrays; the tensors
+exposed here (legal mask, current player, rewards, terminated, truncated,
+observations) are torch CUDA tensors written in place by the kernels.
+Every method is stream-ordered on the current torch stream; nothing is
+copied to the host on the step path.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import torch
+
+from . import abi
+from ._lib import check, lib
+
+_RULES = {"red": abi.RULE_RED, "no-red": abi.RULE_NO_RED}
+_MODES = {"single": abi.MODE_SINGLE, "east": abi.MODE_EAST, "half": abi.MODE_HALF}
+_SCHEMES = {"score_delta": abi.REWARD_SCORE_DELTA, "rank": abi.REWARD_RANK}
+
+
+@dataclass(frozen=True)
+class EnvConfig:
+    """reference env/core.py:41-61 (plus GameConfig flags, engine/types.py:49-57)"""
+
+    rule: str = "red"
+    mode: str = "single"
+    illegal_penalty: float = -1.0
+    reward_scheme: str = "score_delta"
+    max_steps: int = 10_000
+    kazoe: bool = False
+    double_yakuman: bool = False
+    agari_yame: bool = True
+    renchan_cap: int = 32
+
+    def __post_init__(self):
+        if self.rule not in _RULES:
+            raise ValueError(f"bad rule {self.rule!r}")
+        if self.mode not in _MODES:
+            raise ValueError(f"bad mode {self.mode!r}")
+        if self.reward_scheme not in _SCHEMES:
+            raise ValueError(f"bad reward scheme {self.reward_scheme!r}")
+        if self.illegal_penalty > 0:
+            raise ValueError("illegal penalty must be <= 0")
+
+    def to_abi(self) -> abi.rs_config:
+        return abi.rs_config(
+            rule=_RULES[self.rule], mode=_MODES[self.mode], reward_scheme=_SCHEMES[self.reward_scheme],
+            illegal_penalty=self.illegal_penalty, max_steps=self.max_steps, kazoe=int(self.kazoe),
+            double_yakuman=int(self.double_yakuman), agari_yame=int(self.agari_yame),
+            renchan_cap=self.renchan_cap)
+
+
+def _ptr(t: torch.Tensor | None) -> int | None:
+    return None if t is None else t.data_ptr()
+
+
+class Observations(dict):
+    """Observation tensors keyed like Observation.to_dict() (docs/formats.md:32-52)."""
+
+
+def alloc_observations(n: int, device, slots: int | None = None) -> Observations:
+    lead = (n,) if slots is None else (slots, n)
+    kw = dict(device=device)
+    return Observations(
+        hand_tokens=torch.empty(*lead, 14, dtype=torch.uint8, **kw),
+        event_tokens=torch.empty(*lead, 64, 3, dtype=torch.uint8, **kw),
+        shanten=torch.empty(*lead, dtype=torch.int8, **kw),
+        scores=torch.empty(*lead, 4, dtype=torch.int16, **kw),
+        round_wind=torch.empty(*lead, dtype=torch.uint8, **kw),
+        seat_wind=torch.empty(*lead, dtype=torch.uint8, **kw),
+        kyoku=torch.empty(*lead, dtype=torch.uint8, **kw),
+        honba=torch.empty(*lead, dtype=torch.int16, **kw),
+        deposits=torch.empty(*lead, dtype=torch.int16, **kw),
+        dora_indicator_tokens=torch.empty(*lead, 5, dtype=torch.uint8, **kw),
+        live_wall=torch.empty(*lead, dtype=torch.uint8, **kw),
+        riichi_flags=torch.empty(*lead, 4, dtype=torch.uint8, **kw),
+    )
+
+
+def obs_struct(o: Observations) -> abi.rs_obs_out:
+    return abi.rs_obs_out(
+        hand_tokens=_ptr(o["hand_tokens"]), event_tokens=_ptr(o["event_tokens"]),
+        shanten=_ptr(o["shanten"]), scores=_ptr(o["scores"]), round_wind=_ptr(o["round_wind"]),
+        seat_wind=_ptr(o["seat_wind"]), kyoku=_ptr(o["kyoku"]), honba=_ptr(o["honba"]),
+        deposits=_ptr(o["deposits"]), dora_tokens=_ptr(o["dora_indicator_tokens"]),
+        live_wall=_ptr(o["live_wall"]), riichi_flags=_ptr(o["riichi_flags"]))
+
+
+class BatchEnv:
+    """`n` independent envs on one GPU (the batched drop-in of mjsim.init/step/observe)."""
+
+    def __init__(self, n: int, config: EnvConfig | None = None, device: str | torch.device = "cuda",
+                 **kw):
+        if config is None:
+            config = EnvConfig(**kw)
+        elif kw:
+            raise TypeError("pass either config or keyword fields")
+        self.config = config
+        self.n = int(n)
+        self.device = torch.device(device)
+        if self.device.type != "cuda":
+            raise ValueError("BatchEnv runs on a CUDA device (there is no CPU fallback)")
+        if self.device.index is None:
+            self.device = torch.device("cuda", torch.cuda.current_device())
+        self._L = lib()
+        self._cfg = config.to_abi()
+        h = C.c_void_p()
+        check(self._L.rs_create(C.byref(h), self.n, C.byref(self._cfg), self.device.index), "rs_create")
+        self._h = h
+        dev = self.device
+        self.legal_action_mask = torch.zeros(self.n, abi.NUM_ACTIONS, dtype=torch.bool, device=dev)
+        self.legal_bits = torch.zeros(self.n, 4, dtype=torch.int32, device=dev)
+        self.current_player = torch.zeros(self.n, dtype=torch.int8, device=dev)
+        self.rewards = torch.zeros(self.n, 4, dtype=torch.float32, device=dev)
+        self.terminated = torch.zeros(self.n, dtype=torch.bool, device=dev)
+        self.truncated = torch.zeros(self.n, dtype=torch.bool, device=dev)
+        self.status = torch.zeros(self.n, dtype=torch.uint8, device=dev)
+        self._out = abi.rs_step_out(
+            legal_mask=_ptr(self.legal_action_mask), legal_bits=_ptr(self.legal_bits),
+            current_player=_ptr(self.current_player), rewards=_ptr(self.rewards),
+            terminated=_ptr(self.terminated), truncated=_ptr(self.truncated), status=_ptr(self.status))
+        self._obs = None
+
+    # -- lifecycle ---------------------------------------------------------
+    def close(self):
+        if getattr(self, "_h", None):
+            self._L.rs_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _stream(self) -> int:
+        return torch.cuda.current_stream(self.device).cuda_stream
+
+    @property
+    def state_bytes(self) -> int:
+        return int(self._L.rs_state_bytes(self._h))
+
+    # -- env API -----------------------------------------------------------
+    def init(self, seeds: torch.Tensor | None = None, *, seed: int | None = None,
+             index_base: int = 0) -> "BatchEnv":
+        """init(seed) for every env.  Either explicit u64 game seeds (a CUDA
+        int64 tensor holding the bit patterns), or bench seeding: env i uses
+        env_game_seed(seed, index_base + i) and env_policy_state(seed,
+        index_base + i) (reference bench/runner.py:25-33)."""
+        if seeds is not None:
+            seeds = seeds.to(device=self.device, dtype=torch.int64).contiguous()
+            if seeds.numel() != self.n:
+                raise ValueError("need one seed per env")
+            check(self._L.rs_init(self._h, seeds.data_ptr(), C.byref(self._out), self._stream()), "rs_init")
+        else:
+            s = 0 if seed is None else int(seed) & ((1 << 64) - 1)
+            check(self._L.rs_init_indexed(self._h, s, int(index_base), C.byref(self._out), self._stream()),
+                  "rs_init_indexed")
+        return self
+
+    def step(self, actions: torch.Tensor) -> "BatchEnv":
+        """step(state, action) for every env (env/core.py:101-110): illegal ids
+        end the episode with the penalty at the offender; stepping a finished
+        env sets RS_STATUS_CONTRACT in `status` and changes nothing."""
+        actions = actions.to(device=self.device, dtype=torch.int32).contiguous()
+        if actions.numel() != self.n:
+            raise ValueError("need one action per env")
+        check(self._L.rs_step(self._h, actions.data_ptr(), C.byref(self._out), self._stream()), "rs_step")
+        return self
+
+    def observe(self, seats: torch.Tensor | None = None, out: Observations | None = None) -> Observations:
+        """observe(state, seat) for every env; `seats` defaults to each env's
+        current player (env/observe.py:191-234)."""
+        if out is None:
+            if self._obs is None:
+                self._obs = alloc_observations(self.n, self.device)
+            out = self._obs
+        st = obs_struct(out)
+        sp = None
+        if seats is not None:
+            seats = seats.to(device=self.device, dtype=torch.int8).contiguous()
+            sp = seats.data_ptr()
+        check(self._L.rs_observe(self._h, sp, C.byref(st), self._stream()), "rs_observe")
+        return out
+
+    def random_actions(self, out: torch.Tensor | None = None) -> torch.Tensor:
+        """random_policy over each env's legal list from its policy stream
+        (env/policies.py:17-22); -1 for finished envs."""
+        if out is None:
+            out = torch.empty(self.n, dtype=torch.int32, device=self.device)
+        check(self._L.rs_policy_random(self._h, out.data_ptr(), self._stream()), "rs_policy_random")
+        return out
+
+    def rollout(self, steps: int, obs: Observations | None = None, obs_slots: int = 0,
+                actions_log: torch.Tensor | None = None, stats: torch.Tensor | None = None,
+                digests: torch.Tensor | None = None) -> "BatchEnv":
+        """Fused `steps` x {auto-reset, random policy, step, observe} per env
+        in one kernel (bench/runner.py:97-121).  stats: int64[3] CUDA tensor
+        (steps, games_completed, illegal) accumulated; digests: int64[n]."""
+        st = obs_struct(obs) if obs is not None else None
+        check(self._L.rs_rollout(
+            self._h, int(steps), C.byref(st) if st is not None else None, int(obs_slots if obs is not None else 0),
+            _ptr(actions_log), _ptr(stats), _ptr(digests), C.byref(self._out), self._stream()), "rs_rollout")
+        return self
+
+    # -- projection records (parity harness) ----------------------------------
+    def export(self, i: int) -> abi.rs_env_rec:
+        torch.cuda.current_stream(self.device).synchronize()
+        r = abi.rs_env_rec()
+        check(self._L.rs_export_env(self._h, int(i), C.byref(r)), "rs_export_env")
+        return r
+
+    def load(self, i: int, rec: abi.rs_env_rec) -> None:
+        torch.cuda.current_stream(self.device).synchronize()
+        check(self._L.rs_import_env(self._h, int(i), C.byref(rec)), "rs_import_env")

@@ -1,0 +1,133 @@
+"""CUDA path vs the CPU oracle (bit-exact).  Needs a B200: `pytest -m gpu`."""
+
+from __future__ import annotations
+
+import random
+
+import pytest
+import torch
+
+from oracle import mjoracle as O
+from paper_2605_20577_b200.env import BatchEnv, EnvConfig
+from paritylib import diff, projection
+
+pytestmark = pytest.mark.gpu
+
+RULES = ("no-red", "red")
+
+
+def _oracle_cfg(cfg: EnvConfig):
+    return O.make_config(rule=cfg.rule, mode=cfg.mode, illegal_penalty=cfg.illegal_penalty,
+                         reward_scheme=cfg.reward_scheme, max_steps=cfg.max_steps)
+
+
+@pytest.mark.parametrize("rule", RULES)
+@pytest.mark.parametrize("mode", ("single", "east", "half"))
+def test_fused_rollout_digests_match_oracle(rule, mode):
+    """fused rollout (auto-reset + random policy + step) == oracle run_shard,
+    env by env, through the 64-bit trajectory digest."""
+    n, steps = (2048, 300) if mode == "single" else (256, 900)
+    cfg = EnvConfig(rule=rule, mode=mode)
+    env = BatchEnv(n, cfg).init(seed=11, index_base=0)
+    digests = torch.zeros(n, dtype=torch.int64, device="cuda")
+    stats = torch.zeros(3, dtype=torch.int64, device="cuda")
+    env.rollout(steps, digests=digests, stats=stats)
+    torch.cuda.synchronize()
+    games, ref = O.run_shard(_oracle_cfg(cfg), 11, 0, n, steps, digests=True)
+    got = [int(x) & ((1 << 64) - 1) for x in digests.cpu().tolist()]
+    bad = [i for i in range(n) if got[i] != ref[i]]
+    assert not bad, f"{len(bad)} envs diverge, first {bad[:8]}"
+    st = stats.cpu().tolist()
+    assert st[0] == n * steps and st[1] == games
+
+
+@pytest.mark.parametrize("rule", RULES)
+def test_rollout_chunks_equal_one_launch(rule):
+    """K steps in one launch == K/3 steps in three launches (state fully in HBM between)."""
+    n = 512
+    cfg = EnvConfig(rule=rule)
+    a = BatchEnv(n, cfg).init(seed=5)
+    b = BatchEnv(n, cfg).init(seed=5)
+    da = torch.zeros(n, dtype=torch.int64, device="cuda")
+    db = torch.zeros(n, dtype=torch.int64, device="cuda")
+    a.rollout(240, digests=da)
+    for _ in range(3):
+        b.rollout(80, digests=db)
+    torch.cuda.synchronize()
+    assert torch.equal(da, db)
+
+
+def _lockstep(rule, mode, n, steps, policy, seed=3):
+    cfg = EnvConfig(rule=rule, mode=mode)
+    ocfg = _oracle_cfg(cfg)
+    seeds = [O.env_game_seed(seed, i) for i in range(n)]
+    env = BatchEnv(n, cfg).init(torch.tensor([s - (1 << 64) if s >= 1 << 63 else s for s in seeds]))
+    oes = [O.OracleEnv(ocfg).init(s) for s in seeds]
+    rng = random.Random(seed)
+    for t in range(steps):
+        for i in range(n):
+            a, b = projection(env.export(i)), projection(oes[i].record())
+            d = diff(a, b)
+            assert not d, f"env {i} step {t}: {d[:6]}"
+        acts = []
+        for i in range(n):
+            r = oes[i].record()
+            if r.env_terminated or r.env_truncated:
+                acts.append(0)
+                continue
+            legal = oes[i].legal()
+            if policy == "heuristic":
+                acts.append(oes[i].heuristic_policy())
+            else:  # biased towards rare actions + occasional illegal probes
+                rare = [x for x in legal if x >= 37 and x != 113]
+                if rare and rng.random() < 0.8:
+                    acts.append(rng.choice(rare))
+                elif rng.random() < 0.01:
+                    acts.append(rng.randrange(115))
+                else:
+                    acts.append(rng.choice(legal))
+        env.step(torch.tensor(acts, dtype=torch.int32))
+        for i in range(n):
+            oes[i].step(acts[i])
+        # observation of the current player, env by env
+        if t % 7 == 0:
+            obs = env.observe()
+            torch.cuda.synchronize()
+            for i in range(n):
+                cp = oes[i].record().current_player
+                o = oes[i].observe(cp)
+                assert obs["hand_tokens"][i].tolist() == o["hand_tokens"]
+                assert obs["event_tokens"][i].tolist() == o["event_tokens"]
+                assert int(obs["shanten"][i]) == o["shanten"]
+                assert obs["scores"][i].tolist() == o["scores"]
+                assert obs["dora_indicator_tokens"][i].tolist() == o["dora_indicator_tokens"]
+                assert obs["riichi_flags"][i].tolist() == o["riichi_flags"]
+                assert [int(obs[k][i]) for k in ("round_wind", "seat_wind", "kyoku", "honba", "deposits", "live_wall")] == \
+                    [o[k] for k in ("round_wind", "seat_wind", "kyoku", "honba", "deposits", "live_wall")]
+
+
+@pytest.mark.parametrize("rule", RULES)
+def test_lockstep_heuristic_records(rule):
+    _lockstep(rule, "east", 16, 160, "heuristic")
+
+
+@pytest.mark.parametrize("rule", RULES)
+def test_lockstep_biased_records(rule):
+    _lockstep(rule, "single", 16, 120, "biased")
+
+
+def test_step_tensors_match_records():
+    n = 64
+    env = BatchEnv(n, EnvConfig(rule="red")).init(seed=1)
+    for _ in range(50):
+        env.step(env.random_actions())
+    torch.cuda.synchronize()
+    for i in range(0, n, 9):
+        r = env.export(i)
+        bits = [int(x) & 0xFFFFFFFF for x in env.legal_bits[i].tolist()]
+        assert bits == [int(x) for x in r.legal_mask]
+        mask = env.legal_action_mask[i].tolist()
+        assert mask == [bool((bits[a >> 5] >> (a & 31)) & 1) for a in range(115)]
+        assert int(env.current_player[i]) == r.current_player
+        assert env.rewards[i].tolist() == [float(x) for x in r.rewards]
+        assert bool(env.terminated[i]) == bool(r.env_terminated)
