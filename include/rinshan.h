@@ -20,6 +20,7 @@
  *   rs_policy_random  env/policies.py:17-22    random_policy(legal, rng)
  *   rs_rollout        bench/runner.py:97-121   run_shard.one_pass (auto-reset +
  *                                              random_policy + step), fused
+ *   rs_autoreset      bench/runner.py:107-109  auto-reset of finished envs
  *   rs_export_env     engine/state.py:191-242  serialize_state (projection record)
  *   rs_import_env     tests/engine_helpers.py:58-105 craft() (crafted states)
  *
@@ -236,6 +237,8 @@ int rs_tables_shanten_std(uint32_t cm, uint32_t cp, uint32_t cs, uint32_t cz,
 int rs_create(rs_handle** out, int64_t n_envs, const rs_config* cfg, int32_t device);
 int rs_destroy(rs_handle* h);
 int64_t rs_num_envs(const rs_handle* h);
+/* h != NULL: bytes of the handle's device allocation; h == NULL: canonical
+ * bytes of one env's game state (the S of the roofline B_step = 2S+O+M+R+A) */
 int64_t rs_state_bytes(const rs_handle* h);
 
 /* seeds_dev: device u64[n] game seeds; policy streams are derived from them */
@@ -245,6 +248,20 @@ int rs_init(rs_handle* h, const uint64_t* seeds_dev, const rs_step_out* out, voi
 int rs_init_indexed(rs_handle* h, uint64_t seed, int64_t index_base,
                     const rs_step_out* out, void* stream);
 int rs_step(rs_handle* h, const int32_t* actions_dev, const rs_step_out* out, void* stream);
+
+/* rs_step fused with what an actor loop does next, in the same kernel:
+ *   RS_STEP_AUTORESET  finished envs start their next game (auto-reset,
+ *                      bench/runner.py:107-109); rewards / terminated /
+ *                      truncated / status describe the transition while the
+ *                      legal mask, current player and observation belong to
+ *                      the new game (Pgx auto_reset convention)
+ *   RS_STEP_OBSERVE    observe(current player) into `obs` (observe.py:191)
+ * next_actions_dev (may be NULL) receives random_policy's next action from
+ * each env's policy stream (policies.py:17-22), -1 for finished envs. */
+#define RS_STEP_AUTORESET 1
+#define RS_STEP_OBSERVE 2
+int rs_step_ex(rs_handle* h, const int32_t* actions_dev, int32_t flags, const rs_step_out* out,
+               const rs_obs_out* obs, int32_t* next_actions_dev, void* stream);
 /* seats_dev: device int8[n] or NULL for each env's current player */
 int rs_observe(rs_handle* h, const int8_t* seats_dev, const rs_obs_out* obs, void* stream);
 /* random policy over each env's legal list using its policy stream */
@@ -261,6 +278,10 @@ int rs_policy_random(rs_handle* h, int32_t* actions_dev, void* stream);
 int rs_rollout(rs_handle* h, int32_t steps, const rs_obs_out* obs, int32_t obs_slots,
                int16_t* actions_log, rs_rollout_stats* stats_dev, uint64_t* digests_dev,
                const rs_step_out* out, void* stream);
+
+/* auto-reset (bench/runner.py:107-109): every finished env starts its next
+ * game from env_game_seed(seed, index, resets + 1); outputs for all envs */
+int rs_autoreset(rs_handle* h, const rs_step_out* out, void* stream);
 
 int rs_export_env(rs_handle* h, int64_t env, rs_env_rec* out);
 int rs_import_env(rs_handle* h, int64_t env, const rs_env_rec* in);

@@ -2208,3 +2208,60 @@ int64_t orc_run_shard(const rs_config* cfg, uint64_t seed, int64_t idx0, int64_t
   orc_env_free(e);
   return games;
 }
+
+/* ------------------------------------------------- batched CPU baseline */
+
+/* A persistent shard of envs stepped like bench/runner.py:97-121 one_pass
+ * (auto-reset + random policy + step) plus observe(current player), the
+ * same work per env step as the GPU bench step. */
+struct orc_batch {
+  rs_config cfg;
+  int64_t n;
+  orc_env** envs;
+  orc_obs obs;
+};
+
+orc_batch* orc_batch_new(const rs_config* cfg, uint64_t seed, int64_t idx0, int64_t n) {
+  orc_tables_build();
+  orc_batch* b = (orc_batch*)calloc(1, sizeof(orc_batch));
+  b->cfg = *cfg;
+  b->n = n;
+  b->envs = (orc_env**)calloc((size_t)n, sizeof(orc_env*));
+  for (int64_t j = 0; j < n; j++) {
+    orc_env* e = orc_env_new();
+    e->env_key = orc_derive_key(orc_seed_key(seed), (uint64_t)(idx0 + j));
+    e->policy_key = orc_derive_key(e->env_key, 1);
+    e->policy_counter = 0;
+    e->resets = 0;
+    orc_env_init(e, cfg, orc_derive_key(e->env_key, 2));
+    b->envs[j] = e;
+  }
+  return b;
+}
+
+void orc_batch_free(orc_batch* b) {
+  if (!b) return;
+  for (int64_t j = 0; j < b->n; j++) orc_env_free(b->envs[j]);
+  free(b->envs);
+  free(b);
+}
+
+int64_t orc_batch_step(orc_batch* b, int32_t steps, int32_t observe) {
+  int64_t games = 0;
+  for (int64_t j = 0; j < b->n; j++) {
+    orc_env* e = b->envs[j];
+    for (int t = 0; t < steps; t++) {
+      if (e->env_terminated || e->env_truncated) {
+        e->resets++;
+        orc_env_init(e, &b->cfg, orc_derive_key(e->env_key, 2 + (uint64_t)e->resets));
+      }
+      uint64_t kc[2] = {e->policy_key, e->policy_counter};
+      const int a = orc_random_policy(e, kc);
+      e->policy_counter = kc[1];
+      orc_env_step(e, a);
+      if (observe) orc_env_observe(e, e->current_player, &b->obs);
+      if (e->env_terminated || e->env_truncated) games++;
+    }
+  }
+  return games;
+}

@@ -74,6 +74,9 @@ def lib():
             L.orc_run_shard.restype = C.c_int64
             L.orc_run_shard.argtypes = [vp, u64, C.c_int64, C.c_int64, i32, i32, vp]
             L.orc_digest_step.restype = u64; L.orc_digest_step.argtypes = [u64, C.c_int, vp]
+            L.orc_batch_new.restype = vp; L.orc_batch_new.argtypes = [vp, u64, C.c_int64, C.c_int64]
+            L.orc_batch_free.argtypes = [vp]
+            L.orc_batch_step.restype = C.c_int64; L.orc_batch_step.argtypes = [vp, i32, i32]
             _lib = L
     return _lib
 
@@ -322,3 +325,21 @@ def score(ctx: orc_winctx):
     if not ok:
         return None
     return w, [int(order[i]) for i in range(norder.value)]
+
+
+class OracleBatch:
+    """Persistent shard [idx0, idx0+n) of bench-seeded envs (CPU baseline)."""
+
+    def __init__(self, config: abi.rs_config, seed: int, idx0: int, n: int):
+        self._L = lib()
+        self.config = config
+        self._p = self._L.orc_batch_new(C.byref(config), seed, idx0, n)
+
+    def step(self, steps: int = 1, observe: bool = True) -> int:
+        return self._L.orc_batch_step(self._p, steps, 1 if observe else 0)
+
+    def __del__(self):
+        try:
+            self._L.orc_batch_free(self._p)
+        except Exception:
+            pass

@@ -25,8 +25,8 @@ INCLUDE = PKG_DIR.parent / "include" / "rinshan.h"
 SYMBOLS = (
     "rs_last_error", "rs_abi_version", "rs_tables_build", "rs_tables_load", "rs_tables_blob",
     "rs_tables_crc", "rs_tables_info", "rs_tables_shanten_std", "rs_create", "rs_destroy",
-    "rs_num_envs", "rs_state_bytes", "rs_init", "rs_init_indexed", "rs_step", "rs_observe",
-    "rs_policy_random", "rs_rollout", "rs_export_env", "rs_import_env", "rs_record_sizes",
+    "rs_num_envs", "rs_state_bytes", "rs_init", "rs_init_indexed", "rs_step", "rs_step_ex", "rs_observe",
+    "rs_policy_random", "rs_rollout", "rs_autoreset", "rs_export_env", "rs_import_env", "rs_record_sizes",
 )
 
 _lib = None
@@ -81,9 +81,11 @@ def lib():
         L.rs_init.argtypes = [vp, vp, vp, vp]
         L.rs_init_indexed.argtypes = [vp, u64, i64, vp, vp]
         L.rs_step.argtypes = [vp, vp, vp, vp]
+        L.rs_step_ex.argtypes = [vp, vp, i32, vp, vp, vp, vp]
         L.rs_observe.argtypes = [vp, vp, vp, vp]
         L.rs_policy_random.argtypes = [vp, vp, vp]
         L.rs_rollout.argtypes = [vp, i32, vp, i32, vp, vp, vp, vp, vp]
+        L.rs_autoreset.argtypes = [vp, vp, vp]
         L.rs_export_env.argtypes = [vp, i64, vp]
         L.rs_import_env.argtypes = [vp, i64, vp]
         L.rs_record_sizes.argtypes = [vp]

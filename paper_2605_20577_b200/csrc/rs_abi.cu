@@ -15,6 +15,7 @@
 #include <stdio.h>
 #include <string.h>
 
+#include <algorithm>
 #include <mutex>
 #include <string>
 
@@ -25,6 +26,8 @@ using namespace rs;
 namespace {
 
 constexpr int BLOCK = 128;
+// bytes of the staged t3 | t1 | t2 block (a TMA bulk copy is a multiple of 16 B)
+constexpr uint32_t STAGE_BYTES = (SMEM_TABLE_BYTES + 15u) & ~15u;
 
 thread_local std::string g_err;
 int set_err(int code, const char* fmt, ...) {
@@ -79,6 +82,9 @@ int device_tables(int device, DevTables* out) {
     CUDA_TRY(cudaMemcpy(base, H.t3.data(), H.t3.size() * 4, cudaMemcpyHostToDevice));
     CUDA_TRY(cudaMemcpy(base + T1_OFF, H.t1.data(), H.t1.size(), cudaMemcpyHostToDevice));
     CUDA_TRY(cudaMemcpy(base + T2_OFF, H.t2.data(), H.t2.size(), cudaMemcpyHostToDevice));
+    uint32_t pw[34];
+    for (int k = 0; k < 34; k++) pw[k] = kind_pow_calc(k);
+    CUDA_TRY(cudaMemcpy(base + POW_OFF, pw, sizeof(pw), cudaMemcpyHostToDevice));
     CUDA_TRY(cudaMemcpy(suit, H.suit_cls.data(), H.suit_cls.size(), cudaMemcpyHostToDevice));
     CUDA_TRY(cudaMemcpy(honor, H.honor_cls.data(), H.honor_cls.size(), cudaMemcpyHostToDevice));
     const uint8_t* sp = suit;
@@ -91,7 +97,7 @@ int device_tables(int device, DevTables* out) {
     dt.D.t1 = base + T1_OFF;
     dt.D.t2 = base + T2_OFF;
     dt.D.ns = NS; dt.D.nh = NH; dt.D.na = NA; dt.D.nb = NB;
-    dt.D.smem = SMEM_TABLE_BYTES;
+    dt.D.smem = (int)STAGE_BYTES;
     dt.mem = mem;
   }
   *out = dt.D;
@@ -107,15 +113,35 @@ struct StepOut {
   uint8_t* status;
 };
 
-// stage the packed t3 | t1 | t2 block (SMEM_TABLE_BYTES, a multiple of 2)
-// into shared memory with 16-byte vector copies; the engine reads it at
-// compile-time offsets (rs_hand.cuh t1_at / t2_at / t3_at)
+// stage the packed t3 | t1 | t2 block into shared memory; the engine reads
+// it at compile-time offsets (rs_hand.cuh t1_at / t2_at / t3_at).
+// One elected thread issues a single TMA bulk copy (cp.async.bulk, no tensor
+// map needed for a contiguous block) completing on an mbarrier; the other
+// warps spend no instructions on the copy and wait on the barrier phase.
 __device__ __forceinline__ Tabs stage_tables(const DevTables& D) {
-  const uint4* src = reinterpret_cast<const uint4*>(D.t3);
-  uint4* dst = reinterpret_cast<uint4*>(g_smem);
-  constexpr int n16 = (SMEM_TABLE_BYTES + 15) / 16;
-  for (int i = threadIdx.x; i < n16; i += blockDim.x) dst[i] = __ldg(src + i);
+  __shared__ __align__(8) uint64_t bar;
+  const uint32_t bar_addr = (uint32_t)__cvta_generic_to_shared(&bar);
+  if (threadIdx.x == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar_addr) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar_addr), "r"(STAGE_BYTES)
+                 : "memory");
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            (uint32_t)__cvta_generic_to_shared(g_smem)),
+        "l"(D.t3), "r"(STAGE_BYTES), "r"(bar_addr)
+        : "memory");
+  }
   __syncthreads();
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(bar_addr)
+      : "memory");
   return Tabs{};
 }
 
@@ -157,8 +183,13 @@ __global__ void __launch_bounds__(BLOCK) k_init(const __grid_constant__ Soa S, c
   write_step_out(out, e, E, E.load_legal(), r, 0);
 }
 
+// step (+ optional auto-reset, observation and next random action) in one
+// pass over the env's state.  With RS_STEP_AUTORESET the rewards / flags
+// describe the transition while the legal mask, current player and
+// observation already belong to the next game (Pgx auto_reset convention).
 __global__ void __launch_bounds__(BLOCK) k_step(const __grid_constant__ Soa S, const __grid_constant__ DevTables D,
-    const __grid_constant__ Cfg C, const int32_t* actions, StepOut out) {
+    const __grid_constant__ Cfg C, const int32_t* actions, int flags, rs_obs_out obs, int32_t* next_actions,
+    StepOut out) {
   const Tabs T = stage_tables(D);
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= S.n) return;
@@ -167,8 +198,28 @@ __global__ void __launch_bounds__(BLOCK) k_step(const __grid_constant__ Soa S, c
   Mask115 m;
   float r[4];
   const int st = E.step(actions[e], m, r);
-  if (st != RS_STATUS_CONTRACT) E.store();
-  write_step_out(out, e, E, m, r, st);
+  const int term = E.g.env_terminated, trunc = E.g.env_truncated;
+  bool dirty = st != RS_STATUS_CONTRACT;
+  if ((flags & RS_STEP_AUTORESET) && (term || trunc)) {
+    float r2[4];
+    E.g.resets++;
+    E.init_game(derive_key(E.g.env_key, 2 + (uint64_t)E.g.resets), r2);
+    m = E.load_legal();
+    dirty = true;
+  }
+  if (flags & RS_STEP_OBSERVE) write_obs(E, E.g.current_player, obs, e);
+  if (next_actions) {
+    const bool done = E.g.env_terminated || E.g.env_truncated;
+    next_actions[e] = done ? -1 : E.random_action(m);
+    dirty |= !done;
+  }
+  if (dirty) E.store();
+  if (out.legal_bits) reinterpret_cast<uint4*>(out.legal_bits)[e] = make_uint4(m.m[0], m.m[1], m.m[2], m.m[3]);
+  if (out.current_player) out.current_player[e] = (int8_t)E.g.current_player;
+  if (out.rewards) reinterpret_cast<float4*>(out.rewards)[e] = make_float4(r[0], r[1], r[2], r[3]);
+  if (out.terminated) out.terminated[e] = (uint8_t)term;
+  if (out.truncated) out.truncated[e] = (uint8_t)trunc;
+  if (out.status) out.status[e] = (uint8_t)st;
 }
 
 __global__ void __launch_bounds__(BLOCK) k_policy(const __grid_constant__ Soa S, const __grid_constant__ DevTables D,
@@ -193,15 +244,17 @@ __global__ void __launch_bounds__(BLOCK) k_observe(const __grid_constant__ Soa S
   write_obs(E, seats ? (int)seats[e] : E.g.current_player, obs, e);
 }
 
-// the fused rollout: the packed header stays in registers for all K steps
+// the fused rollout: the packed header stays in registers for all K steps.
+// Persistent grid (at most the resident CTA count): each CTA stages the
+// tables once and walks env tiles grid-stride.
 __global__ void __launch_bounds__(BLOCK) k_rollout(const __grid_constant__ Soa S, const __grid_constant__ DevTables D,
     const __grid_constant__ Cfg C, int steps, rs_obs_out obs,
                                                    int obs_slots, int16_t* actions_log, rs_rollout_stats* stats,
                                                    uint64_t* digests, StepOut out) {
   const Tabs T = stage_tables(D);
-  const int e = blockIdx.x * blockDim.x + threadIdx.x;
   unsigned long long games = 0;
-  if (e < S.n) {
+  const int stride = gridDim.x * blockDim.x;
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < S.n; e += stride) {
     Engine E(S, T, C, e);
     E.load();
     uint64_t d = digests ? digests[e] : 0ull;
@@ -230,13 +283,32 @@ __global__ void __launch_bounds__(BLOCK) k_rollout(const __grid_constant__ Soa S
   if (stats) {
     unsigned long long g = games;
     for (int off = 16; off > 0; off >>= 1) g += __shfl_down_sync(0xffffffffu, g, off);
-    const int lane = threadIdx.x & 31;
-    const int active = min(32, max(0, S.n - (int)(blockIdx.x * blockDim.x + (threadIdx.x & ~31))));
-    if (lane == 0 && active > 0) {
-      atomicAdd(reinterpret_cast<unsigned long long*>(&stats->games_completed), g);
-      atomicAdd(reinterpret_cast<unsigned long long*>(&stats->steps), (unsigned long long)active * steps);
-    }
+    if ((threadIdx.x & 31) == 0 && g) atomicAdd(reinterpret_cast<unsigned long long*>(&stats->games_completed), g);
+    if (blockIdx.x == 0 && threadIdx.x == 0)
+      atomicAdd(reinterpret_cast<unsigned long long*>(&stats->steps), (unsigned long long)S.n * steps);
   }
+}
+
+// bench/runner.py:107-109: a finished env starts its next game from
+// env_game_seed(seed, index, resets + 1); unfinished envs are untouched
+__global__ void __launch_bounds__(BLOCK) k_autoreset(const __grid_constant__ Soa S,
+    const __grid_constant__ DevTables D, const __grid_constant__ Cfg C, StepOut out) {
+  stage_tables(D);
+  const Tabs T{};
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= S.n) return;
+  Engine E(S, T, C, e);
+  E.load();
+  float r[4];
+  int st = 0;
+  if (E.g.env_terminated || E.g.env_truncated) {
+    E.g.resets++;
+    E.init_game(derive_key(E.g.env_key, 2 + (uint64_t)E.g.resets), r);
+    E.store();
+  } else {
+    E.current_rewards(r);
+  }
+  write_step_out(out, e, E, E.load_legal(), r, st);
 }
 
 __global__ void k_expand(const uint32_t* bits, uint8_t* bools, int n) {
@@ -276,6 +348,8 @@ struct rs_handle {
   size_t mem_bytes;
   uint32_t* legal_bits_tmp;  // step output when the caller asks only for bools
   rs_env_rec* rec_dev;
+  int num_sms;
+  int rollout_ctas_per_sm;  // resident k_rollout CTAs per SM (occupancy)
 };
 
 namespace {
@@ -285,6 +359,17 @@ Cfg to_cfg(const rs_config* c) {
              c->kazoe, c->double_yakuman, c->agari_yame, c->renchan_cap};
 }
 int grid_of(int n) { return (n + BLOCK - 1) / BLOCK; }
+
+// one thread per env; below 148 x 128 envs the CTAs shrink (to a multiple
+// of 32) so the warps spread over every SM instead of filling a few
+void launch_dims(const rs_handle* h, int* grid, int* block) {
+  if (h->n < h->num_sms * BLOCK) {
+    *block = std::max(32, ((h->n + h->num_sms - 1) / h->num_sms + 31) & ~31);
+  } else {
+    *block = BLOCK;
+  }
+  *grid = (h->n + *block - 1) / *block;
+}
 
 StepOut step_out(rs_handle* h, const rs_step_out* o) {
   StepOut s{};
@@ -351,11 +436,11 @@ int rs_tables_shanten_std(uint32_t cm, uint32_t cp, uint32_t cs, uint32_t cz, in
   return 0;
 }
 
-int64_t rs_state_bytes(const rs_handle* h) { return h ? (int64_t)h->mem_bytes : bytes_per_env(); }
+int64_t rs_state_bytes(const rs_handle* h) { return h ? (int64_t)h->mem_bytes : canonical_state_bytes(); }
 int64_t rs_num_envs(const rs_handle* h) { return h ? h->n : 0; }
 
 int rs_create(rs_handle** out, int64_t n_envs, const rs_config* cfg, int32_t device) {
-  if (!out || !cfg || n_envs <= 0 || n_envs > (1 << 26)) return set_err(RS_E_ARG, "bad rs_create arguments");
+  if (!out || !cfg || n_envs <= 0 || n_envs > (1 << 23)) return set_err(RS_E_ARG, "bad rs_create arguments (1 <= n <= 2^23)");
   if (cfg->rule != RS_RULE_RED && cfg->rule != RS_RULE_NO_RED) return set_err(RS_E_ARG, "bad rule");
   if (cfg->mode < 0 || cfg->mode > 2) return set_err(RS_E_ARG, "bad mode");
   if (cfg->illegal_penalty > 0.f) return set_err(RS_E_ARG, "illegal penalty must be <= 0");
@@ -383,6 +468,7 @@ int rs_create(rs_handle** out, int64_t n_envs, const rs_config* cfg, int32_t dev
       {(void**)&S.hrkind, 32 * n},           {(void**)&S.mtiles, 64 * n},
       {(void**)&S.minfo, 64 * n},            {(void**)&S.river, 4 * RS_MAX_RIVER * 2 * n},
       {(void**)&S.events, 64 * 2 * n},       {(void**)&S.legal, 16 * n},
+      {(void**)&S.evobs, (size_t)EVOBS_BYTES * n},
       {(void**)&S.results, sizeof(rs_result_rec) * n},
       {(void**)&h->legal_bits_tmp, 16 * n},  {(void**)&h->rec_dev, sizeof(rs_env_rec)},
   };
@@ -407,10 +493,14 @@ int rs_create(rs_handle** out, int64_t n_envs, const rs_config* cfg, int32_t dev
   if ((err = cudaMemset(h->mem, 0, total))) return cleanup(err, "state clear");
   const void* kernels[] = {(const void*)k_init, (const void*)k_step, (const void*)k_policy,
                            (const void*)k_observe, (const void*)k_rollout, (const void*)k_export,
-                           (const void*)k_import};
+                           (const void*)k_import, (const void*)k_autoreset};
   for (const void* k : kernels)
     if ((err = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, h->D.smem)))
       return cleanup(err, "cudaFuncSetAttribute");
+  if ((err = cudaDeviceGetAttribute(&h->num_sms, cudaDevAttrMultiProcessorCount, device)) ||
+      (err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&h->rollout_ctas_per_sm, k_rollout, BLOCK, h->D.smem)))
+    return cleanup(err, "occupancy query");
+  if (h->rollout_ctas_per_sm < 1) h->rollout_ctas_per_sm = 1;
   *out = h;
   return 0;
 }
@@ -439,9 +529,20 @@ int rs_init_indexed(rs_handle* h, uint64_t seed, int64_t index_base, const rs_st
 }
 
 int rs_step(rs_handle* h, const int32_t* actions_dev, const rs_step_out* out, void* stream) {
+  return rs_step_ex(h, actions_dev, 0, out, nullptr, nullptr, stream);
+}
+
+int rs_step_ex(rs_handle* h, const int32_t* actions_dev, int32_t flags, const rs_step_out* out,
+               const rs_obs_out* obs, int32_t* next_actions_dev, void* stream) {
   if (!h || !actions_dev) return set_err(RS_E_ARG, "rs_step: null argument");
+  if ((flags & RS_STEP_OBSERVE) && !obs) return set_err(RS_E_ARG, "RS_STEP_OBSERVE needs obs buffers");
   cudaStream_t st = (cudaStream_t)stream;
-  k_step<<<grid_of(h->n), BLOCK, h->D.smem, st>>>(h->S, h->D, h->cfg, actions_dev, step_out(h, out));
+  rs_obs_out o{};
+  if (obs) o = *obs;
+  int grid, block;
+  launch_dims(h, &grid, &block);
+  k_step<<<grid, block, h->D.smem, st>>>(h->S, h->D, h->cfg, actions_dev, flags, o, next_actions_dev,
+                                         step_out(h, out));
   return finish_step_out(h, out, st);
 }
 
@@ -469,8 +570,25 @@ int rs_rollout(rs_handle* h, int32_t steps, const rs_obs_out* obs, int32_t obs_s
   cudaStream_t st = (cudaStream_t)stream;
   rs_obs_out o{};
   if (obs) o = *obs;
-  k_rollout<<<grid_of(h->n), BLOCK, h->D.smem, st>>>(h->S, h->D, h->cfg, steps, o, obs ? obs_slots : 0,
+  // small batches: 32-thread CTAs spread the warps over every SM; large
+  // batches: a persistent grid of the resident CTA count (tables staged
+  // once per CTA, envs walked grid-stride)
+  int block = BLOCK, grid;
+  if (h->n < h->num_sms * BLOCK) {
+    block = ((h->n + h->num_sms - 1) / h->num_sms + 31) & ~31;
+    grid = (h->n + block - 1) / block;
+  } else {
+    grid = std::min(grid_of(h->n), h->num_sms * h->rollout_ctas_per_sm);
+  }
+  k_rollout<<<grid, block, h->D.smem, st>>>(h->S, h->D, h->cfg, steps, o, obs ? obs_slots : 0,
                                                      actions_log, stats_dev, digests_dev, step_out(h, out));
+  return finish_step_out(h, out, st);
+}
+
+int rs_autoreset(rs_handle* h, const rs_step_out* out, void* stream) {
+  if (!h) return set_err(RS_E_ARG, "rs_autoreset: null handle");
+  cudaStream_t st = (cudaStream_t)stream;
+  k_autoreset<<<grid_of(h->n), BLOCK, h->D.smem, st>>>(h->S, h->D, h->cfg, step_out(h, out));
   return finish_step_out(h, out, st);
 }
 

@@ -66,6 +66,18 @@ RS_HD uint64_t umulhi64(uint64_t a, uint64_t b) {
 #endif
 }
 
+// PRMT: byte i of the result is byte (s >> 4i) & 7 of {x (0-3), y (4-7)}
+RS_HD uint32_t byte_perm(uint32_t x, uint32_t y, uint32_t s) {
+#if defined(__CUDA_ARCH__)
+  return __byte_perm(x, y, s);
+#else
+  const uint64_t v = (uint64_t)x | ((uint64_t)y << 32);
+  uint32_t r = 0;
+  for (int i = 0; i < 4; i++) r |= (uint32_t)((v >> (8 * ((s >> (4 * i)) & 7))) & 0xFF) << (8 * i);
+  return r;
+#endif
+}
+
 // ---------------------------------------------- counter RNG (rng.py:18-65)
 // SplitMix64 finalizer; key/counter streams; randbelow = high word of x*n.
 RS_HD uint64_t mix64(uint64_t x) {
@@ -132,7 +144,7 @@ RS_HD uint32_t pow5(int i) {  // 5^i, i in 0..8, without memory
   return p;
 }
 // code delta of one tile of kind k, and the suit slot (0 m, 1 p, 2 s, 3 z)
-RS_HD uint32_t kind_pow(int k) {
+RS_HD uint32_t kind_pow_calc(int k) {
   return k < 27 ? pow5(8 - k % 9) : pow5(6 - (k - 27));
 }
 RS_HD int kind_suit(int k) { return k < 27 ? k / 9 : 3; }

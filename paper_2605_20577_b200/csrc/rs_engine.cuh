@@ -64,7 +64,8 @@ struct Engine {
   RS_HD Engine(const Soa& s, const Tabs& t, const Cfg& c, int env) : S(s), T(t), C(c), e(env) {}
 
   // ------------------------------------------------------------- memory
-  RS_HD size_t at(int f) const { return (size_t)f * S.n + e; }
+  // 32-bit index math: rs_create bounds n so that 160 * n < 2^31
+  RS_HD uint32_t at(int f) const { return (uint32_t)f * (uint32_t)S.n + (uint32_t)e; }
   RS_HD void load() {
     g.unpack(S.hdr[at(0)], S.hdr[at(1)], S.hdr[at(2)], S.hdr[at(3)], S.scores[e]);
   }
@@ -88,9 +89,32 @@ struct Engine {
   // engine.py:100-102 (64-slot ring; the full history is reconstructed by
   // the host while stepping)
   RS_HD void emit(int type, int actor, int tile) {
-    S.events[at((int)(g.events_len & 63))] =
-        (uint16_t)(type | ((actor + 1) << 4) | ((tile + 1) << 7));
+    const uint32_t p = g.events_len & 63u;
+    S.events[(uint32_t)e * RS_EVENT_WINDOW + p] = (uint16_t)(type | ((actor + 1) << 4) | ((tile + 1) << 7));
+    // observe.py:92-106 per observer, done once here instead of per observe
+    const uint32_t ty = (uint32_t)(type <= 8 ? type : type - 1);  // ron / tsumo share token 8
+    const uint32_t tok = tile < 0 ? 37u
+                         : (C.rule == RS_RULE_RED && is_red_tile(tile)) ? (uint32_t)(34 + red_index_of_kind(tile >> 2))
+                                                                         : (uint32_t)(tile >> 2);
+    uint32_t* ob = S.evobs + (uint32_t)e * (4 * EVOBS_SLOTS);
+#pragma unroll
+    for (int o = 0; o < 4; o++) {
+      const uint32_t rel = actor >= 0 ? (uint32_t)((actor - o) & 3) : 0u;
+      const uint32_t t = (type == EV_DRAW && actor != o) ? 37u : tok;  // opponents' draws hidden
+      const uint32_t w = ty | (rel << 8) | (t << 16);
+      ob[o * EVOBS_SLOTS + p] = w;
+      ob[o * EVOBS_SLOTS + p + RS_EVENT_WINDOW] = w;
+    }
     g.events_len++;
+  }
+  // empty window for every observer (the first 64 slots are read as pads
+  // until overwritten; slots 64.. are always written before being read)
+  RS_HD void clear_event_window() {
+    uint4* ob = reinterpret_cast<uint4*>(S.evobs + (uint32_t)e * (4 * EVOBS_SLOTS));
+    const uint4 pad = make_uint4(EVOBS_PAD, EVOBS_PAD, EVOBS_PAD, EVOBS_PAD);
+#pragma unroll 4
+    for (int o = 0; o < 4; o++)
+      for (int i = 0; i < RS_EVENT_WINDOW / 4; i++) ob[o * (EVOBS_SLOTS / 4) + i] = pad;
   }
 
   // ------------------------------------------------------ rng / dealing
@@ -251,22 +275,29 @@ struct Engine {
     w.kazoe = C.kazoe != 0;
   }
 
-  // engine.py:386-390
-  RS_COLD bool can_tsumo(int seat, const Hand& h) const {
+  // engine.py:386-390: the cheap shanten test inline, the yaku search cold
+  RS_HOT bool can_tsumo(int seat, const Hand& h) const {
     if (hi::shanten(h.info) != -1) return false;
+    return tsumo_has_yaku(seat, h);
+  }
+  RS_COLD bool tsumo_has_yaku(int seat, const Hand& h) const {
     WinIn w;
     win_input(seat, h, g.drawn, true, false, w);
     Reading r;
     return score_win(w, r, true);
   }
-  // engine.py:393-399 + types.py:93-100 (furiten)
-  RS_COLD bool can_ron(int seat, int tile, bool chankan) const {
+  // engine.py:393-399 + types.py:93-100 (furiten): the wait / furiten
+  // rejections inline (they decide almost every call), the yaku search cold
+  RS_HOT bool can_ron(int seat, int tile, bool chankan) const {
     const uint32_t inf = info(seat);
     if (hi::shanten(inf) != 0) return false;
     const uint64_t wt = waits(seat);
     if (!((wt >> (tile >> 2)) & 1)) return false;
     if (hi::temp(inf) || hi::perm(inf)) return false;
     if (wt & S.hrkind[at(seat)]) return false;
+    return ron_has_yaku(seat, tile, chankan);
+  }
+  RS_COLD bool ron_has_yaku(int seat, int tile, bool chankan) const {
     const Hand h = load_hand(S, e, seat);
     WinIn w;
     win_input(seat, h, tile, false, chankan, w);
@@ -354,7 +385,7 @@ struct Engine {
   }
 
   // engine.py:309-328
-  RS_COLD void legal_call(Mask115& m) const {
+  RS_HD void legal_call(Mask115& m) const {
     const int seat = g.qseat(0), stage = g.qstage(0);
     const int kind = g.call_tile >> 2;
     m.set(A_PASS);
@@ -928,6 +959,7 @@ struct Engine {
     g.honba = g.deposits = g.repeats = g.n_results = 0;
     g.step_count = 0;
     g.events_len = 0;
+    clear_event_window();
     g.drawn = -1;
     for (int s = 0; s < 4; s++) g.scores[s] = 25000;
     g.rng_key = mix64(seed);

@@ -56,26 +56,26 @@ struct Hand {
 };
 
 RS_HD Hand load_hand(const Soa& S, int e, int seat) {
-  const int n = S.n;
+  const uint32_t n = (uint32_t)S.n, s = (uint32_t)seat, x = (uint32_t)e;
   Hand h;
-  const uint32_t* m = S.hmask + (size_t)(seat * 5) * n + e;
+  const uint32_t* m = S.hmask + (s * 5u * n + x);
   h.w0 = m[0]; h.w1 = m[n]; h.w2 = m[2 * n]; h.w3 = m[3 * n]; h.w4 = m[4 * n];
-  const uint32_t* c = S.hcode + (size_t)(seat * 4) * n + e;
+  const uint32_t* c = S.hcode + (s * 4u * n + x);
   h.cm = c[0]; h.cp = c[n]; h.cs = c[2 * n]; h.cz = c[3 * n];
-  h.cls = S.hcls[(size_t)seat * n + e];
-  h.info = S.hinfo[(size_t)seat * n + e];
-  h.waits = S.hwaits[(size_t)seat * n + e];
+  h.cls = S.hcls[s * n + x];
+  h.info = S.hinfo[s * n + x];
+  h.waits = S.hwaits[s * n + x];
   return h;
 }
 RS_HD void store_hand(const Soa& S, int e, int seat, const Hand& h) {
-  const int n = S.n;
-  uint32_t* m = S.hmask + (size_t)(seat * 5) * n + e;
+  const uint32_t n = (uint32_t)S.n, s = (uint32_t)seat, x = (uint32_t)e;
+  uint32_t* m = S.hmask + (s * 5u * n + x);
   m[0] = h.w0; m[n] = h.w1; m[2 * n] = h.w2; m[3 * n] = h.w3; m[4 * n] = h.w4;
-  uint32_t* c = S.hcode + (size_t)(seat * 4) * n + e;
+  uint32_t* c = S.hcode + (s * 4u * n + x);
   c[0] = h.cm; c[n] = h.cp; c[2 * n] = h.cs; c[3 * n] = h.cz;
-  S.hcls[(size_t)seat * n + e] = h.cls;
-  S.hinfo[(size_t)seat * n + e] = h.info;
-  S.hwaits[(size_t)seat * n + e] = h.waits;
+  S.hcls[s * n + x] = h.cls;
+  S.hinfo[s * n + x] = h.info;
+  S.hwaits[s * n + x] = h.waits;
 }
 
 #if defined(__CUDACC__)
@@ -115,6 +115,14 @@ RS_HD uint32_t t3_at(const Tabs& T, int i) {
 #endif
 }
 RS_HD int cls_byte(uint32_t cls, int s) { return (cls >> (8 * s)) & 255; }
+// base-5 code delta of one tile of kind k (staged table on the device)
+RS_HD uint32_t kind_pow(int k) {
+#if defined(__CUDA_ARCH__)
+  return reinterpret_cast<const uint32_t*>(g_smem + POW_OFF)[k];
+#else
+  return kind_pow_calc(k);
+#endif
+}
 
 // best value (2*sets + partials + head) at block budget `budget` (shanten.py:30-63)
 RS_HD int std_best(const Tabs& T, int cm, int cp, int cs, int cz, int budget) {

@@ -20,45 +20,54 @@ RS_HD void write_obs(const Engine& E, int seat, const rs_obs_out& obs, int64_t o
   const int rule = E.C.rule;
   const Hand h = load_hand(S, E.e, seat);
   if (obs.hand_tokens) {
-    uint8_t* ht = obs.hand_tokens + o * 14;
+    // sorted tokens (kinds ascending, then the held red fives 34..36), padded
+    // with 37, assembled in two registers and written as 7 u16 stores
+    uint64_t lo = 0x2525252525252525ull, hi8 = 0x2525252525252525ull;
     int n = 0;
-    for (int k = 0; k < 34; k++) {
+    auto put = [&](uint32_t v) {
+      if (n < 8) lo = (lo & ~(0xFFull << (8 * n))) | ((uint64_t)v << (8 * n));
+      else hi8 = (hi8 & ~(0xFFull << (8 * (n - 8)))) | ((uint64_t)v << (8 * (n - 8)));
+      n++;
+    };
+    uint64_t present = h.kinds_ge(1);
+    while (present) {
+      const int k = ctz64(present);
+      present &= present - 1;
       int c = h.count(k);
       if (rule == RS_RULE_RED && red_index_of_kind(k) >= 0 && h.has(4 * k)) c--;
-      for (int j = 0; j < c; j++) ht[n++] = (uint8_t)k;
+      for (int j = 0; j < c; j++) put((uint32_t)k);
     }
     if (rule == RS_RULE_RED) {
-      if (h.has(16)) ht[n++] = 34;
-      if (h.has(52)) ht[n++] = 35;
-      if (h.has(88)) ht[n++] = 36;
+      if (h.has(16)) put(34);
+      if (h.has(52)) put(35);
+      if (h.has(88)) put(36);
     }
-    for (; n < 14; n++) ht[n] = 37;
+    uint16_t* ht = reinterpret_cast<uint16_t*>(obs.hand_tokens + o * 14);
+    ht[0] = (uint16_t)lo; ht[1] = (uint16_t)(lo >> 16); ht[2] = (uint16_t)(lo >> 32); ht[3] = (uint16_t)(lo >> 48);
+    ht[4] = (uint16_t)hi8; ht[5] = (uint16_t)(hi8 >> 16); ht[6] = (uint16_t)(hi8 >> 32);
   }
   if (obs.event_tokens) {
-    // 64 x (type, rel actor, token), oldest first, padded (0,0,37)
-    uint32_t words[48];
-    const uint32_t len = g.events_len;
-    const int cnt = len < 64 ? (int)len : 64, pad = 64 - cnt;
-    for (int i = 0; i < 48; i++) words[i] = 0;
-    for (int i = 0; i < 64; i++) {
-      uint32_t ty = 0, rel = 0, tok = 37;
-      if (i >= pad) {
-        const uint32_t idx = (len - (uint32_t)cnt + (uint32_t)(i - pad)) & 63u;
-        const uint32_t ev = S.events[(size_t)idx * S.n + E.e];
-        const int type = ev & 15, actor = (int)((ev >> 4) & 7) - 1, tile = (int)((ev >> 7) & 255) - 1;
-        ty = (uint32_t)ev_token(type);
-        rel = actor >= 0 ? (uint32_t)((actor - seat) & 3) : 0u;
-        if (type == EV_DRAW && actor != seat) tok = 37;
-        else tok = tile >= 0 ? (uint32_t)tile_token(tile, rule) : 37u;
-      }
-      const int b = 3 * i;
-      words[b >> 2] |= ty << (8 * (b & 3));
-      words[(b + 1) >> 2] |= rel << (8 * ((b + 1) & 3));
-      words[(b + 2) >> 2] |= tok << (8 * ((b + 2) & 3));
-    }
+    // 64 x (type, rel actor, token), oldest first, padded (0,0,37): the
+    // observer's pre-encoded stream holds them contiguously from len & 63
+    // (Engine::emit); pack 4 triples into 3 words with byte permutes
+    const uint32_t* ob = S.evobs + (uint32_t)E.e * (4 * EVOBS_SLOTS) + (uint32_t)seat * EVOBS_SLOTS +
+                         (g.events_len & 63u);
     uint4* dst = reinterpret_cast<uint4*>(obs.event_tokens + o * 192);
 #pragma unroll
-    for (int i = 0; i < 12; i++) dst[i] = make_uint4(words[4 * i], words[4 * i + 1], words[4 * i + 2], words[4 * i + 3]);
+    for (int q = 0; q < 4; q++) {
+      uint32_t w[12];
+#pragma unroll
+      for (int r = 0; r < 4; r++) {
+        const uint32_t a = ob[16 * q + 4 * r], b = ob[16 * q + 4 * r + 1], c = ob[16 * q + 4 * r + 2],
+                       d = ob[16 * q + 4 * r + 3];
+        w[3 * r] = byte_perm(a, b, 0x4210);
+        w[3 * r + 1] = byte_perm(b, c, 0x5421);
+        w[3 * r + 2] = byte_perm(c, d, 0x6542);
+      }
+      dst[3 * q] = make_uint4(w[0], w[1], w[2], w[3]);
+      dst[3 * q + 1] = make_uint4(w[4], w[5], w[6], w[7]);
+      dst[3 * q + 2] = make_uint4(w[8], w[9], w[10], w[11]);
+    }
   }
   if (obs.shanten) obs.shanten[o] = (int8_t)hi::shanten(h.info);
   if (obs.scores)
@@ -178,7 +187,7 @@ RS_COLD void export_env(Engine& E, const Cfg& C, rs_env_rec& r) {
   for (int i = 0; i < 64; i++) {
     if (i < cnt) {
       const uint32_t idx = (g.events_len - (uint32_t)cnt + (uint32_t)i) & 63u;
-      const uint32_t ev = S.events[(size_t)idx * S.n + E.e];
+      const uint32_t ev = S.events[(uint32_t)E.e * RS_EVENT_WINDOW + idx];
       r.events[i][0] = (int16_t)(ev & 15);
       r.events[i][1] = (int16_t)((int)((ev >> 4) & 7) - 1);
       r.events[i][2] = (int16_t)((int)((ev >> 7) & 255) - 1);
@@ -268,6 +277,7 @@ RS_COLD void import_env(Engine& E, const rs_env_rec& r) {
   g.step_count = (uint32_t)r.step_count; g.terminated = r.terminated; g.truncated = r.truncated;
   const int cnt = r.events_len < 64 ? r.events_len : 64;
   g.events_len = (uint32_t)(r.events_len - cnt);
+  E.clear_event_window();
   for (int i = 0; i < cnt; i++) E.emit(r.events[i][0], r.events[i][1], r.events[i][2]);
   g.n_results = r.n_results;
   S.results[E.e] = r.last_result;

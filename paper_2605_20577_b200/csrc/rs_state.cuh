@@ -19,6 +19,9 @@
 namespace rs {
 
 constexpr int WALL_STRIDE = 144;  // 136 tiles padded to 9 x 16 B
+constexpr int EVOBS_SLOTS = 2 * RS_EVENT_WINDOW;           // doubled window
+constexpr int EVOBS_BYTES = 4 * EVOBS_SLOTS * 4;             // per env
+constexpr uint32_t EVOBS_PAD = 37u << 16;                    // (0, 0, 37)
 
 struct Soa {
   int n;
@@ -34,14 +37,28 @@ struct Soa {
   uint32_t* mtiles;  // [4 seat][4 meld][n] tile ids (4 x u8)
   uint32_t* minfo;   // [4 seat][4 meld][n] type | n | from | called
   uint16_t* river;   // [4 seat][40][n] tile | flags << 8
-  uint16_t* events;  // [64][n] ring: type | (actor+1) << 4 | (tile+1) << 7
+  uint16_t* events;  // [n][64] ring (128 B per env): type | (actor+1) << 4 | (tile+1) << 7
+  // [n][4 observer][128] the same events pre-encoded for each observer as
+  // observe() emits them (type token, relative actor, visible tile token)
+  // and written twice (slot p and p + 64): the last 64 events of any
+  // observer are then the contiguous slots [len & 63, (len & 63) + 64)
+  uint32_t* evobs;
   uint32_t* legal;   // [4][n] env-view legal mask
   rs_result_rec* results;  // [n] last kyoku result (written at kyoku end)
 };
 
+// S of the roofline: the fields that define one env's game (header, scores,
+// wall, concealed sets, flags, waits, river kinds, melds, river, event ring,
+// legal mask); excludes derived caches (suit codes / classes, per-observer
+// event streams) and the kyoku-result output record
+constexpr int64_t canonical_state_bytes() {
+  return 4 * 16 + 16 + WALL_STRIDE + 4 * 5 * 4 + 4 * 4 + 4 * 8 + 4 * 8 + 4 * 4 * 4 + 4 * 4 * 4 +
+         4 * RS_MAX_RIVER * 2 + RS_EVENT_WINDOW * 2 + 4 * 4;
+}
+
 inline int64_t bytes_per_env() {
   return 4 * 16 + 16 + WALL_STRIDE + 4 * 5 * 4 + 4 * 4 * 4 + 4 * 4 + 4 * 4 + 4 * 8 + 4 * 8 +
-         4 * 4 * 4 + 4 * 4 * 4 + 4 * RS_MAX_RIVER * 2 + RS_EVENT_WINDOW * 2 + 4 * 4 +
+         4 * 4 * 4 + 4 * 4 * 4 + 4 * RS_MAX_RIVER * 2 + RS_EVENT_WINDOW * 2 + EVOBS_BYTES + 4 * 4 +
          (int64_t)sizeof(rs_result_rec);
 }
 

@@ -34,7 +34,8 @@ constexpr int NB = 84;  // distinct (s, z) merges
 constexpr int T3_BYTES = 4 * NA * NB;
 constexpr int T1_OFF = T3_BYTES;
 constexpr int T2_OFF = T1_OFF + NS * NS;
-constexpr int SMEM_TABLE_BYTES = T2_OFF + NS * NH;
+constexpr int POW_OFF = (T2_OFF + NS * NH + 3) & ~3;  // u32[34]: code delta per kind
+constexpr int SMEM_TABLE_BYTES = POW_OFF + 4 * 34;
 
 struct HostTables {
   bool ready = false;

@@ -164,15 +164,37 @@ class BatchEnv:
                   "rs_init_indexed")
         return self
 
-    def step(self, actions: torch.Tensor) -> "BatchEnv":
+    def step(self, actions: torch.Tensor, *, autoreset: bool = False, observe: bool = False,
+             next_actions: torch.Tensor | None = None, out: abi.rs_step_out | None = None) -> "BatchEnv":
         """step(state, action) for every env (env/core.py:101-110): illegal ids
         end the episode with the penalty at the offender; stepping a finished
-        env sets RS_STATUS_CONTRACT in `status` and changes nothing."""
+        env sets RS_STATUS_CONTRACT in `status` and changes nothing.
+
+        In the same kernel: `autoreset` restarts finished envs (rewards and
+        flags still describe the transition, the mask / player / observation
+        belong to the new game); `observe` fills `self.observe()`'s tensors
+        for the current players; `next_actions` (int32[n]) receives the
+        random policy's next action (-1 for finished envs)."""
         actions = actions.to(device=self.device, dtype=torch.int32).contiguous()
         if actions.numel() != self.n:
             raise ValueError("need one action per env")
-        check(self._L.rs_step(self._h, actions.data_ptr(), C.byref(self._out), self._stream()), "rs_step")
+        flags = (1 if autoreset else 0) | (2 if observe else 0)
+        ost = None
+        if observe:
+            if self._obs is None:
+                self._obs = alloc_observations(self.n, self.device)
+            ost = obs_struct(self._obs)
+        check(self._L.rs_step_ex(self._h, actions.data_ptr(), flags, C.byref(out if out is not None else self._out),
+                                 C.byref(ost) if ost is not None else None, _ptr(next_actions), self._stream()),
+              "rs_step_ex")
         return self
+
+    @property
+    def observations(self) -> Observations:
+        """the tensors `observe()` / `step(observe=True)` write into"""
+        if self._obs is None:
+            self._obs = alloc_observations(self.n, self.device)
+        return self._obs
 
     def observe(self, seats: torch.Tensor | None = None, out: Observations | None = None) -> Observations:
         """observe(state, seat) for every env; `seats` defaults to each env's
@@ -197,6 +219,12 @@ class BatchEnv:
         check(self._L.rs_policy_random(self._h, out.data_ptr(), self._stream()), "rs_policy_random")
         return out
 
+    def autoreset(self) -> "BatchEnv":
+        """Restart every finished env with its next bench seed
+        (bench/runner.py:107-109); the output tensors are refreshed."""
+        check(self._L.rs_autoreset(self._h, C.byref(self._out), self._stream()), "rs_autoreset")
+        return self
+
     def rollout(self, steps: int, obs: Observations | None = None, obs_slots: int = 0,
                 actions_log: torch.Tensor | None = None, stats: torch.Tensor | None = None,
                 digests: torch.Tensor | None = None) -> "BatchEnv":
@@ -219,3 +247,87 @@ class BatchEnv:
     def load(self, i: int, rec: abi.rs_env_rec) -> None:
         torch.cuda.current_stream(self.device).synchronize()
         check(self._L.rs_import_env(self._h, int(i), C.byref(rec)), "rs_import_env")
+
+
+class HostStepper:
+    """Host-driven stepping through pinned memory, one CUDA graph per step.
+
+    Per `step()`: the actions in `actions` (pinned int32[n], written by the
+    caller) are copied to the device, one fused kernel steps every env
+    (optionally auto-resetting, observing and sampling the random policy's
+    next action), and the step result is copied back into pinned host
+    buffers.  The H2D copy, the kernel and the D2H copy are captured once
+    into a CUDA graph and replayed, so a step costs one graph launch.
+
+    Host result views (valid after `step()` returns): rewards f32[n,4],
+    legal_bits i32[n,4], next_actions i32[n], current_player i8[n],
+    terminated / truncated / status u8[n].
+    """
+
+    BYTES_PER_ENV = 40
+
+    def __init__(self, env: BatchEnv, *, autoreset: bool = True, observe: bool = True, policy: bool = True,
+                 graph: bool = True):
+        n, dev = env.n, env.device
+        self.env = env
+        self.n = n
+        self.autoreset, self.observe, self.policy = autoreset, observe, policy
+        self.actions = torch.zeros(n, dtype=torch.int32, pin_memory=True)
+        self._act_dev = torch.zeros(n, dtype=torch.int32, device=dev)
+        self._res_dev = torch.zeros(n * self.BYTES_PER_ENV, dtype=torch.uint8, device=dev)
+        self._res_host = torch.zeros(n * self.BYTES_PER_ENV, dtype=torch.uint8, pin_memory=True)
+        d, h = self._views(self._res_dev), self._views(self._res_host)
+        self.rewards, self.legal_bits, self.next_actions = h["rewards"], h["legal_bits"], h["next_actions"]
+        self.current_player, self.terminated = h["current_player"], h["terminated"]
+        self.truncated, self.status = h["truncated"], h["status"]
+        self._dev_views = d
+        self._out = abi.rs_step_out(
+            legal_mask=None, legal_bits=d["legal_bits"].data_ptr(), current_player=d["current_player"].data_ptr(),
+            rewards=d["rewards"].data_ptr(), terminated=d["terminated"].data_ptr(),
+            truncated=d["truncated"].data_ptr(), status=d["status"].data_ptr())
+        self.bytes_h2d = 4 * n
+        self.bytes_d2h = self.BYTES_PER_ENV * n
+        self._graph = None
+        if graph:
+            # no eager warm-up: a step mutates the envs, and nothing in the
+            # body needs lazy initialisation (capture does not execute)
+            s = torch.cuda.Stream(device=dev)
+            s.wait_stream(torch.cuda.current_stream(dev))
+            torch.cuda.synchronize(dev)
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=s):
+                self._body()
+            self._graph = g
+            self._stream = s
+
+    def _views(self, buf: torch.Tensor) -> dict:
+        n = self.n
+        return {
+            "rewards": buf[0:16 * n].view(torch.float32).view(n, 4),
+            "legal_bits": buf[16 * n:32 * n].view(torch.int32).view(n, 4),
+            "next_actions": buf[32 * n:36 * n].view(torch.int32),
+            "current_player": buf[36 * n:37 * n].view(torch.int8),
+            "terminated": buf[37 * n:38 * n],
+            "truncated": buf[38 * n:39 * n],
+            "status": buf[39 * n:40 * n],
+        }
+
+    def _body(self):
+        self._act_dev.copy_(self.actions, non_blocking=True)
+        self.env.step(self._act_dev, autoreset=self.autoreset, observe=self.observe,
+                      next_actions=self._dev_views["next_actions"] if self.policy else None, out=self._out)
+        self._res_host.copy_(self._res_dev, non_blocking=True)
+
+    def launch(self):
+        """enqueue one step (graph replay) without waiting"""
+        if self._graph is not None:
+            self._graph.replay()
+        else:
+            self._body()
+
+    def step(self):
+        """one step; returns when the host result views are valid (graph
+        replays run on the current stream)"""
+        self.launch()
+        torch.cuda.current_stream(self.env.device).synchronize()
+        return self

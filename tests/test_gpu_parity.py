@@ -131,3 +131,42 @@ def test_step_tensors_match_records():
         assert int(env.current_player[i]) == r.current_player
         assert env.rewards[i].tolist() == [float(x) for x in r.rewards]
         assert bool(env.terminated[i]) == bool(r.env_terminated)
+
+
+@pytest.mark.parametrize("rule", RULES)
+def test_host_stepper_equals_fused_rollout(rule):
+    """HostStepper (CUDA graph: H2D actions, fused step+autoreset+observe+
+    policy, D2H results) follows the same trajectories as k_rollout."""
+    from paper_2605_20577_b200.env import HostStepper
+
+    n, steps = 300, 150
+    cfg = EnvConfig(rule=rule)
+    a = BatchEnv(n, cfg).init(seed=9)
+    b = BatchEnv(n, cfg).init(seed=9)
+    a.rollout(steps)
+    hs = HostStepper(b, autoreset=True, observe=True, policy=True)
+    first = torch.empty(n, dtype=torch.int32, device="cuda")
+    b.random_actions(out=first)
+    hs.actions.copy_(first.cpu())
+    # k_rollout resets before choosing; HostStepper resets after stepping:
+    # identical sequence of (reset, policy draw, step)
+    for _ in range(steps):
+        hs.step()
+        hs.actions.copy_(hs.next_actions)
+    torch.cuda.synchronize()
+    compared = 0
+    for i in range(0, n, 3):
+        reca, recb = a.export(i), b.export(i)
+        if reca.env_terminated or reca.env_truncated:
+            continue  # b has already auto-reset this env
+        assert recb.policy_counter == reca.policy_counter + 1
+        compared += 1
+        ra, rb = projection(reca), projection(recb)
+        # b has already drawn (and consumed) the next policy action
+        ra["internal"].pop("rewards"); rb["internal"].pop("rewards")
+        ra["internal"].pop("legal_mask"); rb["internal"].pop("legal_mask")
+        ra.pop("legal"); rb.pop("legal")
+        for d in (ra, rb):
+            d["internal"].pop("env_terminated"); d["internal"].pop("env_truncated")
+        assert not diff(ra, rb), (i, diff(ra, rb)[:5])
+    assert compared > 50

@@ -1,0 +1,148 @@
+"""The CPU oracle against the golden fixtures generated from the Python
+reference (tests/golden/make_golden.py).  Pins the oracle before it is used
+as the checker of the CUDA path."""
+
+from __future__ import annotations
+
+import gzip
+import json
+from pathlib import Path
+
+import pytest
+
+from oracle import mjoracle as O
+from paper_2605_20577_b200 import abi
+
+GOLD = Path(__file__).resolve().parent / "golden"
+
+
+def load(name):
+    p = GOLD / name
+    data = gzip.open(p).read() if name.endswith(".gz") else p.read_bytes()
+    return json.loads(data)
+
+
+def test_rng_known_answers():
+    g = load("rng.json")
+    for x, want in g["mix"]:
+        assert O.mix(x) == want
+    for a, b, want in g["derive_key"]:
+        assert O.derive_key(a, b) == want
+    for s, i, r, want in g["env_game_seed"]:
+        assert O.env_game_seed(s, i, r) == want
+    for s, i, want in g["env_policy_key"]:
+        assert O.env_policy_key(s, i) == want
+    for seed, wall, counter in g["walls"]:
+        got, c = O.shuffle136(O.mix(seed), 0)
+        assert got == wall and c == counter
+
+
+def test_survey_kats():
+    # KATs captured from the reference
+    assert O.mix(0) == 0
+    assert O.env_game_seed(0, 0) == 0xCD7B50C3B2B4AC9F
+    assert O.env_policy_key(0, 0) == 0xFB5E449867F698F6
+    e = O.OracleEnv(O.make_config(rule="no-red")).init(O.env_game_seed(0, 0))
+    rec = e.record()
+    assert list(rec.wall[:16]) == [113, 101, 135, 73, 10, 105, 97, 19, 127, 3, 47, 27, 21, 81, 134, 17]
+    assert e.legal() == (6, 11, 13, 18, 20, 25, 28, 30, 32, 33)
+    assert rec.rng_counter == 135
+
+
+def test_tables_blob_matches_reference():
+    g = load("tables.json")
+    blob = O.tables_blob()
+    import hashlib
+    assert len(blob) == g["size"]
+    assert O.tables_crc() == g["crc32"] == 0x33D1141E
+    assert hashlib.sha256(blob).hexdigest() == g["sha256"]
+
+
+def test_shanten_and_waits():
+    for counts, melds, sh, waits in load("shanten.json.gz"):
+        assert O.shanten(counts, melds) == sh, (counts, melds)
+        if waits is not None:
+            assert list(O.waits(counts, melds)) == waits, (counts, melds)
+
+
+def ctx_from_json(c, kazoe, dy) -> O.orc_winctx:
+    x = O.orc_winctx()
+    for k in range(34):
+        x.concealed[k] = c["concealed"][k]
+    x.n_melds = len(c["melds"])
+    for i, (typ, tiles, called, frm) in enumerate(c["melds"]):
+        m = x.melds[i]
+        m.type, m.n_tiles, m.from_seat = typ, len(tiles), frm
+        for j, t in enumerate(tiles):
+            m.tiles[j] = t
+        m.called_tile = called
+    x.win_tile = c["win_tile"]
+    x.tsumo = int(c["tsumo"])
+    x.seat_wind, x.round_wind = c["seat_wind"], c["round_wind"]
+    x.n_ids = len(c["ids"])
+    for i, t in enumerate(c["ids"]):
+        x.ids[i] = t
+    x.riichi, x.ippatsu = c["riichi"], int(c["ippatsu"])
+    x.last_tile, x.rinshan, x.chankan, x.first_draw = (int(c[k]) for k in ("last_tile", "rinshan", "chankan", "first_draw"))
+    x.n_dora = len(c["dora"])
+    for i, t in enumerate(c["dora"]):
+        x.dora[i] = t
+    x.n_ura = len(c["ura"])
+    for i, t in enumerate(c["ura"]):
+        x.ura[i] = t
+    x.rule = c["rule"]
+    x.kazoe, x.double_yakuman = int(kazoe), int(dy)
+    return x
+
+
+def test_scoring_golden_and_randomized():
+    cases = load("scoring.json.gz")
+    assert len(cases) >= 900
+    scored = 0
+    for case in cases:
+        got = O.score(ctx_from_json(case["ctx"], case["kazoe"], case["dy"]))
+        want = case["want"]
+        if want is None:
+            assert got is None
+            continue
+        w, order = got
+        from paper_2605_20577_b200.records import yaku_entries
+        assert [[y, int(w.yaku_han[y])] for y in order] == want["yaku"]
+        assert yaku_entries(w) == want["yaku"]  # host-side order reconstruction
+        assert (w.yakuman, w.han, w.fu, w.base, w.dora, w.ura, w.reds) == \
+            (want["yakuman"], want["han"], want["fu"], want["base"], want["dora"], want["ura"], want["reds"])
+        assert abi.FORMS[w.form] == want["form"]
+        scored += 1
+    assert scored > 500
+
+
+def _obs_digest(o: dict) -> str:
+    import hashlib
+    return hashlib.sha256(json.dumps(o, sort_keys=True).encode()).hexdigest()[:16]
+
+
+@pytest.mark.parametrize("chunk", range(4))
+def test_traces_full_fingerprints(chunk):
+    """Every step of reference games: the sha256 fingerprint of the full
+    serialize_state (events, results, win details included), the
+    observation, legal ids, player and rewards."""
+    games = load("traces.json.gz")
+    games = games[chunk::4]
+    for g in games:
+        cfg = O.make_config(rule=g["rule"], mode=g["mode"])
+        env = O.OracleEnv(cfg).init(O.env_game_seed(g["seed"], g["index"]))
+        kc = [O.env_policy_key(g["seed"], g["index"]), 0]
+        for t, row in enumerate(g["steps"]):
+            fp, od, cp, legal, rewards, term, trunc = row[:7]
+            rec = env.record()
+            where = f"{g['rule']} {g['mode']} {g['policy']} idx {g['index']} step {t}"
+            assert env.fingerprint()[:16] == fp, where
+            assert rec.current_player == cp, where
+            assert list(env.legal()) == legal, where
+            assert [round(float(x), 6) for x in rec.rewards] == [round(x, 6) for x in rewards], where
+            assert (rec.env_terminated, rec.env_truncated) == (term, trunc), where
+            assert _obs_digest(env.observe(cp)) == od, where
+            if len(row) > 7:
+                a = env.random_policy(kc) if g["policy"] == "random" else env.heuristic_policy()
+                assert a == row[7], where
+                env.step(a)
