@@ -16,7 +16,7 @@ from pathlib import Path
 from . import abi
 
 PKG_DIR = Path(__file__).resolve().parent
-LIB_PATH = PKG_DIR / "_rinshan.so"
+LIB_PATH = Path(os.environ.get("RINSHAN_LIB", PKG_DIR / "_rinshan.so"))  # override: build experiments
 CSRC = PKG_DIR / "csrc"
 INCLUDE = PKG_DIR.parent / "include" / "rinshan.h"
 

@@ -101,20 +101,9 @@ struct Engine {
     for (int o = 0; o < 4; o++) {
       const uint32_t rel = actor >= 0 ? (uint32_t)((actor - o) & 3) : 0u;
       const uint32_t t = (type == EV_DRAW && actor != o) ? 37u : tok;  // opponents' draws hidden
-      const uint32_t w = ty | (rel << 8) | (t << 16);
-      ob[o * EVOBS_SLOTS + p] = w;
-      ob[o * EVOBS_SLOTS + p + RS_EVENT_WINDOW] = w;
+      ob[o * EVOBS_SLOTS + p] = ty | (rel << 8) | (t << 16);
     }
     g.events_len++;
-  }
-  // empty window for every observer (the first 64 slots are read as pads
-  // until overwritten; slots 64.. are always written before being read)
-  RS_HD void clear_event_window() {
-    uint4* ob = reinterpret_cast<uint4*>(S.evobs + (uint32_t)e * (4 * EVOBS_SLOTS));
-    const uint4 pad = make_uint4(EVOBS_PAD, EVOBS_PAD, EVOBS_PAD, EVOBS_PAD);
-#pragma unroll 4
-    for (int o = 0; o < 4; o++)
-      for (int i = 0; i < RS_EVENT_WINDOW / 4; i++) ob[o * (EVOBS_SLOTS / 4) + i] = pad;
   }
 
   // ------------------------------------------------------ rng / dealing
@@ -959,7 +948,6 @@ struct Engine {
     g.honba = g.deposits = g.repeats = g.n_results = 0;
     g.step_count = 0;
     g.events_len = 0;
-    clear_event_window();
     g.drawn = -1;
     for (int s = 0; s < 4; s++) g.scores[s] = 25000;
     g.rng_key = mix64(seed);

@@ -47,19 +47,22 @@ RS_HD void write_obs(const Engine& E, int seat, const rs_obs_out& obs, int64_t o
     ht[4] = (uint16_t)hi8; ht[5] = (uint16_t)(hi8 >> 16); ht[6] = (uint16_t)(hi8 >> 32);
   }
   if (obs.event_tokens) {
-    // 64 x (type, rel actor, token), oldest first, padded (0,0,37): the
-    // observer's pre-encoded stream holds them contiguously from len & 63
-    // (Engine::emit); pack 4 triples into 3 words with byte permutes
-    const uint32_t* ob = S.evobs + (uint32_t)E.e * (4 * EVOBS_SLOTS) + (uint32_t)seat * EVOBS_SLOTS +
-                         (g.events_len & 63u);
+    // 64 x (type, rel actor, token), oldest first, padded (0,0,37): slot i
+    // of the window is ring entry (len + i) & 63 of the observer's
+    // pre-encoded stream (Engine::emit), pads while i < 64 - len; pack 4
+    // triples into 3 words with byte permutes
+    const uint32_t* ob = S.evobs + (uint32_t)E.e * (4 * EVOBS_SLOTS) + (uint32_t)seat * EVOBS_SLOTS;
+    const uint32_t len = g.events_len;
+    const int pad = len >= 64u ? 0 : 64 - (int)len;
+    auto slot = [&](int i) -> uint32_t { return i < pad ? EVOBS_PAD : ob[(len + (uint32_t)i) & 63u]; };
     uint4* dst = reinterpret_cast<uint4*>(obs.event_tokens + o * 192);
 #pragma unroll
     for (int q = 0; q < 4; q++) {
       uint32_t w[12];
 #pragma unroll
       for (int r = 0; r < 4; r++) {
-        const uint32_t a = ob[16 * q + 4 * r], b = ob[16 * q + 4 * r + 1], c = ob[16 * q + 4 * r + 2],
-                       d = ob[16 * q + 4 * r + 3];
+        const int i0 = 16 * q + 4 * r;
+        const uint32_t a = slot(i0), b = slot(i0 + 1), c = slot(i0 + 2), d = slot(i0 + 3);
         w[3 * r] = byte_perm(a, b, 0x4210);
         w[3 * r + 1] = byte_perm(b, c, 0x5421);
         w[3 * r + 2] = byte_perm(c, d, 0x6542);
@@ -277,7 +280,6 @@ RS_COLD void import_env(Engine& E, const rs_env_rec& r) {
   g.step_count = (uint32_t)r.step_count; g.terminated = r.terminated; g.truncated = r.truncated;
   const int cnt = r.events_len < 64 ? r.events_len : 64;
   g.events_len = (uint32_t)(r.events_len - cnt);
-  E.clear_event_window();
   for (int i = 0; i < cnt; i++) E.emit(r.events[i][0], r.events[i][1], r.events[i][2]);
   g.n_results = r.n_results;
   S.results[E.e] = r.last_result;

@@ -19,7 +19,7 @@
 namespace rs {
 
 constexpr int WALL_STRIDE = 144;  // 136 tiles padded to 9 x 16 B
-constexpr int EVOBS_SLOTS = 2 * RS_EVENT_WINDOW;           // doubled window
+constexpr int EVOBS_SLOTS = RS_EVENT_WINDOW;                 // per observer
 constexpr int EVOBS_BYTES = 4 * EVOBS_SLOTS * 4;             // per env
 constexpr uint32_t EVOBS_PAD = 37u << 16;                    // (0, 0, 37)
 
@@ -38,10 +38,9 @@ struct Soa {
   uint32_t* minfo;   // [4 seat][4 meld][n] type | n | from | called
   uint16_t* river;   // [4 seat][40][n] tile | flags << 8
   uint16_t* events;  // [n][64] ring (128 B per env): type | (actor+1) << 4 | (tile+1) << 7
-  // [n][4 observer][128] the same events pre-encoded for each observer as
-  // observe() emits them (type token, relative actor, visible tile token)
-  // and written twice (slot p and p + 64): the last 64 events of any
-  // observer are then the contiguous slots [len & 63, (len & 63) + 64)
+  // [n][4 observer][64] the same ring pre-encoded for each observer as
+  // observe() emits it (type token, relative actor, visible tile token);
+  // observe() reads the window slots (len + i) & 63 and synthesizes pads
   uint32_t* evobs;
   uint32_t* legal;   // [4][n] env-view legal mask
   rs_result_rec* results;  // [n] last kyoku result (written at kyoku end)
