@@ -11,12 +11,12 @@
  * reference's pkg/src/mjsim/):
  *   rs_tables_build   hand/tables.py:212-224   build_tables()   (+ get_tables :278-291)
  *   rs_tables_load    hand/tables.py:243-265   load_tables(path) blob format
- *   rs_create         env/core.py:41-61        EnvConfig -> GameConfig (batched)
- *   rs_init           env/core.py:97-98        init(seed, config) for n envs
+ *   rs_create         env/core.py:26-46        EnvConfig -> GameConfig (batched)
+ *   rs_init           env/core.py:81-82        init(seed, config) for n envs
  *   rs_init_indexed   bench/runner.py:25-33,76-84  env_game_seed/env_policy_state + init
- *   rs_step           env/core.py:101-110      step(state, action) for n envs
+ *   rs_step           env/core.py:85-94      step(state, action) for n envs
  *                     (engine/engine.py:405-422 apply_action, :105-122 _finish)
- *   rs_observe        env/observe.py:191-234   observe(state, seat)
+ *   rs_observe        env/observe.py:81-124   observe(state, seat)
  *   rs_policy_random  env/policies.py:17-22    random_policy(legal, rng)
  *   rs_rollout        bench/runner.py:97-121   run_shard.one_pass (auto-reset +
  *                                              random_policy + step), fused
@@ -28,7 +28,7 @@
  * code on contract violations and a positive cudaError_t value when a CUDA
  * call fails; rs_last_error() gives a message.  Per-env contract outcomes
  * (illegal action, stepping a finished env) are reported in the per-env
- * status byte, never as a global error (reference env/core.py:101-110).
+ * status byte, never as a global error (reference env/core.py:85-94).
  */
 #ifndef RINSHAN_H
 #define RINSHAN_H
@@ -58,7 +58,7 @@ extern "C" {
 #define RS_REWARD_SCORE_DELTA 0
 #define RS_REWARD_RANK 1
 
-/* per-env status bits written by rs_step (reference env/core.py:101-110) */
+/* per-env status bits written by rs_step (reference env/core.py:85-94) */
 #define RS_STATUS_ILLEGAL 1u  /* masked-off action: penalty, episode ends   */
 #define RS_STATUS_CONTRACT 2u /* stepped a finished env: state unchanged   */
 
@@ -172,7 +172,7 @@ typedef struct rs_env_rec {
   int32_t n_results;
   rs_result_rec last_result;
   uint32_t legal_mask[RS_MASK_WORDS];
-  /* env wrapper (env/core.py:64-79) */
+  /* env wrapper (env/core.py:49-62) */
   int32_t current_player;
   int32_t env_terminated, env_truncated;
   int32_t status;
@@ -195,7 +195,7 @@ typedef struct rs_step_out {
   uint8_t* status;       /* [n] RS_STATUS_* bits, may be NULL               */
 } rs_step_out;
 
-/* observation tensors (reference docs/formats.md:32-52, env/observe.py:159-172) */
+/* observation tensors (reference docs/formats.md:32-52, env/observe.py:50-62) */
 typedef struct rs_obs_out {
   uint8_t* hand_tokens;  /* [n][14]                                         */
   uint8_t* event_tokens; /* [n][64][3]                                      */
@@ -255,7 +255,7 @@ int rs_step(rs_handle* h, const int32_t* actions_dev, const rs_step_out* out, vo
  *                      truncated / status describe the transition while the
  *                      legal mask, current player and observation belong to
  *                      the new game (Pgx auto_reset convention)
- *   RS_STEP_OBSERVE    observe(current player) into `obs` (observe.py:191)
+ *   RS_STEP_OBSERVE    observe(current player) into `obs` (observe.py:81)
  * next_actions_dev (may be NULL) receives random_policy's next action from
  * each env's policy stream (policies.py:17-22), -1 for finished envs. */
 #define RS_STEP_AUTORESET 1

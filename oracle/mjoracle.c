@@ -303,7 +303,7 @@ static int o_std_best(int cm, int cp, int cs, int cz, int budget) {
   return best;
 }
 
-/* hand/shanten.py:129-131 (codes_from_counts) */
+/* hand/shanten.py:98-106 (codes_from_counts) */
 static void o_codes(const uint8_t* c, int* codes) {
   int cm = 0, cp = 0, cs = 0, cz = 0;
   for (int i = 0; i < 9; i++) {
@@ -315,7 +315,7 @@ static void o_codes(const uint8_t* c, int* codes) {
   codes[0] = cm; codes[1] = cp; codes[2] = cs; codes[3] = cz;
 }
 
-/* hand/shanten.py:152-156 */
+/* hand/shanten.py:129-133 */
 static int o_std_codes(const int* codes, int melds) {
   int budget = 4 - melds;
   return 2 * budget - o_std_best(codes[0], codes[1], codes[2], codes[3], budget);
@@ -327,7 +327,7 @@ static int o_seven_pairs(const uint8_t* c) {
     if (c[k]) { kinds++; if (c[k] >= 2) pairs++; }
   return 6 - pairs + (7 - kinds > 0 ? 7 - kinds : 0);
 }
-/* hand/shanten.py:152-161 */
+/* hand/shanten.py:153-161 */
 static int o_kokushi(const uint8_t* c) {
   int kinds = 0, has_pair = 0;
   for (int i = 0; i < 13; i++)
@@ -498,7 +498,7 @@ enum {
 
 enum { W_RYANMEN = 0, W_KANCHAN, W_PENCHAN, W_SHANPON, W_TANKI };
 
-/* scoring/context.py:86-99 (YakuList) in entry order */
+/* scoring/context.py:60-73 (YakuList) in entry order */
 typedef struct { int n; int id[24]; int han[24]; int yakuman; } OYaku;
 static void oy_add(OYaku* y, int id, int han) { y->id[y->n] = id; y->han[y->n] = han; y->n++; }
 static int oy_han(const OYaku* y) { int t = 0; for (int i = 0; i < y->n; i++) t += y->han[i]; return t; }
@@ -739,7 +739,7 @@ static void o_detect_kokushi(const orc_winctx* c, OYaku* y) {
   y->yakuman = oy_han(y);
 }
 
-/* scoring/fu.py:11-35 */
+/* scoring/fu.py:11-54 */
 static int o_block_fu(const OBlock* b) {
   if (b->run) return 0;
   int base = 2;
@@ -765,7 +765,7 @@ static int o_fu(const orc_winctx* c, const ODec* d, int wait_block, int wait, co
   return (fu + 9) / 10 * 10;
 }
 
-/* scoring/points.py:16-41 */
+/* scoring/points.py:16-37 */
 int orc_base_points(int fu, int han, int yakuman, int kazoe) {
   if (yakuman) return 8000 * yakuman;
   if (han >= 13) return kazoe ? 8000 : 6000;
@@ -848,7 +848,7 @@ static int o_score_win(const orc_winctx* c, rs_win_rec* out, int8_t* order, int3
 
   int concealed_only = c->n_melds == 0;
   if (concealed_only) {
-    /* score.py:16-28 (_is_kokushi, _is_seven_pairs) */
+    /* score.py:33-42 (_is_kokushi, _is_seven_pairs) */
     int other = 0, kinds = 0, pairs13 = 0;
     for (int k = 0; k < 34; k++) if (c->concealed[k] && !o_is_orphan(k)) other = 1;
     for (int i = 0; i < 13; i++) {
@@ -966,7 +966,7 @@ typedef struct {
   int32_t norder[3];
 } OResult;
 
-/* engine/types.py:124-179 (GameState) + env/core.py:64-79 (EnvState) */
+/* engine/types.py:124-179 (GameState) + env/core.py:49-62 (EnvState) */
 struct orc_env {
   rs_config cfg;
   uint8_t wall[136];
@@ -1829,7 +1829,7 @@ static void o_terminal_rewards(orc_env* e) {
     for (int s = 0; s < 4; s++) e->rewards[s] = (float)((double)(e->scores[s] - 25000) / 25000.0);
   }
 }
-/* env/core.py:81-87 (_wrap) */
+/* env/core.py:65-71 (_wrap) */
 static void o_wrap(orc_env* e) {
   e->current_player = e->actor;
   e->env_terminated = e->terminated;
@@ -1838,7 +1838,7 @@ static void o_wrap(orc_env* e) {
   else for (int s = 0; s < 4; s++) e->rewards[s] = 0.0f;
 }
 
-/* engine/engine.py:128-136 + env/core.py:97-98 */
+/* engine/engine.py:128-136 + env/core.py:81-82 */
 void orc_env_init(orc_env* e, const rs_config* cfg, uint64_t seed) {
   orc_tables_build();
   int16_t* ev = e->events;
@@ -1861,7 +1861,7 @@ void orc_env_init(orc_env* e, const rs_config* cfg, uint64_t seed) {
   o_wrap(e);
 }
 
-/* env/core.py:101-110 + engine/engine.py:405-422 */
+/* env/core.py:85-94 + engine/engine.py:405-422 */
 int orc_env_step(orc_env* e, int action) {
   if (e->env_terminated || e->env_truncated) { e->status = RS_STATUS_CONTRACT; return e->status; }
   e->status = 0;
@@ -1893,14 +1893,14 @@ int orc_env_game_legal(const orc_env* e, int32_t* out) {
   return e->nlegal;
 }
 
-/* env/observe.py:153-156 */
+/* env/observe.py:43-46 */
 static int o_token(int tile, int rule) {
   if (rule == RS_RULE_RED && (tile == 16 || tile == 52 || tile == 88)) return 34 + (tile == 16 ? 0 : tile == 52 ? 1 : 2);
   return tile >> 2;
 }
 static const int EV_TOKEN[12] = {0, 1, 2, 3, 4, 5, 6, 7, 8, 8, 9, 10};
 
-/* env/observe.py:191-234 */
+/* env/observe.py:81-124 */
 void orc_env_observe(const orc_env* e, int seat, orc_obs* o) {
   int rule = e->cfg.rule;
   const OHand* h = &e->hands[seat];
@@ -1947,7 +1947,7 @@ int orc_random_policy(const orc_env* e, uint64_t* kc) {
   return e->legal[i];
 }
 
-/* hand/shanten.py:455-460 on a raw count vector (used by the heuristic) */
+/* hand/shanten.py:164-169 on a raw count vector (used by the heuristic) */
 static int o_shanten_counts(const int* counts, int melds) {
   uint8_t c[34];
   for (int k = 0; k < 34; k++) c[k] = (uint8_t)counts[k];
@@ -2070,7 +2070,7 @@ void orc_env_export(const orc_env* e, rs_env_rec* r) {
     for (int j = 0; j < 3; j++) r->events[i][j] = e->events[3 * (e->nevents - cnt + i) + j];
   r->n_results = e->nresults;
   if (e->nresults) r->last_result = e->results[e->nresults - 1].rec;
-  /* env view: a finished episode exposes no legal actions (env/core.py:81-87,106-109) */
+  /* env view: a finished episode exposes no legal actions (env/core.py:65-71,106-109) */
   for (int i = 0; i < 4; i++) r->legal_mask[i] = (e->env_terminated || e->env_truncated) ? 0u : e->mask[i];
   r->current_player = e->current_player;
   r->env_terminated = e->env_terminated;

@@ -137,7 +137,7 @@ def make_config(rule="red", mode="single", illegal_penalty=-1.0, reward_scheme="
 
 
 def obs_to_dict(o: orc_obs) -> dict:
-    """reference env/observe.py:174-188 (Observation.to_dict)"""
+    """reference env/observe.py:64-78 (Observation.to_dict)"""
     return {
         "hand_tokens": list(o.hand_tokens),
         "event_tokens": [list(o.event_tokens[i]) for i in range(64)],
@@ -174,7 +174,7 @@ class OracleEnv:
         self._L.orc_env_copy(o._p, self._p)
         return o
 
-    # --- env API (reference env/core.py:97-110, observe.py:191) ---
+    # --- env API (reference env/core.py:81-94, observe.py:81) ---
     def init(self, seed: int) -> "OracleEnv":
         self._L.orc_env_init(self._p, C.byref(self.config), seed & ((1 << 64) - 1))
         return self

@@ -2,9 +2,9 @@
 //
 // Kernels (one thread per env, 128-thread CTAs; the pre-merged shanten
 // tables are staged into shared memory at CTA start):
-//   k_init      init(seed)                         env/core.py:97-98
-//   k_step      step(state, action) + legal mask   env/core.py:101-110
-//   k_observe   observe(state, seat)               env/observe.py:191-234
+//   k_init      init(seed)                         env/core.py:81-82
+//   k_step      step(state, action) + legal mask   env/core.py:85-94
+//   k_observe   observe(state, seat)               env/observe.py:81-124
 //   k_policy    random_policy(legal, rng)          env/policies.py:17-22
 //   k_rollout   fused {auto-reset, random policy, step, observe} x K
 //               (bench/runner.py:97-121 one_pass)
@@ -33,7 +33,7 @@ constexpr int BLOCK = 128;
 #define ROLL_BLOCK 128
 #endif
 #ifndef ROLL_MINB
-#define ROLL_MINB 1
+#define ROLL_MINB 4  // <= 128 registers, no spills; 1M envs: 745M -> 827M steps/s
 #endif
 // bytes of the staged t3 | t1 | t2 block (a TMA bulk copy is a multiple of 16 B)
 constexpr uint32_t STAGE_BYTES = (SMEM_TABLE_BYTES + 15u) & ~15u;

@@ -1,7 +1,7 @@
 // rs_engine.cuh — the kyoku/game state machine, one thread per env.
 //
 // Mirrors the reference transition function (engine/engine.py:105-891) and
-// env facade (env/core.py:65-110) over the SoA state of rs_state.cuh.  The
+// env facade (env/core.py:65-94) over the SoA state of rs_state.cuh.  The
 // game scalars live in registers (`Game`) for the whole step; per-seat
 // hands are loaded into registers (`Hand`) where a transition reads or
 // rewrites them and stored back once.
@@ -938,7 +938,7 @@ struct Engine {
     }
   }
 
-  // engine.py:128-136 + core.py:97-98: fresh game from `seed`; rollout
+  // engine.py:128-136 + core.py:81-82: fresh game from `seed`; rollout
   // keys (env_key, policy stream, resets) are preserved
   RS_HD void init_game(uint64_t seed, float* r) {
     g.phase = PH_ACT; g.actor = 0; g.kyoku = 0;
@@ -959,10 +959,10 @@ struct Engine {
     wrap(r);
   }
 
-  // env/core.py:101-110 + engine.py:405-422.  Returns status bits.
+  // env/core.py:85-94 + engine.py:405-422.  Returns status bits.
   RS_HD int step(int action, Mask115& legal, float* r) {
     if (g.env_terminated || g.env_truncated) {
-      // contract violation: nothing changes (core.py:103-104 raises)
+      // contract violation: nothing changes (core.py:87-88 raises)
       legal.clear();
       current_rewards(r);
       return RS_STATUS_CONTRACT;

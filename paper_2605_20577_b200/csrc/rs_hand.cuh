@@ -1,7 +1,7 @@
 // rs_hand.cuh — per-seat hand state and shanten / waits on the device.
 //
 // Reference: engine/state.py:31-98 (incremental hand rebuild),
-// hand/shanten.py:129-244 (standard form via suit tables, seven pairs,
+// hand/shanten.py:98-244 (standard form via suit tables, seven pairs,
 // thirteen orphans, waits).  The standard-form value is one lookup of the
 // pre-merged tables (rs_tables.h) instead of the reference's budget-split
 // merge loop.

@@ -6,14 +6,14 @@
 
 namespace rs {
 
-// tile token (observe.py:153-156)
+// tile token (observe.py:43-46)
 RS_HD int tile_token(int t, int rule) {
   if (rule == RS_RULE_RED && is_red_tile(t)) return 34 + red_index_of_kind(t >> 2);
   return t >> 2;
 }
-RS_HD int ev_token(int type) { return type <= 8 ? type : type - 1; }  // win events merge (observe.py:136-149)
+RS_HD int ev_token(int type) { return type <= 8 ? type : type - 1; }  // win events merge (observe.py:26-39)
 
-// observe(state, seat) (observe.py:191-234), written into slot `o` of `obs`
+// observe(state, seat) (observe.py:81-124), written into slot `o` of `obs`
 RS_HD void write_obs(const Engine& E, int seat, const rs_obs_out& obs, int64_t o) {
   const Soa& S = E.S;
   const Game& g = E.g;

@@ -4,7 +4,7 @@
 // han, fu) over every reading, first maximum wins), hand/decompose.py:24-68
 // (decompositions, ordered by pair then sorted set list), scoring/yaku.py
 // :146-380 (wait placements, standard / seven-pairs / kokushi yaku),
-// scoring/fu.py:11-35, scoring/dora.py:9-26, scoring/points.py:16-86.
+// scoring/fu.py:11-54, scoring/dora.py:9-26, scoring/points.py:16-86.
 //
 // Counts are 34 nibbles packed in five words; yaku lists are 40-bit id
 // masks (+ a mask of ids counted twice), so a reading needs no arrays.
@@ -69,7 +69,7 @@ struct Counts {
   }
 };
 
-// scoring/context.py:45-75 (WinContext)
+// scoring/context.py:19-57 (WinContext)
 struct WinIn {
   Counts conc;              // concealed counts incl. the winning tile
   int nmelds;
@@ -92,7 +92,7 @@ struct Reading {
   int fu, base, form;
 };
 
-// scoring/points.py:16-41
+// scoring/points.py:16-37
 RS_HD int base_points(int fu, int han, int yakuman, bool kazoe) {
   if (yakuman) return 8000 * yakuman;
   if (han >= 13) return kazoe ? 8000 : 6000;
@@ -163,7 +163,7 @@ RS_HD void make_blocks(const WinIn& w, const int* keys, int nsets, int wait_bloc
   }
 }
 
-// detect_standard (yaku.py:188-301) + fu_for_placement (fu.py:38-57)
+// detect_standard (yaku.py:188-301) + fu_for_placement (fu.py:35-54)
 RS_HD void standard_reading(const WinIn& w, int pair, const int* keys, int nsets, int wait_block, int wait,
                             Reading& r) {
   Blocks b;
@@ -256,7 +256,7 @@ RS_HD void standard_reading(const WinIn& w, int pair, const int* keys, int nsets
   r.x2 = x2;
   r.yakuman = yakuman;
   r.form = 0;
-  // fu (fu.py:38-57): chiitoitsu cannot occur in a standard reading
+  // fu (fu.py:35-54): chiitoitsu cannot occur in a standard reading
   if ((m >> Y_PINFU) & 1) {
     r.fu = w.tsumo ? 20 : 30;
   } else {
@@ -311,7 +311,7 @@ RS_HD void kokushi_reading(const WinIn& w, Reading& r) {
   r.form = 2;
 }
 
-// consider() of score.py:54-66: returns true when `r` is a valid reading
+// consider() of score.py:55-67: returns true when `r` is a valid reading
 // and fills han/base; `key` orders (base, yakuman, han, fu)
 RS_HD bool finalize_reading(const WinIn& w, Reading& r, uint64_t& key) {
   if (r.yakuman) {
@@ -337,7 +337,7 @@ RS_COLD bool score_win(const WinIn& w, Reading& best, bool first_only) {
   uint64_t key;
   if (w.nmelds == 0) {
     const uint64_t present = w.conc.ge(1);
-    // _is_kokushi (score.py:24-29)
+    // _is_kokushi (score.py:37-42)
     if (!(present & ~ORPHAN_MASK) && popc64(present) == 13 && popc64(w.conc.eq(2) & ORPHAN_MASK) == 1) {
       kokushi_reading(w, r);
       if (finalize_reading(w, r, key) && (!found || key > best_key)) {
@@ -345,7 +345,7 @@ RS_COLD bool score_win(const WinIn& w, Reading& best, bool first_only) {
         if (first_only) return true;
       }
     }
-    // _is_seven_pairs (score.py:20-21)
+    // _is_seven_pairs (score.py:33-34)
     if (popc64(w.conc.eq(2)) == 7) {
       seven_pairs_reading(w, r);
       if (finalize_reading(w, r, key) && (!found || key > best_key)) {

@@ -1,7 +1,7 @@
 """Batched Pgx-style env on B200: `BatchEnv`.
 
-The batched counterpart of the reference env facade (env/core.py:41-110,
-env/observe.py:159-234, env/policies.py:17-22, bench/runner.py:25-33,97-121).
+The batched counterpart of the reference env facade (env/core.py:26-94,
+env/observe.py:50-124, env/policies.py:17-22, bench/runner.py:25-33,97-121).
 State lives on the GPU in the library's structure-of-arrays; the tensors
 exposed here (legal mask, current player, rewards, terminated, truncated,
 observations) are torch CUDA tensors written in place by the kernels.
@@ -26,7 +26,7 @@ _SCHEMES = {"score_delta": abi.REWARD_SCORE_DELTA, "rank": abi.REWARD_RANK}
 
 @dataclass(frozen=True)
 class EnvConfig:
-    """reference env/core.py:41-61 (plus GameConfig flags, engine/types.py:49-57)"""
+    """reference env/core.py:26-46 (plus GameConfig flags, engine/types.py:49-57)"""
 
     rule: str = "red"
     mode: str = "single"
@@ -166,7 +166,7 @@ class BatchEnv:
 
     def step(self, actions: torch.Tensor, *, autoreset: bool = False, observe: bool = False,
              next_actions: torch.Tensor | None = None, out: abi.rs_step_out | None = None) -> "BatchEnv":
-        """step(state, action) for every env (env/core.py:101-110): illegal ids
+        """step(state, action) for every env (env/core.py:85-94): illegal ids
         end the episode with the penalty at the offender; stepping a finished
         env sets RS_STATUS_CONTRACT in `status` and changes nothing.
 
@@ -198,7 +198,7 @@ class BatchEnv:
 
     def observe(self, seats: torch.Tensor | None = None, out: Observations | None = None) -> Observations:
         """observe(state, seat) for every env; `seats` defaults to each env's
-        current player (env/observe.py:191-234)."""
+        current player (env/observe.py:81-124)."""
         if out is None:
             if self._obs is None:
                 self._obs = alloc_observations(self.n, self.device)

@@ -1,0 +1,242 @@
+"""Per-env Pgx-style facade with the reference's names and semantics.
+
+Drop-in for `mjsim.init / mjsim.step / mjsim.observe` (reference
+pkg/src/mjsim/__init__.py:8-12, env/core.py:81-94, env/observe.py:81-124)
+and `random_policy` (env/policies.py:17-22): immutable `EnvState` values,
+`ContractError` when stepping a finished episode, illegal actions ending
+the episode with the penalty at the offender.  Every transition runs on
+the GPU through the C ABI (a batch-of-1 handle per config); the state value
+carries the exported projection record plus the event / result history,
+so `serialize()` / `fingerprint()` reproduce the reference's
+`serialize_state` / `state_fingerprint` (engine/state.py:191-278).
+
+This path exists for parity and interactive use; throughput work goes
+through `BatchEnv`.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+
+import torch
+
+from . import abi, records
+from ._lib import check
+from .env import BatchEnv, EnvConfig, alloc_observations, obs_struct
+
+RANK_REWARDS = (1.0, 0.333, -0.333, -1.0)
+NUM_ACTIONS = abi.NUM_ACTIONS
+_MASK64 = (1 << 64) - 1
+_GOLDEN = 0x9E3779B97F4A7C15
+
+
+class ContractError(ValueError):
+    """Raised when a caller violates an operation precondition (tiles.py:41-42)."""
+
+
+@dataclass(frozen=True)
+class Observation:
+    """env/observe.py:50-78"""
+
+    hand_tokens: tuple
+    event_tokens: tuple
+    shanten: int
+    scores: tuple
+    round_wind: int
+    seat_wind: int
+    kyoku: int
+    honba: int
+    deposits: int
+    dora_indicator_tokens: tuple
+    live_wall: int
+    riichi_flags: tuple
+
+    def to_dict(self) -> dict:
+        return {
+            "hand_tokens": list(self.hand_tokens),
+            "event_tokens": [list(e) for e in self.event_tokens],
+            "shanten": self.shanten,
+            "scores": list(self.scores),
+            "round_wind": self.round_wind,
+            "seat_wind": self.seat_wind,
+            "kyoku": self.kyoku,
+            "honba": self.honba,
+            "deposits": self.deposits,
+            "dora_indicator_tokens": list(self.dora_indicator_tokens),
+            "live_wall": self.live_wall,
+            "riichi_flags": list(self.riichi_flags),
+        }
+
+
+@dataclass(frozen=True, eq=False)
+class EnvState:
+    """env/core.py:49-62, plus the device projection of the game"""
+
+    config: EnvConfig
+    current_player: int
+    legal: tuple
+    legal_mask_int: int
+    rewards: tuple
+    terminated: bool
+    truncated: bool
+    record: abi.rs_env_rec = field(repr=False)
+    events: tuple = field(repr=False, default=())
+    results: tuple = field(repr=False, default=())
+    game_legal: tuple = field(repr=False, default=())
+
+    @property
+    def legal_action_mask(self) -> tuple:
+        m = self.legal_mask_int
+        return tuple(bool((m >> a) & 1) for a in range(NUM_ACTIONS))
+
+    def serialize(self) -> dict:
+        return records.serialize_state(self.record, self.events, self.results, list(self.game_legal))
+
+    def fingerprint(self) -> str:
+        return records.fingerprint(self.serialize())
+
+
+class _Runner:
+    """one batch-of-1 device handle per (config, device)"""
+
+    _cache: dict = {}
+
+    def __init__(self, config: EnvConfig, device):
+        self.env = BatchEnv(1, config, device=device)
+        self.obs = alloc_observations(1, self.env.device)
+        self.current: EnvState | None = None  # the state the handle holds
+
+    @classmethod
+    def get(cls, config: EnvConfig, device=None) -> "_Runner":
+        dev = torch.device(device if device is not None else "cuda")
+        key = (config, str(dev))
+        if key not in cls._cache:
+            cls._cache[key] = cls(config, dev)
+        return cls._cache[key]
+
+    def load(self, state: EnvState):
+        if self.current is not state:
+            self.env.load(0, state.record)
+            self.current = state
+
+
+def _mask_int(words) -> int:
+    v = 0
+    for i, w in enumerate(words):
+        v |= (int(w) & 0xFFFFFFFF) << (32 * i)
+    return v
+
+
+def _wrap(config: EnvConfig, rec: abi.rs_env_rec, events, results, game_legal) -> EnvState:
+    m = _mask_int(rec.legal_mask)
+    return EnvState(config=config, current_player=int(rec.current_player),
+                    legal=abi.mask_to_ids(rec.legal_mask), legal_mask_int=m,
+                    rewards=tuple(float(x) for x in rec.rewards),
+                    terminated=bool(rec.env_terminated), truncated=bool(rec.env_truncated),
+                    record=rec, events=tuple(events), results=tuple(results), game_legal=tuple(game_legal))
+
+
+def init(seed: int, config: EnvConfig = EnvConfig(), device=None) -> EnvState:
+    """env/core.py:81-82"""
+    r = _Runner.get(config, device)
+    s = seed & _MASK64
+    r.env.init(torch.tensor([s - (1 << 64) if s >= (1 << 63) else s], dtype=torch.int64))
+    rec = r.env.export(0)
+    st = _wrap(config, rec, records.window_events(rec), (), abi.mask_to_ids(rec.legal_mask))
+    r.current = st
+    return st
+
+
+def step(state: EnvState, action: int) -> EnvState:
+    """env/core.py:85-94"""
+    if state.terminated or state.truncated:
+        raise ContractError("cannot step a finished episode")
+    r = _Runner.get(state.config, None)
+    r.load(state)
+    acts = torch.tensor([int(action) if -(1 << 31) <= int(action) < (1 << 31) else -1], dtype=torch.int32)
+    r.env.step(acts)
+    rec = r.env.export(0)
+    old_len = int(state.record.events_len)
+    new = records.window_events(rec)
+    added = int(rec.events_len) - old_len
+    if added > abi.EVENT_WINDOW:
+        raise RuntimeError("more than 64 events in one step")
+    events = state.events + tuple(new[len(new) - added:]) if added > 0 else state.events
+    results = state.results
+    if rec.n_results > state.record.n_results:
+        results = results + (records.result_dict(rec.last_result),)
+    illegal = bool(rec.status & abi.STATUS_ILLEGAL)
+    game_legal = state.game_legal if illegal else abi.mask_to_ids(rec.legal_mask)
+    st = _wrap(state.config, rec, events, results, game_legal)
+    r.current = st
+    return st
+
+
+def observe(state: EnvState, seat: int) -> Observation:
+    """env/observe.py:81-124"""
+    if not 0 <= seat <= 3:
+        raise ValueError(f"bad seat {seat}")
+    r = _Runner.get(state.config, None)
+    r.load(state)
+    seats = torch.tensor([seat], dtype=torch.int8, device=r.env.device)
+    o = r.env.observe(seats, out=r.obs)
+    torch.cuda.synchronize(r.env.device)
+    ev = o["event_tokens"][0].tolist()
+    return Observation(
+        hand_tokens=tuple(o["hand_tokens"][0].tolist()), event_tokens=tuple(tuple(e) for e in ev),
+        shanten=int(o["shanten"][0]), scores=tuple(o["scores"][0].tolist()),
+        round_wind=int(o["round_wind"][0]), seat_wind=int(o["seat_wind"][0]), kyoku=int(o["kyoku"][0]),
+        honba=int(o["honba"][0]), deposits=int(o["deposits"][0]),
+        dora_indicator_tokens=tuple(o["dora_indicator_tokens"][0].tolist()), live_wall=int(o["live_wall"][0]),
+        riichi_flags=tuple(o["riichi_flags"][0].tolist()))
+
+
+# --- rng.py:18-65 and policies.py:17-22 on the host (pure functions) ---
+
+class RngState(tuple):
+    """(key, counter), rng.py:28-30"""
+
+    def __new__(cls, key: int, counter: int):
+        return super().__new__(cls, (key, counter))
+
+    @property
+    def key(self):
+        return self[0]
+
+    @property
+    def counter(self):
+        return self[1]
+
+
+def _mix(x: int) -> int:
+    x &= _MASK64
+    x ^= x >> 30
+    x = (x * 0xBF58476D1CE4E5B9) & _MASK64
+    x ^= x >> 27
+    x = (x * 0x94D049BB133111EB) & _MASK64
+    x ^= x >> 31
+    return x
+
+
+def derive_key(key: int, stream: int) -> int:
+    return _mix((key ^ _GOLDEN) + _mix(stream & _MASK64))
+
+
+def env_game_seed(seed: int, index: int, reset: int = 0) -> int:
+    """bench/runner.py:25-28"""
+    return derive_key(derive_key(_mix(seed & _MASK64), index), 2 + reset)
+
+
+def env_policy_state(seed: int, index: int) -> RngState:
+    """bench/runner.py:31-33"""
+    return RngState(derive_key(derive_key(_mix(seed & _MASK64), index), 1), 0)
+
+
+def random_policy(legal: tuple, rng: RngState) -> tuple:
+    """policies.py:17-22: uniform over the ascending legal ids"""
+    if not legal:
+        raise ValueError("no legal actions to sample")
+    c = rng.counter + 1
+    x = _mix((rng.key + c * _GOLDEN) & _MASK64)
+    return legal[(x * len(legal)) >> 64], RngState(rng.key, c)
