@@ -253,9 +253,144 @@ def make_traces():
     dump("traces.json.gz", games)
 
 
+# ---------------------------------------------------------------------------
+# crafted engine scenarios: every apply_action made by the reference's own
+# engine tests (tests/test_engine.py, tests/test_engine_rounds.py), recorded
+# as (pre-state record, action, post-state projection | exception)
+
+def state_record(gs) -> dict:
+    """GameState -> the fields of rs_env_rec (include/rinshan.h)"""
+    cfg = gs.config
+    hands = []
+    for h in gs.hands:
+        hands.append({
+            "concealed": list(h.concealed), "n_concealed": len(h.concealed), "n_melds": len(h.melds),
+            "melds": [{"type": m.type, "n_tiles": len(m.tiles), "from_seat": m.from_seat, "tiles": list(m.tiles),
+                       "called_tile": m.called_tile} for m in h.melds],
+            "river_tile": [rt.tile for rt in h.river],
+            "river_flags": [int(rt.tsumogiri) | (2 * int(rt.riichi)) | (4 * int(rt.called)) for rt in h.river],
+            "n_river": len(h.river), "riichi": h.riichi, "riichi_index": h.riichi_index, "ippatsu": int(h.ippatsu),
+            "temp_furiten": int(h.temp_furiten), "perm_furiten": int(h.perm_furiten), "shanten": h.shanten,
+            "waits": sum(1 << k for k in h.waits),
+        })
+    ev = gs.events()
+    win = ev[-64:]
+    mask = gs.legal_mask if not (gs.terminated or gs.truncated) else 0
+    return {
+        "cfg": {"rule": cfg.rule, "mode": cfg.mode, "reward_scheme": 0, "illegal_penalty": -1.0,
+                "max_steps": cfg.max_steps, "kazoe": int(cfg.kazoe), "double_yakuman": int(cfg.double_yakuman),
+                "agari_yame": int(cfg.agari_yame), "renchan_cap": cfg.renchan_cap},
+        "wall": list(gs.wall.tiles), "cursor": gs.wall.cursor, "kan_draws": gs.wall.kan_draws,
+        "dora_count": gs.wall.dora_count, "hands": hands, "scores": list(gs.scores), "kyoku": gs.kyoku,
+        "honba": gs.honba, "deposits": gs.deposits, "repeats": gs.repeats, "phase": gs.phase, "actor": gs.actor,
+        "drawn": gs.drawn, "riichi_pending": int(gs.riichi_pending), "rinshan_pending": int(gs.rinshan_pending),
+        "call_tile": gs.call_tile, "call_from": gs.call_from, "n_queue": len(gs.call_queue),
+        "queue_seat": [s for s, _ in gs.call_queue], "queue_stage": [t for _, t in gs.call_queue],
+        "n_rons": len(gs.call_rons), "rons": list(gs.call_rons), "call_chankan": int(gs.call_chankan),
+        "kakan_kind": gs.kakan_kind, "pending_dora": gs.pending_dora, "four_kan_pending": int(gs.four_kan_pending),
+        "any_call_made": int(gs.any_call_made), "rng_key": gs.rng.key, "rng_counter": gs.rng.counter,
+        "step_count": gs.step_count, "terminated": int(gs.terminated), "truncated": int(gs.truncated),
+        "events_len": len(ev), "events": [list(e) for e in win], "n_results": len(gs.results),
+        "legal_mask": [(mask >> (32 * i)) & 0xFFFFFFFF for i in range(4)],
+        "current_player": gs.actor, "env_terminated": int(gs.terminated), "env_truncated": int(gs.truncated),
+    }
+
+
+def state_projection(gs) -> dict:
+    """the same projection tests/paritylib.projection computes from records"""
+    from mjsim.engine.state import _result_dict, serialize_state
+    d = serialize_state(gs)
+    d.pop("events")
+    d.pop("results")
+    d["legal"] = list(gs.legal) if not (gs.terminated or gs.truncated) else []
+    if gs.terminated or gs.truncated:
+        rewards = [(s - 25000) / 25000 for s in gs.scores]
+    else:
+        rewards = [0.0] * 4
+    mask = gs.legal_mask if not (gs.terminated or gs.truncated) else 0
+    d["internal"] = {
+        "repeats": gs.repeats, "riichi_pending": int(gs.riichi_pending),
+        "rinshan_pending": int(gs.rinshan_pending), "call_tile": gs.call_tile, "call_from": gs.call_from,
+        "queue": [list(q) for q in gs.call_queue], "rons": list(gs.call_rons),
+        "call_chankan": int(gs.call_chankan), "kakan_kind": gs.kakan_kind, "pending_dora": gs.pending_dora,
+        "four_kan_pending": int(gs.four_kan_pending), "any_call_made": int(gs.any_call_made),
+        "rng": [gs.rng.key, gs.rng.counter], "events_len": len(gs.events()), "n_results": len(gs.results),
+        "hands": [{"riichi_index": h.riichi_index, "temp_furiten": int(h.temp_furiten),
+                   "perm_furiten": int(h.perm_furiten), "waits": sum(1 << k for k in h.waits)} for h in gs.hands],
+        "legal_mask": [(mask >> (32 * i)) & 0xFFFFFFFF for i in range(4)],
+        "current_player": gs.actor, "env_terminated": int(gs.terminated), "env_truncated": int(gs.truncated),
+        "rewards": [float(round(r, 9)) for r in rewards],
+    }
+    d["window"] = [list(e) for e in gs.events()[-64:]]
+    d["last_result"] = _result_dict(gs.results[-1]) if gs.results else None
+    return d
+
+
+def make_scenarios():
+    import engine_helpers
+    import test_engine
+    import test_engine_rounds
+    from mjsim.engine import engine as eng
+    from mjsim.engine.state import state_fingerprint as fp
+
+    seen = {}
+    per_test = {}
+    out = []
+    real_apply = eng.apply_action
+    current = {"test": None}
+
+    def recording_apply(state, action):
+        key = (fp(state), int(action))
+        exc = None
+        try:
+            nxt = real_apply(state, action)
+            post, err = state_projection(nxt), None
+        except Exception as e:  # IllegalActionError / ContractError
+            nxt, post, err, exc = None, None, type(e).__name__, e
+        per_test[current["test"]] = per_test.get(current["test"], 0) + 1
+        # keep every transition of the crafted scenarios, cap the long random
+        # plays some tests run (the traces fixture covers those)
+        if key not in seen and per_test[current["test"]] <= 80:
+            seen[key] = True
+            out.append({"test": current["test"], "pre": state_record(state), "action": int(action),
+                        "post": post, "error": err})
+        if exc is not None:
+            raise exc
+        return nxt
+
+    test_engine.apply_action = recording_apply
+    test_engine_rounds.apply_action = recording_apply
+    tables = get_tables()
+    import inspect
+    for mod in (test_engine, test_engine_rounds):
+        for cname, cls in inspect.getmembers(mod, inspect.isclass):
+            if not cname.startswith("Test"):
+                continue
+            for mname, meth in inspect.getmembers(cls, inspect.isfunction):
+                if not mname.startswith("test_"):
+                    continue
+                current["test"] = f"{mod.__name__}::{cname}::{mname}"
+                obj = cls()
+                args = ["tables"] if "tables" in inspect.signature(meth).parameters else []
+                try:
+                    meth(obj, *[tables for _ in args])
+                except Exception as e:  # a reference test that fails here is simply not harvested
+                    print("  (skipped)", current["test"], type(e).__name__, e)
+    by_test = {}
+    for s in out:
+        by_test[s["test"]] = by_test.get(s["test"], 0) + 1
+    print(f"scenarios: {len(out)} transitions from {len(by_test)} tests")
+    dump("scenarios.json.gz", out)
+
+
 if __name__ == "__main__":
+    if len(sys.argv) > 1:
+        for name in sys.argv[1:]:
+            globals()[f"make_{name}"]()
+        sys.exit(0)
     make_rng()
     make_tables()
     make_shanten()
     make_scoring()
     make_traces()
+    make_scenarios()

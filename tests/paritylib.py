@@ -28,3 +28,59 @@ def diff(a: dict, b: dict, path: str = "") -> list[str]:
         elif va != vb:
             out.append(f"{path}{k}: {str(va)[:200]} != {str(vb)[:200]}")
     return out
+
+
+def record_from_dict(d: dict):
+    """rs_env_rec from the JSON dict of tests/golden/make_golden.state_record"""
+    from paper_2605_20577_b200 import abi
+
+    r = abi.rs_env_rec()
+    r.abi_version = 1
+    for k, v in d["cfg"].items():
+        setattr(r.cfg, k, v)
+    for i, t in enumerate(d["wall"]):
+        r.wall[i] = t
+    for s, h in enumerate(d["hands"]):
+        hr = r.hands[s]
+        for i, t in enumerate(h["concealed"]):
+            hr.concealed[i] = t
+        hr.n_concealed, hr.n_melds = h["n_concealed"], h["n_melds"]
+        for i, m in enumerate(h["melds"]):
+            mr = hr.melds[i]
+            mr.type, mr.n_tiles, mr.from_seat, mr.called_tile = m["type"], m["n_tiles"], m["from_seat"], m["called_tile"]
+            for j, t in enumerate(m["tiles"]):
+                mr.tiles[j] = t
+        for i, (t, f) in enumerate(zip(h["river_tile"], h["river_flags"])):
+            hr.river_tile[i], hr.river_flags[i] = t, f
+        hr.n_river = h["n_river"]
+        for k in ("riichi", "riichi_index", "ippatsu", "temp_furiten", "perm_furiten", "shanten", "waits"):
+            setattr(hr, k, h[k])
+    for k in ("cursor", "kan_draws", "dora_count", "kyoku", "honba", "deposits", "repeats", "phase", "actor",
+              "drawn", "riichi_pending", "rinshan_pending", "call_tile", "call_from", "n_queue", "n_rons",
+              "call_chankan", "kakan_kind", "pending_dora", "four_kan_pending", "any_call_made", "rng_key",
+              "rng_counter", "step_count", "terminated", "truncated", "events_len", "n_results", "current_player",
+              "env_terminated", "env_truncated"):
+        setattr(r, k, d[k])
+    for i, v in enumerate(d["scores"]):
+        r.scores[i] = v
+    for i, (s, t) in enumerate(zip(d["queue_seat"], d["queue_stage"])):
+        r.queue_seat[i], r.queue_stage[i] = s, t
+    for i, s in enumerate(d["rons"]):
+        r.rons[i] = s
+    for i, ev in enumerate(d["events"]):
+        for j in range(3):
+            r.events[i][j] = ev[j]
+    for i, w in enumerate(d["legal_mask"]):
+        r.legal_mask[i] = w
+    return r
+
+
+def normalize(d: dict) -> dict:
+    """JSON round trip (tuples -> lists) and rewards as float32 values"""
+    import json
+    import struct
+
+    d = json.loads(json.dumps(d))
+    if d and "internal" in d:
+        d["internal"]["rewards"] = [struct.unpack("f", struct.pack("f", x))[0] for x in d["internal"]["rewards"]]
+    return d
