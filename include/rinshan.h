@@ -289,6 +289,12 @@ int rs_import_env(rs_handle* h, int64_t env, const rs_env_rec* in);
  * win, result, env */
 int rs_record_sizes(int32_t* out /*[6]*/);
 
+/* profiling hook: a fused rollout recording, per env and step, the clock64
+ * cycles of the auto-reset and of policy + step + observe, the action and
+ * flags into prof_dev[steps][n][4] (u32) */
+int rs_debug_rollout_cycles(rs_handle* h, int32_t steps, const rs_obs_out* obs, uint32_t* prof_dev,
+                            void* stream);
+
 #ifdef __cplusplus
 }
 #endif

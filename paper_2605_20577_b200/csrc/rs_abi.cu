@@ -30,11 +30,14 @@ constexpr int BLOCK = 128;
 // k_rollout CTA shape: one staged table copy is shared by ROLL_BLOCK
 // threads; ROLL_MINB CTAs per SM caps the registers (occupancy)
 #ifndef ROLL_BLOCK
-#define ROLL_BLOCK 128
+#define ROLL_BLOCK 256  // large batches: 2 CTAs x 8 warps per SM
 #endif
 #ifndef ROLL_MINB
-#define ROLL_MINB 4  // <= 128 registers, no spills; 1M envs: 745M -> 827M steps/s
+#define ROLL_MINB 2  // <= 128 registers, no spills
 #endif
+// dynamic shared memory of a CTA: staged tables + one 144-byte wall slot
+// per thread for the deal (rs_engine.cuh start_kyoku)
+constexpr int smem_for(int block) { return WALL_SLOT_OFF + block * WALL_STRIDE; }
 // bytes of the staged t3 | t1 | t2 block (a TMA bulk copy is a multiple of 16 B)
 constexpr uint32_t STAGE_BYTES = (SMEM_TABLE_BYTES + 15u) & ~15u;
 
@@ -205,7 +208,7 @@ __device__ __forceinline__ int env_of_thread(int gtid, int epw) {
   return lane < epw ? (gtid >> 5) * epw + lane : -1;
 }
 
-__global__ void __launch_bounds__(BLOCK) k_step(const __grid_constant__ Soa S, const __grid_constant__ DevTables D,
+__global__ void __launch_bounds__(ROLL_BLOCK, ROLL_MINB) k_step(const __grid_constant__ Soa S, const __grid_constant__ DevTables D,
     const __grid_constant__ Cfg C, const int32_t* actions, int flags, rs_obs_out obs, int32_t* next_actions,
     StepOut out, int epw) {
   const Tabs T = stage_tables(D);
@@ -268,7 +271,8 @@ __global__ void __launch_bounds__(BLOCK) k_observe(const __grid_constant__ Soa S
 __global__ void __launch_bounds__(ROLL_BLOCK, ROLL_MINB) k_rollout(const __grid_constant__ Soa S, const __grid_constant__ DevTables D,
     const __grid_constant__ Cfg C, int steps, rs_obs_out obs,
                                                    int obs_slots, int16_t* actions_log, rs_rollout_stats* stats,
-                                                   uint64_t* digests, StepOut out, int epw) {
+                                                   uint64_t* digests, StepOut out, int epw,
+                                                   uint32_t* prof) {
   const Tabs T = stage_tables(D);
   unsigned long long games = 0;
   const int lane = threadIdx.x & 31;
@@ -283,10 +287,13 @@ __global__ void __launch_bounds__(ROLL_BLOCK, ROLL_MINB) k_rollout(const __grid_
     Mask115 m;
     int st = 0;
     for (int t = 0; t < steps; t++) {
-      if (E.g.env_terminated || E.g.env_truncated) {  // runner.py:107-109
+      const long long t0 = prof ? clock64() : 0;
+      const bool reset = E.g.env_terminated || E.g.env_truncated;
+      if (reset) {  // runner.py:107-109
         E.g.resets++;
         E.init_game(derive_key(E.g.env_key, 2 + (uint64_t)E.g.resets), r);
       }
+      const long long t1 = prof ? clock64() : 0;
       const int a = E.random_action(E.load_legal());
       st = E.step(a, m, r);
       if (actions_log) actions_log[(size_t)t * S.n + e] = (int16_t)a;
@@ -295,6 +302,14 @@ __global__ void __launch_bounds__(ROLL_BLOCK, ROLL_MINB) k_rollout(const __grid_
       if (obs_slots > 0 && (obs_slots > 1 || t == steps - 1)) {
         const int slot = obs_slots > 1 ? t % obs_slots : 0;
         write_obs(E, E.g.current_player, obs, (int64_t)slot * S.n + e);
+      }
+      if (prof) {  // debug hook (rs_debug_rollout_cycles): reset / step+observe cycles, action
+        const long long t2 = clock64();
+        uint32_t* p = prof + ((size_t)t * S.n + e) * 4;
+        p[0] = (uint32_t)(t1 - t0);
+        p[1] = (uint32_t)(t2 - t1);
+        p[2] = (uint32_t)a | ((uint32_t)reset << 8);
+        p[3] = (uint32_t)E.g.phase | ((uint32_t)E.g.env_terminated << 4);
       }
     }
     E.store();
@@ -411,6 +426,22 @@ int warp_grid(const rs_handle* h, int epw, int block, int max_ctas) {
   return (int)std::min<int64_t>(ctas, max_ctas > 0 ? max_ctas : ctas);
 }
 
+// launch shape of the stepping kernels (k_step, k_rollout): 128-thread CTAs
+// while the batch fills under 8 warps per SM (spread over every SM), else
+// ROLL_BLOCK-thread CTAs; `persistent` caps the grid at the resident CTAs
+struct Launch {
+  int grid, block, smem, epw;
+};
+Launch step_launch(const rs_handle* h, bool persistent) {
+  Launch L;
+  L.epw = envs_per_warp(h);
+  const int64_t warps = (h->n + L.epw - 1) / L.epw;
+  L.block = warps * 32 >= (int64_t)h->num_sms * ROLL_BLOCK ? ROLL_BLOCK : BLOCK;
+  L.smem = smem_for(L.block);
+  L.grid = warp_grid(h, L.epw, L.block, persistent ? h->num_sms * h->rollout_ctas_per_sm * ROLL_BLOCK / L.block : 0);
+  return L;
+}
+
 StepOut step_out(rs_handle* h, const rs_step_out* o) {
   StepOut s{};
   if (!o) return s;
@@ -508,7 +539,7 @@ int rs_create(rs_handle** out, int64_t n_envs, const rs_config* cfg, int32_t dev
       {(void**)&S.hrkind, 32 * n},           {(void**)&S.mtiles, 64 * n},
       {(void**)&S.minfo, 64 * n},            {(void**)&S.river, 4 * RS_MAX_RIVER * 2 * n},
       {(void**)&S.events, 64 * 2 * n},       {(void**)&S.legal, 16 * n},
-      {(void**)&S.evobs, (size_t)EVOBS_BYTES * n},
+      {(void**)&S.evobs, (size_t)EVOBS_BYTES * n},  {(void**)&S.htok, 4 * 16 * n},
       {(void**)&S.results, sizeof(rs_result_rec) * n},
       {(void**)&h->legal_bits_tmp, 16 * n},  {(void**)&h->rec_dev, sizeof(rs_env_rec)},
   };
@@ -535,11 +566,11 @@ int rs_create(rs_handle** out, int64_t n_envs, const rs_config* cfg, int32_t dev
                            (const void*)k_observe, (const void*)k_rollout, (const void*)k_export,
                            (const void*)k_import, (const void*)k_autoreset};
   for (const void* k : kernels)
-    if ((err = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, h->D.smem)))
+    if ((err = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_for(ROLL_BLOCK))))
       return cleanup(err, "cudaFuncSetAttribute");
   if ((err = cudaDeviceGetAttribute(&h->num_sms, cudaDevAttrMultiProcessorCount, device)) ||
       (err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&h->rollout_ctas_per_sm, k_rollout, ROLL_BLOCK,
-                                                           h->D.smem)))
+                                                           smem_for(ROLL_BLOCK))))
     return cleanup(err, "occupancy query");
   if (h->rollout_ctas_per_sm < 1) h->rollout_ctas_per_sm = 1;
   const char* epw_env = getenv("RINSHAN_EPW");
@@ -559,14 +590,14 @@ int rs_destroy(rs_handle* h) {
 int rs_init(rs_handle* h, const uint64_t* seeds_dev, const rs_step_out* out, void* stream) {
   if (!h || !seeds_dev) return set_err(RS_E_ARG, "rs_init: null argument");
   cudaStream_t st = (cudaStream_t)stream;
-  k_init<<<grid_of(h->n), BLOCK, h->D.smem, st>>>(h->S, h->D, h->cfg, seeds_dev, 0, 0, 0, step_out(h, out));
+  k_init<<<grid_of(h->n), BLOCK, smem_for(BLOCK), st>>>(h->S, h->D, h->cfg, seeds_dev, 0, 0, 0, step_out(h, out));
   return finish_step_out(h, out, st);
 }
 
 int rs_init_indexed(rs_handle* h, uint64_t seed, int64_t index_base, const rs_step_out* out, void* stream) {
   if (!h) return set_err(RS_E_ARG, "rs_init_indexed: null handle");
   cudaStream_t st = (cudaStream_t)stream;
-  k_init<<<grid_of(h->n), BLOCK, h->D.smem, st>>>(h->S, h->D, h->cfg, nullptr, seed, index_base, 1,
+  k_init<<<grid_of(h->n), BLOCK, smem_for(BLOCK), st>>>(h->S, h->D, h->cfg, nullptr, seed, index_base, 1,
                                                   step_out(h, out));
   return finish_step_out(h, out, st);
 }
@@ -582,12 +613,9 @@ int rs_step_ex(rs_handle* h, const int32_t* actions_dev, int32_t flags, const rs
   cudaStream_t st = (cudaStream_t)stream;
   rs_obs_out o{};
   if (obs) o = *obs;
-  int grid, block;
-  const int epw = envs_per_warp(h);
-  block = BLOCK;
-  grid = warp_grid(h, epw, block, 0);
-  k_step<<<grid, block, h->D.smem, st>>>(h->S, h->D, h->cfg, actions_dev, flags, o, next_actions_dev,
-                                         step_out(h, out), epw);
+  const Launch L = step_launch(h, false);
+  k_step<<<L.grid, L.block, L.smem, st>>>(h->S, h->D, h->cfg, actions_dev, flags, o, next_actions_dev,
+                                          step_out(h, out), L.epw);
   return finish_step_out(h, out, st);
 }
 
@@ -615,20 +643,39 @@ int rs_rollout(rs_handle* h, int32_t steps, const rs_obs_out* obs, int32_t obs_s
   cudaStream_t st = (cudaStream_t)stream;
   rs_obs_out o{};
   if (obs) o = *obs;
-  // small batches: 32-thread CTAs spread the warps over every SM; large
-  // batches: a persistent grid of the resident CTA count (tables staged
-  // once per CTA, envs walked grid-stride)
-  const int epw = envs_per_warp(h), block = ROLL_BLOCK;
-  const int grid = warp_grid(h, epw, block, h->num_sms * h->rollout_ctas_per_sm);
-  k_rollout<<<grid, block, h->D.smem, st>>>(h->S, h->D, h->cfg, steps, o, obs ? obs_slots : 0,
-                                                     actions_log, stats_dev, digests_dev, step_out(h, out), epw);
+  // persistent grid of the resident CTA count (tables staged once per CTA,
+  // envs walked grid-stride)
+  const Launch L = step_launch(h, true);
+  k_rollout<<<L.grid, L.block, L.smem, st>>>(h->S, h->D, h->cfg, steps, o, obs ? obs_slots : 0, actions_log,
+                                             stats_dev, digests_dev, step_out(h, out), L.epw, nullptr);
   return finish_step_out(h, out, st);
 }
+
+// debug / profiling hook: one rollout of `steps` with per-env per-step
+// clock64 cycles of the auto-reset and of policy+step+observe, the action
+// and flags, into prof_dev[steps][n][4] (u32)
+int rs_debug_rollout_cycles(rs_handle* h, int32_t steps, const rs_obs_out* obs, uint32_t* prof_dev, void* stream) {
+  if (!h || !prof_dev || steps < 1) return set_err(RS_E_ARG, "rs_debug_rollout_cycles: bad arguments");
+  cudaStream_t st = (cudaStream_t)stream;
+  rs_obs_out o{};
+  if (obs) o = *obs;
+  const Launch L = step_launch(h, true);
+  k_rollout<<<L.grid, L.block, L.smem, st>>>(h->S, h->D, h->cfg, steps, o, obs ? 1 : 0, nullptr, nullptr, nullptr,
+                                             StepOut{}, L.epw, prof_dev);
+  CUDA_TRY(cudaGetLastError());
+  return 0;
+}
+
+#if defined(RS_PROFILE_MARKS)
+extern "C" int rs_debug_set_marks(void* marks) {
+  return (int)cudaMemcpyToSymbol(g_marks, &marks, sizeof(marks));
+}
+#endif
 
 int rs_autoreset(rs_handle* h, const rs_step_out* out, void* stream) {
   if (!h) return set_err(RS_E_ARG, "rs_autoreset: null handle");
   cudaStream_t st = (cudaStream_t)stream;
-  k_autoreset<<<grid_of(h->n), BLOCK, h->D.smem, st>>>(h->S, h->D, h->cfg, step_out(h, out));
+  k_autoreset<<<grid_of(h->n), BLOCK, smem_for(BLOCK), st>>>(h->S, h->D, h->cfg, step_out(h, out));
   return finish_step_out(h, out, st);
 }
 

@@ -58,6 +58,13 @@ RS_HD int ctz64(uint64_t x) {  // x != 0
   return __builtin_ctzll(x);
 #endif
 }
+RS_HD int clz32(uint32_t x) {  // x != 0
+#if defined(__CUDA_ARCH__)
+  return __clz((int)x);
+#else
+  return __builtin_clz(x);
+#endif
+}
 RS_HD uint64_t umulhi64(uint64_t a, uint64_t b) {
 #if defined(__CUDA_ARCH__)
   return __umul64hi(a, b);

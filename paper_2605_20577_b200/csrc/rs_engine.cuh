@@ -12,6 +12,21 @@
 
 namespace rs {
 
+// phase timestamps for build-time profiling experiments (-DRS_PROFILE_MARKS)
+#if defined(RS_PROFILE_MARKS) && defined(__CUDACC__)
+__device__ unsigned long long* g_marks;
+#endif
+#if defined(RS_PROFILE_MARKS) && defined(__CUDA_ARCH__)
+#define RS_MARK(i)                                                                         \
+  do {                                                                                       \
+    if (g_marks) g_marks[(size_t)(blockIdx.x * blockDim.x + threadIdx.x) * 8 + (i)] = clock64(); \
+  } while (0)
+#else
+#define RS_MARK(i) \
+  do {             \
+  } while (0)
+#endif
+
 enum : int { PH_ACT = 0, PH_CALL = 1, PH_GAME_END = 2 };
 enum : int { ST_RON = 0, ST_PONKAN = 1, ST_CHI = 2 };
 enum : int {
@@ -77,6 +92,7 @@ struct Engine {
     S.scores[e] = sc;
   }
   RS_HD int wall(int pos) const { return S.wall[(size_t)e * WALL_STRIDE + pos]; }
+  RS_HD int tok() const { return C.rule == RS_RULE_RED ? 1 : 0; }  // hand_put / hand_take token mode
   RS_HD uint32_t info(int s) const { return S.hinfo[at(s)]; }
   RS_HD void set_info(int s, uint32_t v) const { S.hinfo[at(s)] = v; }
   RS_HD uint64_t waits(int s) const { return S.hwaits[at(s)]; }
@@ -109,19 +125,38 @@ struct Engine {
   // ------------------------------------------------------ rng / dealing
   // engine.py:139-164 (_start_kyoku) with tiles.py:142-144 / rng.py:59-65
   RS_COLD void start_kyoku() {
+#if defined(__CUDA_ARCH__)
+    // the thread's own 144-byte slot after the staged tables (shared memory:
+    // the swap chain is a dependent load/store sequence, local memory would
+    // round-trip through a thrashed L1 / L2)
+    uint8_t* w = g_smem + WALL_SLOT_OFF + threadIdx.x * WALL_STRIDE;
+#else
     uint8_t w[WALL_STRIDE];
-#pragma unroll 8
-    for (int i = 0; i < 136; i++) w[i] = (uint8_t)i;
-    for (int i = 136; i < WALL_STRIDE; i++) w[i] = 0;
+#endif
+    {
+      uint32_t* w32 = reinterpret_cast<uint32_t*>(w);
+#pragma unroll
+      for (int i = 0; i < 34; i++) w32[i] = 0x03020100u + 0x04040404u * (uint32_t)i;
+      w32[34] = w32[35] = 0;
+    }
+    // Fisher-Yates (rng.py:59-65): the draws are counter-based, so five are
+    // computed ahead (independent multiplies) and then swapped in order
     uint64_t c = g.rng_counter;
-    for (int i = 135; i > 0; i--) {
-      c++;
-      const int j = (int)randbelow_from(stream_value(g.rng_key, c), (uint32_t)(i + 1));
-      const uint8_t t = w[i];
-      w[i] = w[j];
-      w[j] = t;
+    for (int i = 135; i > 0; i -= 5) {
+      int j[5];
+#pragma unroll
+      for (int u = 0; u < 5; u++)
+        j[u] = (int)randbelow_from(stream_value(g.rng_key, c + 1 + u), (uint32_t)(i - u + 1));
+      c += 5;
+#pragma unroll
+      for (int u = 0; u < 5; u++) {
+        const uint8_t t = w[i - u];
+        w[i - u] = w[j[u]];
+        w[j[u]] = t;
+      }
     }
     g.rng_counter = (uint32_t)c;
+    RS_MARK(2);
     uint4* dst = reinterpret_cast<uint4*>(S.wall + (size_t)e * WALL_STRIDE);
     const uint4* src = reinterpret_cast<const uint4*>(w);
 #pragma unroll
@@ -134,22 +169,19 @@ struct Engine {
       Hand h;
       h.w0 = h.w1 = h.w2 = h.w3 = h.w4 = 0;
       h.cm = h.cp = h.cs = h.cz = 0;
-      for (int r = 0; r < 3; r++)
-        for (int j = 0; j < 4; j++) {
-          const int t = w[16 * r + 4 * i + j];
-          h.set_word(t >> 5, h.word(t >> 5) | (1u << (t & 31)));
-          const int k = t >> 2;
-          h.set_code(kind_suit(k), h.code(kind_suit(k)) + kind_pow(k));
-        }
-      {
-        const int t = w[48 + i];
-        h.set_word(t >> 5, h.word(t >> 5) | (1u << (t & 31)));
-        const int k = t >> 2;
-        h.set_code(kind_suit(k), h.code(kind_suit(k)) + kind_pow(k));
+      // the seat's 4-tile blocks are aligned words of the wall
+      const uint32_t* w32 = reinterpret_cast<const uint32_t*>(w);
+#pragma unroll
+      for (int r = 0; r < 3; r++) {
+        const uint32_t q = w32[4 * r + i];
+#pragma unroll
+        for (int j = 0; j < 4; j++) deal_tile(h, (int)((q >> (8 * j)) & 255u));
       }
+      deal_tile(h, w[48 + i]);
       h.cls = class_of(T, 0, h.cm) | (class_of(T, 1, h.cp) << 8) | (class_of(T, 2, h.cs) << 16) |
               (class_of(T, 3, h.cz) << 24);
       h.info = hi::set_nconc(hi::set_riichi_index(0u, -1), 13);
+      tokens_from_set(h, C.rule == RS_RULE_RED);
       finish_hand(T, h);
       store_hand(S, e, s, h);
       S.hrkind[at(s)] = 0ull;
@@ -168,7 +200,9 @@ struct Engine {
     g.pending_dora = 0;
     g.four_kan_pending = 0;
     g.any_call_made = 0;
+    RS_MARK(3);
     draw(dealer);
+    RS_MARK(4);
   }
 
   // engine.py:167-178
@@ -177,7 +211,7 @@ struct Engine {
     h.info = hi::set_temp(h.info, 0);
     const int tile = wall(g.cursor);
     g.cursor++;
-    hand_put(T, h, tile);
+    hand_put(T, h, tile, tok());
     finish_hand(T, h);
     store_hand(S, e, seat, h);
     g.drawn = tile;
@@ -190,7 +224,7 @@ struct Engine {
   RS_HD void rinshan_draw(int seat, Hand& h) {
     const int tile = wall(135 - g.kan_draws);
     g.kan_draws++;
-    hand_put(T, h, tile);
+    hand_put(T, h, tile, tok());
     finish_hand(T, h);
     store_hand(S, e, seat, h);
     g.drawn = tile;
@@ -328,10 +362,10 @@ struct Engine {
   RS_COLD bool kan_keeps_waits(const Hand& h, int kind) const {
     const int melds = hi::nmelds(h.info);
     Hand before = h;
-    hand_take(T, before, before.lowest_of_kind(kind));
+    hand_take(T, before, before.lowest_of_kind(kind), -1);
     const uint64_t old = compute_waits(T, before, melds);
     Hand after = h;
-    for (int j = 0; j < 4; j++) hand_take(T, after, after.lowest_of_kind(kind));
+    for (int j = 0; j < 4; j++) hand_take(T, after, after.lowest_of_kind(kind), -1);
     const uint64_t nw = compute_waits(T, after, melds + 1);
     return old == nw && !((old >> kind) & 1);
   }
@@ -674,7 +708,7 @@ struct Engine {
     S.river[at(seat * RS_MAX_RIVER + nriver)] =
         (uint16_t)(tile | ((tsumogiri ? RS_RIVER_TSUMOGIRI : 0) | (declaring ? RS_RIVER_RIICHI : 0)) << 8);
     S.hrkind[at(seat)] |= 1ull << (tile >> 2);
-    hand_take(T, h, tile);
+    hand_take(T, h, tile, tok());
     h.info = hi::set_nriver(h.info, nriver + 1);
     h.info = hi::set_riichi(h.info, riichi_val);
     h.info = hi::set_riichi_index(h.info, riichi_index);
@@ -759,7 +793,7 @@ struct Engine {
       ids[n++] = h.lowest_of_kind(k0);
       ids[n++] = h.lowest_of_kind(k1);
     }
-    for (int j = 0; j < n; j++) hand_take(T, h, ids[j]);
+    for (int j = 0; j < n; j++) hand_take(T, h, ids[j], tok());
     ids[n] = g.call_tile;
     const int type = action == A_PON ? M_PON : (action == A_KAN_OPEN ? M_KAN_OPEN : M_CHI);
     add_meld(seat, h, type, ids, n + 1, g.call_tile, g.call_from);
@@ -788,7 +822,7 @@ struct Engine {
     int ids[4];
     uint32_t nib = h.nibble(kind);
     for (int j = 0; j < 4; j++) { ids[j] = 4 * kind + ctz32(nib); nib &= nib - 1; }
-    for (int j = 0; j < 4; j++) hand_take(T, h, ids[j]);
+    for (int j = 0; j < 4; j++) hand_take(T, h, ids[j], tok());
     add_meld(seat, h, M_KAN_CLOSED, ids, 4, -1, -1);
     finish_hand(T, h);
     store_hand(S, e, seat, h);
@@ -818,7 +852,7 @@ struct Engine {
           S.minfo[at(seat * 4 + i)] = mi::make(M_KAN_ADDED, 4, mi::from(mf), mi::called(mf));
         }
       }
-    hand_take(T, h, tile);
+    hand_take(T, h, tile, tok());
     finish_hand(T, h);
     store_hand(S, e, seat, h);
     g.any_call_made = 1;
@@ -941,6 +975,12 @@ struct Engine {
   // engine.py:128-136 + core.py:81-82: fresh game from `seed`; rollout
   // keys (env_key, policy stream, resets) are preserved
   RS_HD void init_game(uint64_t seed, float* r) {
+    {
+      const uint64_t ek = g.env_key, pk = g.policy_key, pc = g.policy_counter;
+      const uint32_t rs = g.resets;
+      g = Game{};
+      g.env_key = ek; g.policy_key = pk; g.policy_counter = pc; g.resets = rs;
+    }
     g.phase = PH_ACT; g.actor = 0; g.kyoku = 0;
     g.terminated = g.truncated = 0;
     g.env_terminated = g.env_truncated = 0;
@@ -952,9 +992,11 @@ struct Engine {
     for (int s = 0; s < 4; s++) g.scores[s] = 25000;
     g.rng_key = mix64(seed);
     g.rng_counter = 0;
+    RS_MARK(1);
     start_kyoku();
     Mask115 m;
     compute_legal(m);
+    RS_MARK(5);
     store_legal(m);
     wrap(r);
   }

@@ -19,6 +19,7 @@ struct Hand {
   uint32_t cls;                 // class byte per suit
   uint32_t info;                // hi:: flags
   uint64_t waits;
+  uint64_t tlo, thi;            // sorted observation tokens, 16 bytes, pad 37
 
   RS_HD uint32_t word(int i) const {
     return i == 0 ? w0 : i == 1 ? w1 : i == 2 ? w2 : i == 3 ? w3 : w4;
@@ -65,6 +66,9 @@ RS_HD Hand load_hand(const Soa& S, int e, int seat) {
   h.cls = S.hcls[s * n + x];
   h.info = S.hinfo[s * n + x];
   h.waits = S.hwaits[s * n + x];
+  const uint4 t = S.htok[s * n + x];
+  h.tlo = (uint64_t)t.x | ((uint64_t)t.y << 32);
+  h.thi = (uint64_t)t.z | ((uint64_t)t.w << 32);
   return h;
 }
 RS_HD void store_hand(const Soa& S, int e, int seat, const Hand& h) {
@@ -76,6 +80,88 @@ RS_HD void store_hand(const Soa& S, int e, int seat, const Hand& h) {
   S.hcls[s * n + x] = h.cls;
   S.hinfo[s * n + x] = h.info;
   S.hwaits[s * n + x] = h.waits;
+  S.htok[s * n + x] = make_uint4((uint32_t)h.tlo, (uint32_t)(h.tlo >> 32), (uint32_t)h.thi, (uint32_t)(h.thi >> 32));
+}
+
+// ---- sorted observation tokens (observe.py:89-90) kept incrementally ----
+// Tokens are < 128, so bytewise compares need no carries: (b | 0x80) - v
+// keeps the high bit exactly where b >= v.
+constexpr uint64_t TOK_PAD8 = 0x2525252525252525ull;  // 37 in every byte
+RS_HD int tok_rank(uint64_t lo, uint64_t hi, uint32_t v) {  // bytes < v
+  const uint64_t H = 0x8080808080808080ull, vv = 0x0101010101010101ull * v;
+  return 16 - popc64(((lo | H) - vv) & H) - popc64(((hi | H) - vv) & H);
+}
+RS_HD uint64_t low_bytes(int p) { return p <= 0 ? 0ull : (p >= 8 ? ~0ull : (~0ull >> (64 - 8 * p))); }
+RS_HD void tok_insert(uint64_t& lo, uint64_t& hi, uint32_t v) {
+  const int p = tok_rank(lo, hi, v);
+  if (p < 8) {
+    const uint64_t m = low_bytes(p), carry = lo >> 56;
+    lo = (lo & m) | ((uint64_t)v << (8 * p)) | ((lo & ~m) << 8);
+    hi = (hi << 8) | carry;
+  } else {
+    const uint64_t m = low_bytes(p - 8);
+    hi = (hi & m) | ((uint64_t)v << (8 * (p - 8))) | ((hi & ~m) << 8);
+  }
+}
+RS_HD void tok_remove(uint64_t& lo, uint64_t& hi, uint32_t v) {  // v present
+  const int p = tok_rank(lo, hi, v);
+  if (p < 8) {
+    const uint64_t m = low_bytes(p);
+    lo = (lo & m) | ((lo >> 8) & ~m) | (hi << 56);
+    hi = (hi >> 8) | (0x25ull << 56);
+  } else {
+    const uint64_t m = low_bytes(p - 8);
+    hi = (hi & m) | ((hi >> 8) & ~m) | (0x25ull << 56);
+  }
+}
+RS_HD uint32_t token_of(int t, bool red) {
+  return (red && is_red_tile(t)) ? (uint32_t)(34 + red_index_of_kind(t >> 2)) : (uint32_t)(t >> 2);
+}
+// from scratch (deal, import): walk the set from the highest id down and
+// shift each token in at the bottom, held red fives first (they sort last);
+// the 16-byte register ends sorted with the pads on top
+RS_HD void tokens_from_set(Hand& h, bool red) {
+  uint64_t lo = TOK_PAD8, hi = TOK_PAD8;
+  auto push = [&](uint32_t v) {
+    hi = (hi << 8) | (lo >> 56);
+    lo = (lo << 8) | v;
+  };
+  uint32_t w[5] = {h.w0, h.w1, h.w2, h.w3, h.w4};
+  if (red) {
+    if ((w[2] >> 24) & 1u) { push(36); w[2] &= ~(1u << 24); }  // tile 88
+    if ((w[1] >> 20) & 1u) { push(35); w[1] &= ~(1u << 20); }  // tile 52
+    if ((w[0] >> 16) & 1u) { push(34); w[0] &= ~(1u << 16); }  // tile 16
+  }
+#pragma unroll
+  for (int i = 4; i >= 0; i--) {
+    uint32_t x = w[i];
+    while (x) {
+      const int b = 31 - clz32(x);
+      x &= ~(1u << b);
+      push((uint32_t)((32 * i + b) >> 2));
+    }
+  }
+  h.tlo = lo;
+  h.thi = hi;
+}
+
+RS_HD uint32_t kind_pow(int k);  // below (staged table on the device)
+
+// branchless accumulation of one dealt tile into the set and the suit codes
+RS_HD void deal_tile(Hand& h, int t) {
+  const uint32_t bit = 1u << (t & 31);
+  const int wi = t >> 5;
+  h.w0 |= wi == 0 ? bit : 0u;
+  h.w1 |= wi == 1 ? bit : 0u;
+  h.w2 |= wi == 2 ? bit : 0u;
+  h.w3 |= wi == 3 ? bit : 0u;
+  h.w4 |= wi == 4 ? bit : 0u;
+  const int k = t >> 2, s = kind_suit(k);
+  const uint32_t p = kind_pow(k);
+  h.cm += s == 0 ? p : 0u;
+  h.cp += s == 1 ? p : 0u;
+  h.cs += s == 2 ? p : 0u;
+  h.cz += s == 3 ? p : 0u;
 }
 
 #if defined(__CUDACC__)
@@ -146,22 +232,52 @@ RS_HD int kokushi_shanten(const Hand& h) {
   const int has_pair = (h.kinds_ge(2) & ORPHAN_MASK) ? 1 : 0;
   return 13 - kinds - has_pair;
 }
+// seven pairs and thirteen orphans in one pass over the nibble counts,
+// without gathering kind masks: a nibble count c >= 1 (>= 2) sets bit 3 of
+// c + 7 (c + 6); orphan kinds select those bits per word
+RS_HD void special_shanten(const Hand& h, int& seven, int& kokushi) {
+  constexpr uint32_t OM[5] = {0x8u, 0x88u, 0x880u, 0x88888800u, 0x88u};
+  int kinds = 0, pairs = 0, okinds = 0;
+  uint32_t opair = 0;
+#pragma unroll
+  for (int w = 0; w < 5; w++) {
+    const uint32_t c = nib_counts(h.word(w));
+    const uint32_t pf = (c + 0x77777777u) & 0x88888888u, qf = (c + 0x66666666u) & 0x88888888u;
+    kinds += popc32(pf);
+    pairs += popc32(qf);
+    okinds += popc32(pf & OM[w]);
+    opair |= qf & OM[w];
+  }
+  seven = 6 - pairs + (7 - kinds > 0 ? 7 - kinds : 0);
+  kokushi = 13 - okinds - (opair ? 1 : 0);
+}
 // shanten_codes (shanten.py:172-182)
 RS_HD int full_shanten(const Tabs& T, const Hand& h, int melds) {
   int s = std_shanten_cls(T, h.cls, melds);
   if (melds == 0 && s > -1) {
-    const int sp = seven_pairs_shanten(h);
+    int sp, kk;
+    special_shanten(h, sp, kk);
     if (sp < s) s = sp;
-    if (s > -1) {
-      const int kk = kokushi_shanten(h);
-      if (kk < s) s = kk;
-    }
+    if (s > -1 && kk < s) s = kk;
   }
   return s;
 }
 
 // waits_from_codes (shanten.py:198-244) for a 13-form hand
-RS_COLD uint64_t compute_waits(const Tabs& T, const Hand& h, int melds) {
+RS_HD uint64_t compute_waits_impl(const Tabs& T, const Hand& h, int melds);
+// the hand crosses the call as scalars (registers), so the caller's Hand is
+// never materialised in local memory
+RS_COLD uint64_t compute_waits_s(const Tabs& T, uint32_t w0, uint32_t w1, uint32_t w2, uint32_t w3, uint32_t w4,
+                                 uint32_t cm, uint32_t cp, uint32_t cs, uint32_t cz, uint32_t cls, int melds) {
+  Hand h;
+  h.w0 = w0; h.w1 = w1; h.w2 = w2; h.w3 = w3; h.w4 = w4;
+  h.cm = cm; h.cp = cp; h.cs = cs; h.cz = cz; h.cls = cls;
+  return compute_waits_impl(T, h, melds);
+}
+RS_HD uint64_t compute_waits(const Tabs& T, const Hand& h, int melds) {
+  return compute_waits_s(T, h.w0, h.w1, h.w2, h.w3, h.w4, h.cm, h.cp, h.cs, h.cz, h.cls, melds);
+}
+RS_HD uint64_t compute_waits_impl(const Tabs& T, const Hand& h, int melds) {
   const int budget = 4 - melds, target = 2 * budget + 1;
   const int c0 = cls_byte(h.cls, 0), c1 = cls_byte(h.cls, 1), c2 = cls_byte(h.cls, 2), c3 = cls_byte(h.cls, 3);
   const int a_cur = t1_at(T, c0 * NS + c1), b_cur = t2_at(T, c2 * NH + c3);
@@ -212,27 +328,30 @@ RS_HD void finish_hand(const Tabs& T, Hand& h) {
 }
 
 // add / remove one tile without the rebuild (hand_add / hand_remove parts)
-RS_HD void hand_put(const Tabs& T, Hand& h, int t) {
+// tok: 0 no-red tokens, 1 red-rule tokens, -1 scratch copy (tokens unused)
+RS_HD void hand_put(const Tabs& T, Hand& h, int t, int tok) {
   const int k = t >> 2, s = kind_suit(k);
   h.set_word(t >> 5, h.word(t >> 5) | (1u << (t & 31)));
   const uint32_t nc = h.code(s) + kind_pow(k);
   h.set_code(s, nc);
   h.cls = (h.cls & ~(255u << (8 * s))) | (class_of(T, s, nc) << (8 * s));
   h.info = hi::set_nconc(h.info, hi::nconc(h.info) + 1);
+  if (tok >= 0) tok_insert(h.tlo, h.thi, token_of(t, tok == 1));
 }
-RS_HD void hand_take(const Tabs& T, Hand& h, int t) {
+RS_HD void hand_take(const Tabs& T, Hand& h, int t, int tok) {
   const int k = t >> 2, s = kind_suit(k);
   h.set_word(t >> 5, h.word(t >> 5) & ~(1u << (t & 31)));
   const uint32_t nc = h.code(s) - kind_pow(k);
   h.set_code(s, nc);
   h.cls = (h.cls & ~(255u << (8 * s))) | (class_of(T, s, nc) << (8 * s));
   h.info = hi::set_nconc(h.info, hi::nconc(h.info) - 1);
+  if (tok >= 0) tok_remove(h.tlo, h.thi, token_of(t, tok == 1));
 }
 
 // _shanten_minus_kind (engine.py:214-227)
-RS_COLD int shanten_minus_kind(const Tabs& T, const Hand& h, int k) {
+RS_HD int shanten_minus_kind(const Tabs& T, const Hand& h, int k) {
   Hand x = h;
-  hand_take(T, x, x.lowest_of_kind(k));
+  hand_take(T, x, x.lowest_of_kind(k), -1);
   return full_shanten(T, x, hi::nmelds(h.info));
 }
 

@@ -21,27 +21,9 @@ RS_HD void write_obs(const Engine& E, int seat, const rs_obs_out& obs, int64_t o
   const Hand h = load_hand(S, E.e, seat);
   if (obs.hand_tokens) {
     // sorted tokens (kinds ascending, then the held red fives 34..36), padded
-    // with 37, assembled in two registers and written as 7 u16 stores
-    uint64_t lo = 0x2525252525252525ull, hi8 = 0x2525252525252525ull;
-    int n = 0;
-    auto put = [&](uint32_t v) {
-      if (n < 8) lo = (lo & ~(0xFFull << (8 * n))) | ((uint64_t)v << (8 * n));
-      else hi8 = (hi8 & ~(0xFFull << (8 * (n - 8)))) | ((uint64_t)v << (8 * (n - 8)));
-      n++;
-    };
-    uint64_t present = h.kinds_ge(1);
-    while (present) {
-      const int k = ctz64(present);
-      present &= present - 1;
-      int c = h.count(k);
-      if (rule == RS_RULE_RED && red_index_of_kind(k) >= 0 && h.has(4 * k)) c--;
-      for (int j = 0; j < c; j++) put((uint32_t)k);
-    }
-    if (rule == RS_RULE_RED) {
-      if (h.has(16)) put(34);
-      if (h.has(52)) put(35);
-      if (h.has(88)) put(36);
-    }
+    // with 37: the hand keeps them sorted incrementally (rs_hand.cuh
+    // tok_insert / tok_remove); written as 7 u16 stores
+    const uint64_t lo = h.tlo, hi8 = h.thi;
     uint16_t* ht = reinterpret_cast<uint16_t*>(obs.hand_tokens + o * 14);
     ht[0] = (uint16_t)lo; ht[1] = (uint16_t)(lo >> 16); ht[2] = (uint16_t)(lo >> 32); ht[3] = (uint16_t)(lo >> 48);
     ht[4] = (uint16_t)hi8; ht[5] = (uint16_t)(hi8 >> 16); ht[6] = (uint16_t)(hi8 >> 32);
@@ -54,23 +36,28 @@ RS_HD void write_obs(const Engine& E, int seat, const rs_obs_out& obs, int64_t o
     const uint32_t* ob = S.evobs + (uint32_t)E.e * (4 * EVOBS_SLOTS) + (uint32_t)seat * EVOBS_SLOTS;
     const uint32_t len = g.events_len;
     const int pad = len >= 64u ? 0 : 64 - (int)len;
-    auto slot = [&](int i) -> uint32_t { return i < pad ? EVOBS_PAD : ob[(len + (uint32_t)i) & 63u]; };
     uint4* dst = reinterpret_cast<uint4*>(obs.event_tokens + o * 192);
+    auto emit_window = [&](auto slot) {
 #pragma unroll
-    for (int q = 0; q < 4; q++) {
-      uint32_t w[12];
+      for (int q = 0; q < 4; q++) {
+        uint32_t w[12];
 #pragma unroll
-      for (int r = 0; r < 4; r++) {
-        const int i0 = 16 * q + 4 * r;
-        const uint32_t a = slot(i0), b = slot(i0 + 1), c = slot(i0 + 2), d = slot(i0 + 3);
-        w[3 * r] = byte_perm(a, b, 0x4210);
-        w[3 * r + 1] = byte_perm(b, c, 0x5421);
-        w[3 * r + 2] = byte_perm(c, d, 0x6542);
+        for (int r = 0; r < 4; r++) {
+          const int i0 = 16 * q + 4 * r;
+          const uint32_t a = slot(i0), b = slot(i0 + 1), c = slot(i0 + 2), d = slot(i0 + 3);
+          w[3 * r] = byte_perm(a, b, 0x4210);
+          w[3 * r + 1] = byte_perm(b, c, 0x5421);
+          w[3 * r + 2] = byte_perm(c, d, 0x6542);
+        }
+        dst[3 * q] = make_uint4(w[0], w[1], w[2], w[3]);
+        dst[3 * q + 1] = make_uint4(w[4], w[5], w[6], w[7]);
+        dst[3 * q + 2] = make_uint4(w[8], w[9], w[10], w[11]);
       }
-      dst[3 * q] = make_uint4(w[0], w[1], w[2], w[3]);
-      dst[3 * q + 1] = make_uint4(w[4], w[5], w[6], w[7]);
-      dst[3 * q + 2] = make_uint4(w[8], w[9], w[10], w[11]);
-    }
+    };
+    if (pad == 0)  // a full window (every step after the first 64 events)
+      emit_window([&](int i) -> uint32_t { return ob[(len + (uint32_t)i) & 63u]; });
+    else
+      emit_window([&](int i) -> uint32_t { return i < pad ? EVOBS_PAD : ob[i - pad]; });
   }
   if (obs.shanten) obs.shanten[o] = (int8_t)hi::shanten(h.info);
   if (obs.scores)
@@ -246,6 +233,7 @@ RS_COLD void import_env(Engine& E, const rs_env_rec& r) {
     inf = hi::set_nriver(inf, hr.n_river);
     inf = hi::set_nconc(inf, hr.n_concealed);
     h.info = inf;
+    tokens_from_set(h, E.C.rule == RS_RULE_RED);
     for (int i = 0; i < hr.n_melds; i++) {
       const rs_meld_rec& m = hr.melds[i];
       uint32_t packed = 0;

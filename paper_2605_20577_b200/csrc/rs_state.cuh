@@ -32,6 +32,7 @@ struct Soa {
   uint32_t* hcode;   // [4 seat][4][n] base-5 codes m, p, s, z
   uint32_t* hcls;    // [4 seat][n]    table class per suit (4 x u8)
   uint32_t* hinfo;   // [4 seat][n]    packed HandState flags
+  uint4* htok;       // [4 seat][n]    sorted hand tokens (observe.py:89-90), pad 37, kept incrementally
   uint64_t* hwaits;  // [4 seat][n]    34-bit wait mask (13-form tenpai)
   uint64_t* hrkind;  // [4 seat][n]    kinds present in the river
   uint32_t* mtiles;  // [4 seat][4 meld][n] tile ids (4 x u8)
@@ -56,7 +57,7 @@ constexpr int64_t canonical_state_bytes() {
 }
 
 inline int64_t bytes_per_env() {
-  return 4 * 16 + 16 + WALL_STRIDE + 4 * 5 * 4 + 4 * 4 * 4 + 4 * 4 + 4 * 4 + 4 * 8 + 4 * 8 +
+  return 4 * 16 + 16 + WALL_STRIDE + 4 * 5 * 4 + 4 * 4 * 4 + 4 * 4 + 4 * 4 + 4 * 16 + 4 * 8 + 4 * 8 +
          4 * 4 * 4 + 4 * 4 * 4 + 4 * RS_MAX_RIVER * 2 + RS_EVENT_WINDOW * 2 + EVOBS_BYTES + 4 * 4 +
          (int64_t)sizeof(rs_result_rec);
 }

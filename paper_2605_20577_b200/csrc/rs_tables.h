@@ -36,6 +36,8 @@ constexpr int T1_OFF = T3_BYTES;
 constexpr int T2_OFF = T1_OFF + NS * NS;
 constexpr int POW_OFF = (T2_OFF + NS * NH + 3) & ~3;  // u32[34]: code delta per kind
 constexpr int SMEM_TABLE_BYTES = POW_OFF + 4 * 34;
+// per-thread 144-byte wall slots for the deal follow the tables
+constexpr int WALL_SLOT_OFF = (SMEM_TABLE_BYTES + 15) & ~15;
 
 struct HostTables {
   bool ready = false;
