@@ -291,7 +291,9 @@ int rs_record_sizes(int32_t* out /*[6]*/);
 
 /* profiling hook: a fused rollout recording, per env and step, the clock64
  * cycles of the auto-reset and of policy + step + observe, the action and
- * flags into prof_dev[steps][n][4] (u32) */
+ * flags into prof_dev[steps][n][4] (u32), followed by [n][4] u32 per env:
+ * %globaltimer (ns, low 32 bits) at kernel entry, after the table staging,
+ * at the env's first step and after its last step */
 int rs_debug_rollout_cycles(rs_handle* h, int32_t steps, const rs_obs_out* obs, uint32_t* prof_dev,
                             void* stream);
 

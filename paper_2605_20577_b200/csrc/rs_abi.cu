@@ -71,7 +71,16 @@ struct DevTables {
 // class-map pointers live in __constant__ memory of the module)
 struct DeviceTables {
   void* mem = nullptr;
+  size_t bytes = 0;
   DevTables D{};
+  // L2 residency of the whole table block (class maps + the staged image,
+  // ~2.1 MB of the 126 MB L2): the stepping kernels launch with an access
+  // policy window marking it persisting, so the class-map lookups and the
+  // per-CTA staging copy stay L2 hits even when everything else (the env
+  // state, a policy network between steps) streams through L2.
+  // RINSHAN_L2_PERSIST=0 turns it off.
+  cudaAccessPolicyWindow window{};
+  bool persist = false;
 };
 std::mutex g_dev_mu;
 DeviceTables g_dev_tables[64];
@@ -111,6 +120,25 @@ int device_tables(int device, DevTables* out) {
     dt.D.ns = NS; dt.D.nh = NH; dt.D.na = NA; dt.D.nb = NB;
     dt.D.smem = (int)STAGE_BYTES;
     dt.mem = mem;
+    dt.bytes = sz;
+    const char* pe = getenv("RINSHAN_L2_PERSIST");
+    int max_persist = 0, max_window = 0;
+    cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, device);
+    cudaDeviceGetAttribute(&max_window, cudaDevAttrMaxAccessPolicyWindowSize, device);
+    if (!(pe && pe[0] == '0') && max_persist > 0 && max_window > 0) {
+      size_t cur = 0;
+      cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize);
+      const size_t want = std::min((size_t)max_persist, std::max(cur, sz));
+      if (cur >= want || cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want) == cudaSuccess) {
+        dt.window.base_ptr = mem;
+        dt.window.num_bytes = std::min(sz, (size_t)max_window);
+        dt.window.hitRatio = 1.0f;
+        dt.window.hitProp = cudaAccessPropertyPersisting;
+        dt.window.missProp = cudaAccessPropertyStreaming;
+        dt.persist = true;
+      }
+      cudaGetLastError();  // a refused limit only disables the window
+    }
   }
   *out = dt.D;
   return 0;
@@ -155,6 +183,12 @@ __device__ __forceinline__ Tabs stage_tables(const DevTables& D) {
       "}\n" ::"r"(bar_addr)
       : "memory");
   return Tabs{};
+}
+
+__device__ __forceinline__ uint32_t globaltimer_lo() {
+  uint32_t t;
+  asm volatile("mov.u32 %0, %%globaltimer_lo;" : "=r"(t));
+  return t;
 }
 
 __device__ __forceinline__ void write_step_out(const StepOut& o, int e, const Engine& E, const Mask115& m,
@@ -273,7 +307,9 @@ __global__ void __launch_bounds__(ROLL_BLOCK, ROLL_MINB) k_rollout(const __grid_
                                                    int obs_slots, int16_t* actions_log, rs_rollout_stats* stats,
                                                    uint64_t* digests, StepOut out, int epw,
                                                    uint32_t* prof) {
+  const uint32_t g_entry = prof ? globaltimer_lo() : 0u;
   const Tabs T = stage_tables(D);
+  const uint32_t g_staged = prof ? globaltimer_lo() : 0u;
   unsigned long long games = 0;
   const int lane = threadIdx.x & 31;
   const int warps = (gridDim.x * blockDim.x) >> 5;
@@ -286,6 +322,7 @@ __global__ void __launch_bounds__(ROLL_BLOCK, ROLL_MINB) k_rollout(const __grid_
     float r[4] = {0.f, 0.f, 0.f, 0.f};
     Mask115 m;
     int st = 0;
+    const uint32_t g_first = prof ? globaltimer_lo() : 0u;
     for (int t = 0; t < steps; t++) {
       const long long t0 = prof ? clock64() : 0;
       const bool reset = E.g.env_terminated || E.g.env_truncated;
@@ -294,6 +331,7 @@ __global__ void __launch_bounds__(ROLL_BLOCK, ROLL_MINB) k_rollout(const __grid_
         E.init_game(derive_key(E.g.env_key, 2 + (uint64_t)E.g.resets), r);
       }
       const long long t1 = prof ? clock64() : 0;
+      RS_SMARK(0);
       const int a = E.random_action(E.load_legal());
       st = E.step(a, m, r);
       if (actions_log) actions_log[(size_t)t * S.n + e] = (int16_t)a;
@@ -303,6 +341,7 @@ __global__ void __launch_bounds__(ROLL_BLOCK, ROLL_MINB) k_rollout(const __grid_
         const int slot = obs_slots > 1 ? t % obs_slots : 0;
         write_obs(E, E.g.current_player, obs, (int64_t)slot * S.n + e);
       }
+      RS_SMARK(6);
       if (prof) {  // debug hook (rs_debug_rollout_cycles): reset / step+observe cycles, action
         const long long t2 = clock64();
         uint32_t* p = prof + ((size_t)t * S.n + e) * 4;
@@ -315,6 +354,11 @@ __global__ void __launch_bounds__(ROLL_BLOCK, ROLL_MINB) k_rollout(const __grid_
     E.store();
     if (digests) digests[e] = d;
     write_step_out(out, e, E, m, r, st);
+    RS_SMARK(7);
+    if (prof) {
+      uint32_t* p = prof + ((size_t)steps * S.n + e) * 4;
+      p[0] = g_entry; p[1] = g_staged; p[2] = g_first; p[3] = globaltimer_lo();
+    }
   }
   if (stats) {
     unsigned long long g = games;
@@ -387,6 +431,8 @@ struct rs_handle {
   int num_sms;
   int rollout_ctas_per_sm;  // resident k_rollout CTAs per SM (occupancy)
   int epw_override;         // RINSHAN_EPW (tuning experiments), 0 = heuristic
+  bool persist;             // launch with the tables' L2 persisting window
+  cudaAccessPolicyWindow window;
 };
 
 namespace {
@@ -440,6 +486,25 @@ Launch step_launch(const rs_handle* h, bool persistent) {
   L.smem = smem_for(L.block);
   L.grid = warp_grid(h, L.epw, L.block, persistent ? h->num_sms * h->rollout_ctas_per_sm * ROLL_BLOCK / L.block : 0);
   return L;
+}
+
+// launch with the table block's L2 access policy window (DeviceTables)
+template <typename... KArgs, typename... Args>
+cudaError_t launch_tables(const rs_handle* h, void (*kernel)(KArgs...), int grid, int block, int smem,
+                          cudaStream_t st, Args&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3((unsigned)grid);
+  cfg.blockDim = dim3((unsigned)block);
+  cfg.dynamicSmemBytes = (size_t)smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  if (h->persist) {
+    at[0].id = cudaLaunchAttributeAccessPolicyWindow;
+    at[0].val.accessPolicyWindow = h->window;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+  }
+  return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
 }
 
 StepOut step_out(rs_handle* h, const rs_step_out* o) {
@@ -527,6 +592,11 @@ int rs_create(rs_handle** out, int64_t n_envs, const rs_config* cfg, int32_t dev
   Soa& S = h->S;
   S.n = (int)n;
   const int trc = device_tables(device, &h->D);
+  if (trc == 0) {
+    std::lock_guard<std::mutex> lk(g_dev_mu);
+    h->persist = g_dev_tables[device].persist;
+    h->window = g_dev_tables[device].window;
+  }
   if (trc) {
     delete h;
     return trc;
@@ -614,8 +684,8 @@ int rs_step_ex(rs_handle* h, const int32_t* actions_dev, int32_t flags, const rs
   rs_obs_out o{};
   if (obs) o = *obs;
   const Launch L = step_launch(h, false);
-  k_step<<<L.grid, L.block, L.smem, st>>>(h->S, h->D, h->cfg, actions_dev, flags, o, next_actions_dev,
-                                          step_out(h, out), L.epw);
+  CUDA_TRY(launch_tables(h, k_step, L.grid, L.block, L.smem, st, h->S, h->D, h->cfg, actions_dev, flags, o,
+                         next_actions_dev, step_out(h, out), L.epw));
   return finish_step_out(h, out, st);
 }
 
@@ -646,8 +716,9 @@ int rs_rollout(rs_handle* h, int32_t steps, const rs_obs_out* obs, int32_t obs_s
   // persistent grid of the resident CTA count (tables staged once per CTA,
   // envs walked grid-stride)
   const Launch L = step_launch(h, true);
-  k_rollout<<<L.grid, L.block, L.smem, st>>>(h->S, h->D, h->cfg, steps, o, obs ? obs_slots : 0, actions_log,
-                                             stats_dev, digests_dev, step_out(h, out), L.epw, nullptr);
+  CUDA_TRY(launch_tables(h, k_rollout, L.grid, L.block, L.smem, st, h->S, h->D, h->cfg, steps, o,
+                         obs ? obs_slots : 0, actions_log, stats_dev, digests_dev, step_out(h, out), L.epw,
+                         nullptr));
   return finish_step_out(h, out, st);
 }
 
@@ -660,8 +731,8 @@ int rs_debug_rollout_cycles(rs_handle* h, int32_t steps, const rs_obs_out* obs, 
   rs_obs_out o{};
   if (obs) o = *obs;
   const Launch L = step_launch(h, true);
-  k_rollout<<<L.grid, L.block, L.smem, st>>>(h->S, h->D, h->cfg, steps, o, obs ? 1 : 0, nullptr, nullptr, nullptr,
-                                             StepOut{}, L.epw, prof_dev);
+  CUDA_TRY(launch_tables(h, k_rollout, L.grid, L.block, L.smem, st, h->S, h->D, h->cfg, steps, o, obs ? 1 : 0,
+                         nullptr, nullptr, nullptr, StepOut{}, L.epw, prof_dev));
   CUDA_TRY(cudaGetLastError());
   return 0;
 }

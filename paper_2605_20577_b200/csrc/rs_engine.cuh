@@ -16,15 +16,23 @@ namespace rs {
 #if defined(RS_PROFILE_MARKS) && defined(__CUDACC__)
 __device__ unsigned long long* g_marks;
 #endif
+// RS_PROFILE_MARKS=1: phases of init_game (RS_MARK); =2: phases of a step (RS_SMARK)
 #if defined(RS_PROFILE_MARKS) && defined(__CUDA_ARCH__)
-#define RS_MARK(i)                                                                         \
+#define RS_MARK_AT(i)                                                                        \
   do {                                                                                       \
     if (g_marks) g_marks[(size_t)(blockIdx.x * blockDim.x + threadIdx.x) * 8 + (i)] = clock64(); \
   } while (0)
 #else
-#define RS_MARK(i) \
-  do {             \
+#define RS_MARK_AT(i) \
+  do {                \
   } while (0)
+#endif
+#if defined(RS_PROFILE_MARKS) && RS_PROFILE_MARKS == 2
+#define RS_MARK(i) do {} while (0)
+#define RS_SMARK(i) RS_MARK_AT(i)
+#else
+#define RS_MARK(i) RS_MARK_AT(i)
+#define RS_SMARK(i) do {} while (0)
 #endif
 
 enum : int { PH_ACT = 0, PH_CALL = 1, PH_GAME_END = 2 };
@@ -714,6 +722,7 @@ struct Engine {
     h.info = hi::set_riichi_index(h.info, riichi_index);
     h.info = hi::set_ippatsu(h.info, ipp);
     finish_hand(T, h);
+    RS_SMARK(1);
     store_hand(S, e, seat, h);
     g.drawn = -1;
     g.rinshan_pending = 0;
@@ -721,7 +730,9 @@ struct Engine {
     reveal_pending_dora();
     if (!begin_call_phase(tile, seat, false)) {
       mark_passed_furiten(tile >> 2, seat);
+      RS_SMARK(2);
       discard_stands();
+      RS_SMARK(3);
     }
   }
 
@@ -1025,7 +1036,9 @@ struct Engine {
     if (g.phase == PH_CALL) apply_call_action(action);
     else apply_turn_action(action);
     if (!g.terminated && g.step_count >= (uint32_t)C.max_steps) g.truncated = 1;
+    RS_SMARK(4);
     compute_legal(legal);
+    RS_SMARK(5);
     store_legal(legal);
     wrap(r);
     return 0;
