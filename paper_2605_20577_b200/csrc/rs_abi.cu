@@ -37,6 +37,10 @@ constexpr int BLOCK = 128;
 #endif
 // dynamic shared memory of a CTA: staged tables + one 144-byte wall slot
 // per thread for the deal (rs_engine.cuh start_kyoku)
+// dynamic shared memory: the staged tables, then either one stage slot per
+// env of the CTA (staged stepping kernels) or a 144-byte shuffle scratch
+// per thread (kernels working on the blocks in HBM)
+constexpr int smem_staged(int slots) { return WALL_SLOT_OFF + slots * (int)SLOT_BYTES; }
 constexpr int smem_for(int block) { return WALL_SLOT_OFF + block * WALL_STRIDE; }
 // bytes of the staged t3 | t1 | t2 block (a TMA bulk copy is a multiple of 16 B)
 constexpr uint32_t STAGE_BYTES = (SMEM_TABLE_BYTES + 15u) & ~15u;
@@ -185,6 +189,50 @@ __device__ __forceinline__ Tabs stage_tables(const DevTables& D) {
   return Tabs{};
 }
 
+// --------------------------------------------------------------- stage
+// Each env a CTA works on owns a SLOT_BYTES slot after the staged tables
+// (rs_state.cuh): its 544-byte block moves HBM -> slot with one TMA bulk
+// copy completing on the slot's mbarrier, the step runs on shared memory,
+// and the block moves back with one bulk copy (bulk_group).
+__device__ __forceinline__ uint32_t slot_off(int slot) {
+  return (uint32_t)WALL_SLOT_OFF + (uint32_t)slot * SLOT_BYTES;
+}
+__device__ __forceinline__ uint32_t smem_addr(uint32_t off) {
+  return (uint32_t)__cvta_generic_to_shared(g_smem) + off;
+}
+// once per kernel and slot; the caller tracks the phase parity
+__device__ __forceinline__ void slot_bar_init(uint32_t sb) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(sb + SLOT_BAR)) : "memory");
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void stage_in(const Soa& S, int e, uint32_t sb, uint32_t phase) {
+  const uint32_t dst = smem_addr(sb), bar = smem_addr(sb + SLOT_BAR);
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(BLK_BYTES) : "memory");
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+               "l"(S.blk + (size_t)e * BLK_BYTES), "r"(BLK_BYTES), "r"(bar)
+               : "memory");
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(bar),
+      "r"(phase)
+      : "memory");
+}
+__device__ __forceinline__ void stage_out(const Soa& S, int e, uint32_t sb) {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic-proxy writes -> bulk copy
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(S.blk + (size_t)e * BLK_BYTES),
+               "r"(smem_addr(sb)), "r"(BLK_BYTES)
+               : "memory");
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+// the slot's previous stage_out has read shared memory (slot reusable)
+__device__ __forceinline__ void stage_wait_read() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+// every stage_out of this thread has completed
+__device__ __forceinline__ void stage_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+
 __device__ __forceinline__ uint32_t globaltimer_lo() {
   uint32_t t;
   asm volatile("mov.u32 %0, %%globaltimer_lo;" : "=r"(t));
@@ -209,7 +257,7 @@ __global__ void __launch_bounds__(BLOCK) k_init(const __grid_constant__ Soa S, c
   const Tabs T = stage_tables(D);
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= S.n) return;
-  Engine E(S, T, C, e);
+  Engine E(S, T, C, e, S.blk + (size_t)e * BLK_BYTES);
   uint64_t game_seed;
   if (indexed) {
     // bench/runner.py:25-33
@@ -244,11 +292,16 @@ __device__ __forceinline__ int env_of_thread(int gtid, int epw) {
 
 __global__ void __launch_bounds__(ROLL_BLOCK, ROLL_MINB) k_step(const __grid_constant__ Soa S, const __grid_constant__ DevTables D,
     const __grid_constant__ Cfg C, const int32_t* actions, int flags, rs_obs_out obs, int32_t* next_actions,
-    StepOut out, int epw) {
+    StepOut out, int epw, int staged) {
   const Tabs T = stage_tables(D);
   const int e = env_of_thread(blockIdx.x * blockDim.x + threadIdx.x, epw);
   if (e < 0 || e >= S.n) return;
-  Engine E(S, T, C, e);
+  const uint32_t sb = slot_off((threadIdx.x >> 5) * epw + (threadIdx.x & 31));
+  if (staged) {
+    slot_bar_init(sb);
+    stage_in(S, e, sb, 0);
+  }
+  Engine E(S, T, C, e, staged ? g_smem + sb : S.blk + (size_t)e * BLK_BYTES);
   E.load();
   Mask115 m;
   float r[4];
@@ -268,13 +321,17 @@ __global__ void __launch_bounds__(ROLL_BLOCK, ROLL_MINB) k_step(const __grid_con
     next_actions[e] = done ? -1 : E.random_action(m);
     dirty |= !done;
   }
-  if (dirty) E.store();
+  if (dirty) {
+    E.store();
+    if (staged) stage_out(S, e, sb);
+  }
   if (out.legal_bits) reinterpret_cast<uint4*>(out.legal_bits)[e] = make_uint4(m.m[0], m.m[1], m.m[2], m.m[3]);
   if (out.current_player) out.current_player[e] = (int8_t)E.g.current_player;
   if (out.rewards) reinterpret_cast<float4*>(out.rewards)[e] = make_float4(r[0], r[1], r[2], r[3]);
   if (out.terminated) out.terminated[e] = (uint8_t)term;
   if (out.truncated) out.truncated[e] = (uint8_t)trunc;
   if (out.status) out.status[e] = (uint8_t)st;
+  if (staged && dirty) stage_wait_all();
 }
 
 __global__ void __launch_bounds__(BLOCK) k_policy(const __grid_constant__ Soa S, const __grid_constant__ DevTables D,
@@ -282,7 +339,7 @@ __global__ void __launch_bounds__(BLOCK) k_policy(const __grid_constant__ Soa S,
   const Tabs T = stage_tables(D);
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= S.n) return;
-  Engine E(S, T, C, e);
+  Engine E(S, T, C, e, S.blk + (size_t)e * BLK_BYTES);
   E.load();
   if (E.g.env_terminated || E.g.env_truncated) { actions[e] = -1; return; }
   actions[e] = E.random_action(E.load_legal());
@@ -294,7 +351,7 @@ __global__ void __launch_bounds__(BLOCK) k_observe(const __grid_constant__ Soa S
   const Tabs T = stage_tables(D);
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= S.n) return;
-  Engine E(S, T, C, e);
+  Engine E(S, T, C, e, S.blk + (size_t)e * BLK_BYTES);
   E.load();
   write_obs(E, seats ? (int)seats[e] : E.g.current_player, obs, e);
 }
@@ -306,17 +363,25 @@ __global__ void __launch_bounds__(ROLL_BLOCK, ROLL_MINB) k_rollout(const __grid_
     const __grid_constant__ Cfg C, int steps, rs_obs_out obs,
                                                    int obs_slots, int16_t* actions_log, rs_rollout_stats* stats,
                                                    uint64_t* digests, StepOut out, int epw,
-                                                   uint32_t* prof) {
+                                                   uint32_t* prof, int staged) {
   const uint32_t g_entry = prof ? globaltimer_lo() : 0u;
   const Tabs T = stage_tables(D);
   const uint32_t g_staged = prof ? globaltimer_lo() : 0u;
   unsigned long long games = 0;
   const int lane = threadIdx.x & 31;
   const int warps = (gridDim.x * blockDim.x) >> 5;
+  const uint32_t sb = slot_off((threadIdx.x >> 5) * epw + lane);
+  if (staged && lane < epw) slot_bar_init(sb);
+  uint32_t phase = 0;
   for (int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; w * epw < S.n; w += warps) {
     const int e = w * epw + lane;
     if (lane >= epw || e >= S.n) continue;
-    Engine E(S, T, C, e);
+    if (staged) {
+      stage_wait_read();  // the slot's previous block has left
+      stage_in(S, e, sb, phase);
+      phase ^= 1u;
+    }
+    Engine E(S, T, C, e, staged ? g_smem + sb : S.blk + (size_t)e * BLK_BYTES);
     E.load();
     uint64_t d = digests ? digests[e] : 0ull;
     float r[4] = {0.f, 0.f, 0.f, 0.f};
@@ -352,6 +417,7 @@ __global__ void __launch_bounds__(ROLL_BLOCK, ROLL_MINB) k_rollout(const __grid_
       }
     }
     E.store();
+    if (staged) stage_out(S, e, sb);
     if (digests) digests[e] = d;
     write_step_out(out, e, E, m, r, st);
     RS_SMARK(7);
@@ -360,6 +426,7 @@ __global__ void __launch_bounds__(ROLL_BLOCK, ROLL_MINB) k_rollout(const __grid_
       p[0] = g_entry; p[1] = g_staged; p[2] = g_first; p[3] = globaltimer_lo();
     }
   }
+  if (staged) stage_wait_all();
   if (stats) {
     unsigned long long g = games;
     for (int off = 16; off > 0; off >>= 1) g += __shfl_down_sync(0xffffffffu, g, off);
@@ -377,7 +444,7 @@ __global__ void __launch_bounds__(BLOCK) k_autoreset(const __grid_constant__ Soa
   const Tabs T{};
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= S.n) return;
-  Engine E(S, T, C, e);
+  Engine E(S, T, C, e, S.blk + (size_t)e * BLK_BYTES);
   E.load();
   float r[4];
   int st = 0;
@@ -403,7 +470,7 @@ __global__ void k_export(const __grid_constant__ Soa S, const __grid_constant__ 
     const __grid_constant__ Cfg C, int e, rs_env_rec* out) {
   const Tabs T = stage_tables(D);
   if (threadIdx.x != 0) return;
-  Engine E(S, T, C, e);
+  Engine E(S, T, C, e, S.blk + (size_t)e * BLK_BYTES);
   export_env(E, C, *out);
 }
 
@@ -411,7 +478,7 @@ __global__ void k_import(const __grid_constant__ Soa S, const __grid_constant__ 
     const __grid_constant__ Cfg C, int e, const rs_env_rec* in) {
   const Tabs T = stage_tables(D);
   if (threadIdx.x != 0) return;
-  Engine E(S, T, C, e);
+  Engine E(S, T, C, e, S.blk + (size_t)e * BLK_BYTES);
   E.load();
   import_env(E, *in);
 }
@@ -429,7 +496,14 @@ struct rs_handle {
   uint32_t* legal_bits_tmp;  // step output when the caller asks only for bools
   rs_env_rec* rec_dev;
   int num_sms;
-  int rollout_ctas_per_sm;  // resident k_rollout CTAs per SM (occupancy)
+  int occ_key[16], occ_val[16];  // resident stepping-kernel CTAs per SM per (block, smem)
+  // stepping kernels on a shared-memory stage (RINSHAN_STAGE): 0 = never
+  // (default), 1 = below 32 envs per warp, 2 = always.  Measured on B200 the
+  // stage cuts the mean per-env step latency by ~35% at 4096 envs but not
+  // the launch time (set by the rare long transitions), and halves the
+  // resident warps at large batches (4096 envs: 83 M steps/s unstaged vs
+  // 78 M staged; 1M envs: 880 M vs 501 M)
+  int stage_mode;
   int epw_override;         // RINSHAN_EPW (tuning experiments), 0 = heuristic
   bool persist;             // launch with the tables' L2 persisting window
   cudaAccessPolicyWindow window;
@@ -454,16 +528,6 @@ void launch_dims(const rs_handle* h, int* grid, int* block) {
   *grid = (h->n + *block - 1) / *block;
 }
 
-// envs per warp for the step / rollout kernels: the fewest (power of two)
-// that keeps the warp count at ~8 per SM (measured on B200: 4096 envs run
-// 1.3x faster at 4 envs/warp than at 32, 1024 envs 2x at 1 env/warp)
-int envs_per_warp(const rs_handle* h) {
-  if (h->epw_override > 0) return h->epw_override;
-  const int target_warps = h->num_sms * 8;
-  int epw = 1;
-  while (epw < 32 && (h->n + epw - 1) / epw > target_warps) epw *= 2;
-  return epw;
-}
 // grid of `block`-thread CTAs covering n envs at `epw` envs per warp, capped
 // at `max_ctas` (the grid-stride kernels then loop)
 int warp_grid(const rs_handle* h, int epw, int block, int max_ctas) {
@@ -472,19 +536,63 @@ int warp_grid(const rs_handle* h, int epw, int block, int max_ctas) {
   return (int)std::min<int64_t>(ctas, max_ctas > 0 ? max_ctas : ctas);
 }
 
-// launch shape of the stepping kernels (k_step, k_rollout): 128-thread CTAs
-// while the batch fills under 8 warps per SM (spread over every SM), else
-// ROLL_BLOCK-thread CTAs; `persistent` caps the grid at the resident CTAs
+// Launch shape of the stepping kernels (k_step, k_rollout) at `epw` envs per
+// warp: 128-thread CTAs while the batch fills under ROLL_BLOCK threads per SM
+// (spread over every SM), else ROLL_BLOCK-thread CTAs; one stage slot per
+// env of the CTA.  `ctas` = resident CTAs per SM (occupancy, cached).
 struct Launch {
-  int grid, block, smem, epw;
+  int grid, block, smem, epw, ctas, staged;
 };
-Launch step_launch(const rs_handle* h, bool persistent) {
+int resident_ctas(rs_handle* h, int block, int smem) {
+  const int key = block * 1048576 + smem;
+  for (int i = 0; i < 16; i++)
+    if (h->occ_key[i] == key) return h->occ_val[i];
+  int ctas = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ctas, k_rollout, block, smem) != cudaSuccess) {
+    cudaGetLastError();
+    ctas = 1;
+  }
+  ctas = std::max(ctas, 1);
+  for (int i = 0; i < 16; i++)
+    if (h->occ_key[i] == 0) {
+      h->occ_key[i] = key;
+      h->occ_val[i] = ctas;
+      break;
+    }
+  return ctas;
+}
+Launch launch_at(rs_handle* h, int epw) {
   Launch L;
-  L.epw = envs_per_warp(h);
-  const int64_t warps = (h->n + L.epw - 1) / L.epw;
+  L.epw = epw;
+  const int64_t warps = (h->n + epw - 1) / epw;
   L.block = warps * 32 >= (int64_t)h->num_sms * ROLL_BLOCK ? ROLL_BLOCK : BLOCK;
-  L.smem = smem_for(L.block);
-  L.grid = warp_grid(h, L.epw, L.block, persistent ? h->num_sms * h->rollout_ctas_per_sm * ROLL_BLOCK / L.block : 0);
+  L.staged = h->stage_mode == 2 || (h->stage_mode == 1 && epw < 32);
+  L.smem = L.staged ? smem_staged(L.block / 32 * epw) : smem_for(L.block);
+  L.ctas = resident_ctas(h, L.block, L.smem);
+  L.grid = warp_grid(h, epw, L.block, 0);
+  return L;
+}
+// envs per warp: the fewest (power of two) whose warps all fit in one wave
+// (7/8 of the resident warps).  A step is a long dependent chain per env and
+// the envs of a warp run their divergent paths one after another, so fewer
+// envs per warp is faster as long as no second wave is needed (measured on
+// B200 before the shared-memory stage: 4096 envs 79 M steps/s at 2 envs per
+// warp vs 70 M at 4 and 54 M at 32; 16384 envs 217 M at 8 vs 149 M at 4)
+int envs_per_warp(rs_handle* h) {
+  if (h->epw_override > 0) return h->epw_override;
+  int epw = 1;
+  while (epw < 32) {
+    const Launch L = launch_at(h, epw);
+    const int64_t capacity = (int64_t)h->num_sms * L.ctas * (L.block / 32) * 7 / 8;
+    if ((h->n + epw - 1) / epw <= capacity) break;
+    epw *= 2;
+  }
+  return epw;
+}
+// `persistent` caps the grid at the resident CTAs (k_rollout walks env tiles)
+Launch step_launch(rs_handle* h, bool persistent) {
+  Launch L = launch_at(h, envs_per_warp(h));
+  if (persistent) L.grid = std::min(L.grid, h->num_sms * L.ctas);
   return L;
 }
 
@@ -602,14 +710,11 @@ int rs_create(rs_handle** out, int64_t n_envs, const rs_config* cfg, int32_t dev
     return trc;
   }
   Part parts[] = {
-      {(void**)&S.hdr, 16 * 4 * n},          {(void**)&S.scores, 16 * n},
-      {(void**)&S.wall, (size_t)WALL_STRIDE * n}, {(void**)&S.hmask, 4 * 20 * n},
-      {(void**)&S.hcode, 4 * 16 * n},        {(void**)&S.hcls, 16 * n},
-      {(void**)&S.hinfo, 16 * n},            {(void**)&S.hwaits, 32 * n},
-      {(void**)&S.hrkind, 32 * n},           {(void**)&S.mtiles, 64 * n},
-      {(void**)&S.minfo, 64 * n},            {(void**)&S.river, 4 * RS_MAX_RIVER * 2 * n},
-      {(void**)&S.events, 64 * 2 * n},       {(void**)&S.legal, 16 * n},
-      {(void**)&S.evobs, (size_t)EVOBS_BYTES * n},  {(void**)&S.htok, 4 * 16 * n},
+      {(void**)&S.blk, (size_t)BLK_BYTES * n},
+      {(void**)&S.mtiles, 64 * n},           {(void**)&S.minfo, 64 * n},
+      {(void**)&S.river, 4 * RS_MAX_RIVER * 2 * n},
+      {(void**)&S.events, 64 * 2 * n},
+      {(void**)&S.evobs, (size_t)EVOBS_BYTES * n},
       {(void**)&S.results, sizeof(rs_result_rec) * n},
       {(void**)&h->legal_bits_tmp, 16 * n},  {(void**)&h->rec_dev, sizeof(rs_env_rec)},
   };
@@ -636,13 +741,13 @@ int rs_create(rs_handle** out, int64_t n_envs, const rs_config* cfg, int32_t dev
                            (const void*)k_observe, (const void*)k_rollout, (const void*)k_export,
                            (const void*)k_import, (const void*)k_autoreset};
   for (const void* k : kernels)
-    if ((err = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_for(ROLL_BLOCK))))
+    if ((err = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_staged(ROLL_BLOCK))))
       return cleanup(err, "cudaFuncSetAttribute");
-  if ((err = cudaDeviceGetAttribute(&h->num_sms, cudaDevAttrMultiProcessorCount, device)) ||
-      (err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&h->rollout_ctas_per_sm, k_rollout, ROLL_BLOCK,
-                                                           smem_for(ROLL_BLOCK))))
-    return cleanup(err, "occupancy query");
-  if (h->rollout_ctas_per_sm < 1) h->rollout_ctas_per_sm = 1;
+  if ((err = cudaDeviceGetAttribute(&h->num_sms, cudaDevAttrMultiProcessorCount, device)))
+    return cleanup(err, "device query");
+  for (int i = 0; i < 16; i++) h->occ_key[i] = h->occ_val[i] = 0;
+  const char* stage_env = getenv("RINSHAN_STAGE");
+  h->stage_mode = stage_env ? std::max(0, std::min(2, atoi(stage_env))) : 0;
   const char* epw_env = getenv("RINSHAN_EPW");
   h->epw_override = epw_env ? std::max(0, std::min(32, atoi(epw_env))) : 0;
   *out = h;
@@ -685,14 +790,14 @@ int rs_step_ex(rs_handle* h, const int32_t* actions_dev, int32_t flags, const rs
   if (obs) o = *obs;
   const Launch L = step_launch(h, false);
   CUDA_TRY(launch_tables(h, k_step, L.grid, L.block, L.smem, st, h->S, h->D, h->cfg, actions_dev, flags, o,
-                         next_actions_dev, step_out(h, out), L.epw));
+                         next_actions_dev, step_out(h, out), L.epw, L.staged));
   return finish_step_out(h, out, st);
 }
 
 int rs_observe(rs_handle* h, const int8_t* seats_dev, const rs_obs_out* obs, void* stream) {
   if (!h || !obs) return set_err(RS_E_ARG, "rs_observe: null argument");
   cudaStream_t st = (cudaStream_t)stream;
-  k_observe<<<grid_of(h->n), BLOCK, h->D.smem, st>>>(h->S, h->D, h->cfg, seats_dev, *obs);
+  k_observe<<<grid_of(h->n), BLOCK, smem_for(BLOCK), st>>>(h->S, h->D, h->cfg, seats_dev, *obs);
   CUDA_TRY(cudaGetLastError());
   return 0;
 }
@@ -700,7 +805,7 @@ int rs_observe(rs_handle* h, const int8_t* seats_dev, const rs_obs_out* obs, voi
 int rs_policy_random(rs_handle* h, int32_t* actions_dev, void* stream) {
   if (!h || !actions_dev) return set_err(RS_E_ARG, "rs_policy_random: null argument");
   cudaStream_t st = (cudaStream_t)stream;
-  k_policy<<<grid_of(h->n), BLOCK, h->D.smem, st>>>(h->S, h->D, h->cfg, actions_dev);
+  k_policy<<<grid_of(h->n), BLOCK, smem_for(BLOCK), st>>>(h->S, h->D, h->cfg, actions_dev);
   CUDA_TRY(cudaGetLastError());
   return 0;
 }
@@ -718,7 +823,7 @@ int rs_rollout(rs_handle* h, int32_t steps, const rs_obs_out* obs, int32_t obs_s
   const Launch L = step_launch(h, true);
   CUDA_TRY(launch_tables(h, k_rollout, L.grid, L.block, L.smem, st, h->S, h->D, h->cfg, steps, o,
                          obs ? obs_slots : 0, actions_log, stats_dev, digests_dev, step_out(h, out), L.epw,
-                         nullptr));
+                         nullptr, L.staged));
   return finish_step_out(h, out, st);
 }
 
@@ -732,7 +837,7 @@ int rs_debug_rollout_cycles(rs_handle* h, int32_t steps, const rs_obs_out* obs, 
   if (obs) o = *obs;
   const Launch L = step_launch(h, true);
   CUDA_TRY(launch_tables(h, k_rollout, L.grid, L.block, L.smem, st, h->S, h->D, h->cfg, steps, o, obs ? 1 : 0,
-                         nullptr, nullptr, nullptr, StepOut{}, L.epw, prof_dev));
+                         nullptr, nullptr, nullptr, StepOut{}, L.epw, prof_dev, L.staged));
   CUDA_TRY(cudaGetLastError());
   return 0;
 }
@@ -753,7 +858,7 @@ int rs_autoreset(rs_handle* h, const rs_step_out* out, void* stream) {
 int rs_export_env(rs_handle* h, int64_t env, rs_env_rec* out) {
   if (!h || !out || env < 0 || env >= h->n) return set_err(RS_E_ARG, "rs_export_env: bad arguments");
   CUDA_TRY(cudaSetDevice(h->device));
-  k_export<<<1, 32, h->D.smem>>>(h->S, h->D, h->cfg, (int)env, h->rec_dev);
+  k_export<<<1, 32, smem_for(32)>>>(h->S, h->D, h->cfg, (int)env, h->rec_dev);
   CUDA_TRY(cudaGetLastError());
   CUDA_TRY(cudaMemcpy(out, h->rec_dev, sizeof(rs_env_rec), cudaMemcpyDeviceToHost));
   return 0;
@@ -764,7 +869,7 @@ int rs_import_env(rs_handle* h, int64_t env, const rs_env_rec* in) {
   if (in->abi_version != RS_ABI_VERSION) return set_err(RS_E_ARG, "record abi version mismatch");
   CUDA_TRY(cudaSetDevice(h->device));
   CUDA_TRY(cudaMemcpy(h->rec_dev, in, sizeof(rs_env_rec), cudaMemcpyHostToDevice));
-  k_import<<<1, 32, h->D.smem>>>(h->S, h->D, h->cfg, (int)env, h->rec_dev);
+  k_import<<<1, 32, smem_for(32)>>>(h->S, h->D, h->cfg, (int)env, h->rec_dev);
   CUDA_TRY(cudaGetLastError());
   CUDA_TRY(cudaDeviceSynchronize());
   return 0;

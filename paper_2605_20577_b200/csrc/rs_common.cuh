@@ -27,6 +27,25 @@ inline uint4 make_uint4(uint32_t x, uint32_t y, uint32_t z, uint32_t w) { return
 
 namespace rs {
 
+// -DRS_PROFILE_MARKS=3: per-thread cycle accumulators of selected functions
+// (profiling builds only; g_marks[thread][8])
+#if defined(RS_PROFILE_MARKS) && defined(__CUDACC__)
+__device__ unsigned long long* g_marks;
+#endif
+#if defined(RS_PROFILE_MARKS) && RS_PROFILE_MARKS == 3 && defined(__CUDA_ARCH__)
+struct AccTimer {
+  int slot;
+  long long t0;
+  __device__ explicit AccTimer(int i) : slot(i), t0(clock64()) {}
+  __device__ ~AccTimer() {
+    if (g_marks) g_marks[(size_t)(blockIdx.x * blockDim.x + threadIdx.x) * 8 + slot] += clock64() - t0;
+  }
+};
+#define RS_ACC(i) ::rs::AccTimer _acc_timer_##i(i)
+#else
+#define RS_ACC(i) do {} while (0)
+#endif
+
 constexpr uint64_t GOLDEN = 0x9E3779B97F4A7C15ull;
 
 // ---------------------------------------------------------------- bit ops

@@ -13,9 +13,6 @@
 namespace rs {
 
 // phase timestamps for build-time profiling experiments (-DRS_PROFILE_MARKS)
-#if defined(RS_PROFILE_MARKS) && defined(__CUDACC__)
-__device__ unsigned long long* g_marks;
-#endif
 // RS_PROFILE_MARKS=1: phases of init_game (RS_MARK); =2: phases of a step (RS_SMARK)
 #if defined(RS_PROFILE_MARKS) && defined(__CUDA_ARCH__)
 #define RS_MARK_AT(i)                                                                        \
@@ -30,8 +27,11 @@ __device__ unsigned long long* g_marks;
 #if defined(RS_PROFILE_MARKS) && RS_PROFILE_MARKS == 2
 #define RS_MARK(i) do {} while (0)
 #define RS_SMARK(i) RS_MARK_AT(i)
-#else
+#elif defined(RS_PROFILE_MARKS) && RS_PROFILE_MARKS == 1
 #define RS_MARK(i) RS_MARK_AT(i)
+#define RS_SMARK(i) do {} while (0)
+#else
+#define RS_MARK(i) do {} while (0)
 #define RS_SMARK(i) do {} while (0)
 #endif
 
@@ -82,30 +82,33 @@ struct Engine {
   const Tabs& T;
   const Cfg& C;
   int e;
+  uint8_t* bp;  // the env's block: its shared-memory stage slot or its HBM copy (rs_state.cuh)
   Game g;
 
-  RS_HD Engine(const Soa& s, const Tabs& t, const Cfg& c, int env) : S(s), T(t), C(c), e(env) {}
+  RS_HD Engine(const Soa& s, const Tabs& t, const Cfg& c, int env, uint8_t* block)
+      : S(s), T(t), C(c), e(env), bp(block) {}
 
   // ------------------------------------------------------------- memory
   // 32-bit index math: rs_create bounds n so that 160 * n < 2^31
   RS_HD uint32_t at(int f) const { return (uint32_t)f * (uint32_t)S.n + (uint32_t)e; }
   RS_HD void load() {
-    g.unpack(S.hdr[at(0)], S.hdr[at(1)], S.hdr[at(2)], S.hdr[at(3)], S.scores[e]);
+    const int4 sc = *reinterpret_cast<const int4*>(&squad(bp, W_SCORES));
+    g.unpack(squad(bp, W_HDR), squad(bp, W_HDR + 4), squad(bp, W_HDR + 8), squad(bp, W_HDR + 12), sc);
   }
   RS_HD void store() const {
     uint4 a, b, c, d;
     int4 sc;
     g.pack(a, b, c, d, sc);
-    S.hdr[at(0)] = a; S.hdr[at(1)] = b; S.hdr[at(2)] = c; S.hdr[at(3)] = d;
-    S.scores[e] = sc;
+    squad(bp, W_HDR) = a; squad(bp, W_HDR + 4) = b; squad(bp, W_HDR + 8) = c; squad(bp, W_HDR + 12) = d;
+    *reinterpret_cast<int4*>(&squad(bp, W_SCORES)) = sc;
   }
-  RS_HD int wall(int pos) const { return S.wall[(size_t)e * WALL_STRIDE + pos]; }
+  RS_HD int wall(int pos) const { return swall(bp)[pos]; }
   RS_HD int tok() const { return C.rule == RS_RULE_RED ? 1 : 0; }  // hand_put / hand_take token mode
-  RS_HD uint32_t info(int s) const { return S.hinfo[at(s)]; }
-  RS_HD void set_info(int s, uint32_t v) const { S.hinfo[at(s)] = v; }
-  RS_HD uint64_t waits(int s) const { return S.hwaits[at(s)]; }
+  RS_HD uint32_t info(int s) const { return sword(bp, W_HINFO + s); }
+  RS_HD void set_info(int s, uint32_t v) const { sword(bp, W_HINFO + s) = v; }
+  RS_HD uint64_t waits(int s) const { return sdword(bp, W_HWAITS + 2 * s); }
   RS_HD int count_of(int s, int k) const {
-    return popc32((S.hmask[at(s * 5 + (k >> 3))] >> ((k & 7) * 4)) & 0xFu);
+    return popc32((sword(bp, W_HMASK + 5 * s + (k >> 3)) >> ((k & 7) * 4)) & 0xFu);
   }
   RS_HD uint32_t meld_info(int s, int i) const { return S.minfo[at(s * 4 + i)]; }
   RS_HD uint32_t meld_tiles(int s, int i) const { return S.mtiles[at(s * 4 + i)]; }
@@ -133,13 +136,16 @@ struct Engine {
   // ------------------------------------------------------ rng / dealing
   // engine.py:139-164 (_start_kyoku) with tiles.py:142-144 / rng.py:59-65
   RS_COLD void start_kyoku() {
+    // the swap chain is a dependent load / store sequence: it runs in shared
+    // memory, in place when the block is staged, else in the thread's
+    // 144-byte scratch after the tables (copied to the block afterwards)
+    uint8_t* const wall_dst = swall(bp);
 #if defined(__CUDA_ARCH__)
-    // the thread's own 144-byte slot after the staged tables (shared memory:
-    // the swap chain is a dependent load/store sequence, local memory would
-    // round-trip through a thrashed L1 / L2)
-    uint8_t* w = g_smem + WALL_SLOT_OFF + threadIdx.x * WALL_STRIDE;
+    const bool in_place = __isShared(wall_dst);
+    uint8_t* w = in_place ? wall_dst : g_smem + WALL_SLOT_OFF + threadIdx.x * WALL_STRIDE;
 #else
-    uint8_t w[WALL_STRIDE];
+    const bool in_place = true;
+    uint8_t* w = wall_dst;
 #endif
     {
       uint32_t* w32 = reinterpret_cast<uint32_t*>(w);
@@ -164,11 +170,12 @@ struct Engine {
       }
     }
     g.rng_counter = (uint32_t)c;
-    RS_MARK(2);
-    uint4* dst = reinterpret_cast<uint4*>(S.wall + (size_t)e * WALL_STRIDE);
-    const uint4* src = reinterpret_cast<const uint4*>(w);
+    if (!in_place) {
 #pragma unroll
-    for (int i = 0; i < WALL_STRIDE / 16; i++) dst[i] = src[i];
+      for (int i = 0; i < WALL_STRIDE / 16; i++)
+        reinterpret_cast<uint4*>(wall_dst)[i] = reinterpret_cast<const uint4*>(w)[i];
+    }
+    RS_MARK(2);
     const int dealer = g.dealer();
     // deal 4-4-4 then 1 from the dealer (engine.py:142-151): seat s at
     // offset i = (s - dealer) & 3 receives positions 16r + 4i .. +3 and 48 + i
@@ -191,8 +198,8 @@ struct Engine {
       h.info = hi::set_nconc(hi::set_riichi_index(0u, -1), 13);
       tokens_from_set(h, C.rule == RS_RULE_RED);
       finish_hand(T, h);
-      store_hand(S, e, s, h);
-      S.hrkind[at(s)] = 0ull;
+      store_hand(bp, s, h);
+      sdword(bp, W_HRKIND + 2 * s) = 0ull;
     }
     g.cursor = 52;
     g.kan_draws = 0;
@@ -215,13 +222,13 @@ struct Engine {
 
   // engine.py:167-178
   RS_HD void draw(int seat) {
-    Hand h = load_hand(S, e, seat);
+    Hand h = load_hand(bp, seat);
     h.info = hi::set_temp(h.info, 0);
     const int tile = wall(g.cursor);
     g.cursor++;
     hand_put(T, h, tile, tok());
     finish_hand(T, h);
-    store_hand(S, e, seat, h);
+    store_hand(bp, seat, h);
     g.drawn = tile;
     g.rinshan_pending = 0;
     g.phase = PH_ACT;
@@ -234,7 +241,7 @@ struct Engine {
     g.kan_draws++;
     hand_put(T, h, tile, tok());
     finish_hand(T, h);
-    store_hand(S, e, seat, h);
+    store_hand(bp, seat, h);
     g.drawn = tile;
     g.rinshan_pending = 1;
     g.phase = PH_ACT;
@@ -325,11 +332,11 @@ struct Engine {
     const uint64_t wt = waits(seat);
     if (!((wt >> (tile >> 2)) & 1)) return false;
     if (hi::temp(inf) || hi::perm(inf)) return false;
-    if (wt & S.hrkind[at(seat)]) return false;
+    if (wt & sdword(bp, W_HRKIND + 2 * seat)) return false;
     return ron_has_yaku(seat, tile, chankan);
   }
   RS_COLD bool ron_has_yaku(int seat, int tile, bool chankan) const {
-    const Hand h = load_hand(S, e, seat);
+    const Hand h = load_hand(bp, seat);
     WinIn w;
     win_input(seat, h, tile, false, chankan, w);
     Reading r;
@@ -381,7 +388,7 @@ struct Engine {
   // engine.py:265-306
   RS_HD void legal_act(Mask115& m) const {
     const int seat = g.actor;
-    const Hand h = load_hand(S, e, seat);
+    const Hand h = load_hand(bp, seat);
     if (g.riichi_pending) { discard_bits(h, true, m); return; }
     if (hi::riichi(h.info)) {
       if (can_tsumo(seat, h)) m.set(A_TSUMO);
@@ -546,7 +553,7 @@ struct Engine {
   }
   // engine.py:764-779
   RS_COLD void apply_tsumo(int seat) {
-    const Hand h = load_hand(S, e, seat);
+    const Hand h = load_hand(bp, seat);
     WinIn w;
     win_input(seat, h, g.drawn, true, false, w);
     Reading rd;
@@ -588,7 +595,7 @@ struct Engine {
     for (int i = 0; i < nw; i++) {
       const int seat = w4[i];
       r.winners[i] = (int8_t)seat;
-      const Hand h = load_hand(S, e, seat);
+      const Hand h = load_hand(bp, seat);
       WinIn w;
       win_input(seat, h, g.call_tile, false, g.call_chankan, w);
       Reading rd;
@@ -700,7 +707,7 @@ struct Engine {
   }
   // engine.py:458-486
   RS_HD void apply_discard(int seat, int action) {
-    Hand h = load_hand(S, e, seat);
+    Hand h = load_hand(bp, seat);
     const int tile = pick_discard(h, action);
     const bool tsumogiri = tile == g.drawn;
     const bool declaring = g.riichi_pending;
@@ -715,7 +722,7 @@ struct Engine {
     if (hi::riichi(h.info) && !declaring && ipp) ipp = 0;
     S.river[at(seat * RS_MAX_RIVER + nriver)] =
         (uint16_t)(tile | ((tsumogiri ? RS_RIVER_TSUMOGIRI : 0) | (declaring ? RS_RIVER_RIICHI : 0)) << 8);
-    S.hrkind[at(seat)] |= 1ull << (tile >> 2);
+    sdword(bp, W_HRKIND + 2 * seat) |= 1ull << (tile >> 2);
     hand_take(T, h, tile, tok());
     h.info = hi::set_nriver(h.info, nriver + 1);
     h.info = hi::set_riichi(h.info, riichi_val);
@@ -723,7 +730,7 @@ struct Engine {
     h.info = hi::set_ippatsu(h.info, ipp);
     finish_hand(T, h);
     RS_SMARK(1);
-    store_hand(S, e, seat, h);
+    store_hand(bp, seat, h);
     g.drawn = -1;
     g.rinshan_pending = 0;
     emit(EV_DISCARD, seat, tile);
@@ -790,7 +797,7 @@ struct Engine {
     const int kind = g.call_tile >> 2;
     mark_passed_furiten(kind, g.call_from);
     mark_called_tile();
-    Hand h = load_hand(S, e, seat);
+    Hand h = load_hand(bp, seat);
     int ids[4], n = 0;
     if (action == A_PON || action == A_KAN_OPEN) {
       const int need = action == A_PON ? 2 : 3;
@@ -811,7 +818,7 @@ struct Engine {
     finish_hand(T, h);
     const int called = g.call_tile;
     if (action == A_KAN_OPEN) {
-      store_hand(S, e, seat, h);
+      store_hand(bp, seat, h);
       g.any_call_made = 1;
       clear_all_ippatsu();
       g.pending_dora++;
@@ -822,21 +829,21 @@ struct Engine {
       rinshan_draw(seat, h);
       return;
     }
-    store_hand(S, e, seat, h);
+    store_hand(bp, seat, h);
     finish_meld_call(seat);
     emit(action == A_PON ? EV_PON : EV_CHI, seat, called);
     clear_call();
   }
   // engine.py:714-727
   RS_COLD void apply_closed_kan(int seat, int kind) {
-    Hand h = load_hand(S, e, seat);
+    Hand h = load_hand(bp, seat);
     int ids[4];
     uint32_t nib = h.nibble(kind);
     for (int j = 0; j < 4; j++) { ids[j] = 4 * kind + ctz32(nib); nib &= nib - 1; }
     for (int j = 0; j < 4; j++) hand_take(T, h, ids[j], tok());
     add_meld(seat, h, M_KAN_CLOSED, ids, 4, -1, -1);
     finish_hand(T, h);
-    store_hand(S, e, seat, h);
+    store_hand(bp, seat, h);
     g.any_call_made = 1;
     clear_all_ippatsu();
     g.dora_count = g.dora_count + 1 < 5 ? g.dora_count + 1 : 5;
@@ -848,7 +855,7 @@ struct Engine {
   }
   // engine.py:742-758
   RS_COLD void complete_added_kan(int seat, int kind) {
-    Hand h = load_hand(S, e, seat);
+    Hand h = load_hand(bp, seat);
     const int tile = h.lowest_of_kind(kind);
     const int nm = hi::nmelds(h.info);
     for (int i = 0; i < 4; i++)
@@ -865,7 +872,7 @@ struct Engine {
       }
     hand_take(T, h, tile, tok());
     finish_hand(T, h);
-    store_hand(S, e, seat, h);
+    store_hand(bp, seat, h);
     g.any_call_made = 1;
     clear_all_ippatsu();
     g.pending_dora++;
@@ -876,7 +883,7 @@ struct Engine {
   }
   // engine.py:730-739
   RS_COLD void apply_added_kan(int seat, int kind) {
-    const int tile = 4 * kind + ctz32((S.hmask[at(seat * 5 + (kind >> 3))] >> ((kind & 7) * 4)) & 0xFu);
+    const int tile = 4 * kind + ctz32((sword(bp, W_HMASK + 5 * seat + (kind >> 3)) >> ((kind & 7) * 4)) & 0xFu);
     emit(EV_KAN_ADDED, seat, tile);
     if (begin_call_phase(tile, seat, true)) { g.kakan_kind = kind; return; }
     mark_passed_furiten(kind, seat);
@@ -943,11 +950,11 @@ struct Engine {
 
   // ------------------------------------------------------------ env API
   RS_HD void store_legal(const Mask115& m) const {
-    for (int i = 0; i < 4; i++) S.legal[at(i)] = m.m[i];
+    for (int i = 0; i < 4; i++) sword(bp, W_LEGAL + i) = m.m[i];
   }
   RS_HD Mask115 load_legal() const {
     Mask115 m;
-    for (int i = 0; i < 4; i++) m.m[i] = S.legal[at(i)];
+    for (int i = 0; i < 4; i++) m.m[i] = sword(bp, W_LEGAL + i);
     return m;
   }
   // env/core.py:81-94 (_wrap, _terminal_rewards) -> rewards into r[4]
@@ -986,6 +993,7 @@ struct Engine {
   // engine.py:128-136 + core.py:81-82: fresh game from `seed`; rollout
   // keys (env_key, policy stream, resets) are preserved
   RS_HD void init_game(uint64_t seed, float* r) {
+    RS_ACC(5);
     {
       const uint64_t ek = g.env_key, pk = g.policy_key, pc = g.policy_counter;
       const uint32_t rs = g.resets;
@@ -1014,6 +1022,7 @@ struct Engine {
 
   // env/core.py:85-94 + engine.py:405-422.  Returns status bits.
   RS_HD int step(int action, Mask115& legal, float* r) {
+    RS_ACC(0);
     if (g.env_terminated || g.env_truncated) {
       // contract violation: nothing changes (core.py:87-88 raises)
       legal.clear();
@@ -1046,6 +1055,7 @@ struct Engine {
 
   // env/policies.py:17-22 over the env-view mask
   RS_HD int random_action(const Mask115& legal) {
+    RS_ACC(6);
     const int n = legal.count();
     g.policy_counter++;
     const int i = (int)randbelow_from(stream_value(g.policy_key, g.policy_counter), (uint32_t)n);

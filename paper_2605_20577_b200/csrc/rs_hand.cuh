@@ -56,31 +56,29 @@ struct Hand {
   RS_HD int ntiles() const { return popc32(w0) + popc32(w1) + popc32(w2) + popc32(w3) + popc32(w4); }
 };
 
-RS_HD Hand load_hand(const Soa& S, int e, int seat) {
-  const uint32_t n = (uint32_t)S.n, s = (uint32_t)seat, x = (uint32_t)e;
+RS_HD Hand load_hand(const uint8_t* bp, int seat) {
   Hand h;
-  const uint32_t* m = S.hmask + (s * 5u * n + x);
-  h.w0 = m[0]; h.w1 = m[n]; h.w2 = m[2 * n]; h.w3 = m[3 * n]; h.w4 = m[4 * n];
-  const uint32_t* c = S.hcode + (s * 4u * n + x);
-  h.cm = c[0]; h.cp = c[n]; h.cs = c[2 * n]; h.cz = c[3 * n];
-  h.cls = S.hcls[s * n + x];
-  h.info = S.hinfo[s * n + x];
-  h.waits = S.hwaits[s * n + x];
-  const uint4 t = S.htok[s * n + x];
+  const uint32_t m = W_HMASK + 5 * (uint32_t)seat, c = W_HCODE + 4 * (uint32_t)seat;
+  h.w0 = sword(bp, m); h.w1 = sword(bp, m + 1); h.w2 = sword(bp, m + 2); h.w3 = sword(bp, m + 3);
+  h.w4 = sword(bp, m + 4);
+  h.cm = sword(bp, c); h.cp = sword(bp, c + 1); h.cs = sword(bp, c + 2); h.cz = sword(bp, c + 3);
+  h.cls = sword(bp, W_HCLS + seat);
+  h.info = sword(bp, W_HINFO + seat);
+  h.waits = sdword(bp, W_HWAITS + 2 * seat);
+  const uint4 t = squad(bp, W_HTOK + 4 * seat);
   h.tlo = (uint64_t)t.x | ((uint64_t)t.y << 32);
   h.thi = (uint64_t)t.z | ((uint64_t)t.w << 32);
   return h;
 }
-RS_HD void store_hand(const Soa& S, int e, int seat, const Hand& h) {
-  const uint32_t n = (uint32_t)S.n, s = (uint32_t)seat, x = (uint32_t)e;
-  uint32_t* m = S.hmask + (s * 5u * n + x);
-  m[0] = h.w0; m[n] = h.w1; m[2 * n] = h.w2; m[3 * n] = h.w3; m[4 * n] = h.w4;
-  uint32_t* c = S.hcode + (s * 4u * n + x);
-  c[0] = h.cm; c[n] = h.cp; c[2 * n] = h.cs; c[3 * n] = h.cz;
-  S.hcls[s * n + x] = h.cls;
-  S.hinfo[s * n + x] = h.info;
-  S.hwaits[s * n + x] = h.waits;
-  S.htok[s * n + x] = make_uint4((uint32_t)h.tlo, (uint32_t)(h.tlo >> 32), (uint32_t)h.thi, (uint32_t)(h.thi >> 32));
+RS_HD void store_hand(uint8_t* bp, int seat, const Hand& h) {
+  const uint32_t m = W_HMASK + 5 * (uint32_t)seat, c = W_HCODE + 4 * (uint32_t)seat;
+  sword(bp, m) = h.w0; sword(bp, m + 1) = h.w1; sword(bp, m + 2) = h.w2; sword(bp, m + 3) = h.w3;
+  sword(bp, m + 4) = h.w4;
+  sword(bp, c) = h.cm; sword(bp, c + 1) = h.cp; sword(bp, c + 2) = h.cs; sword(bp, c + 3) = h.cz;
+  sword(bp, W_HCLS + seat) = h.cls;
+  sword(bp, W_HINFO + seat) = h.info;
+  sdword(bp, W_HWAITS + 2 * seat) = h.waits;
+  squad(bp, W_HTOK + 4 * seat) = make_uint4((uint32_t)h.tlo, (uint32_t)(h.tlo >> 32), (uint32_t)h.thi, (uint32_t)(h.thi >> 32));
 }
 
 // ---- sorted observation tokens (observe.py:89-90) kept incrementally ----
@@ -169,7 +167,6 @@ RS_HD void deal_tile(Hand& h, int t) {
 // t3 | t1 | t2 block at the start of dynamic shared memory
 __constant__ const uint8_t* c_suit_cls;
 __constant__ const uint8_t* c_honor_cls;
-extern __shared__ __align__(16) uint8_t g_smem[];
 #endif
 
 RS_HD uint32_t class_of(const Tabs& T, int suit, uint32_t code) {
@@ -278,6 +275,7 @@ RS_HD uint64_t compute_waits(const Tabs& T, const Hand& h, int melds) {
   return compute_waits_s(T, h.w0, h.w1, h.w2, h.w3, h.w4, h.cm, h.cp, h.cs, h.cz, h.cls, melds);
 }
 RS_HD uint64_t compute_waits_impl(const Tabs& T, const Hand& h, int melds) {
+  RS_ACC(2);
   const int budget = 4 - melds, target = 2 * budget + 1;
   const int c0 = cls_byte(h.cls, 0), c1 = cls_byte(h.cls, 1), c2 = cls_byte(h.cls, 2), c3 = cls_byte(h.cls, 3);
   const int a_cur = t1_at(T, c0 * NS + c1), b_cur = t2_at(T, c2 * NH + c3);
@@ -321,6 +319,7 @@ RS_HD uint64_t compute_waits_impl(const Tabs& T, const Hand& h, int melds) {
 
 // _finish_hand (state.py:31-39): shanten always, waits for 13-form tenpai
 RS_HD void finish_hand(const Tabs& T, Hand& h) {
+  RS_ACC(7);
   const int melds = hi::nmelds(h.info);
   const int sh = full_shanten(T, h, melds);
   h.info = hi::set_shanten(h.info, sh);
@@ -350,6 +349,7 @@ RS_HD void hand_take(const Tabs& T, Hand& h, int t, int tok) {
 
 // _shanten_minus_kind (engine.py:214-227)
 RS_HD int shanten_minus_kind(const Tabs& T, const Hand& h, int k) {
+  RS_ACC(3);
   Hand x = h;
   hand_take(T, x, x.lowest_of_kind(k), -1);
   return full_shanten(T, x, hi::nmelds(h.info));

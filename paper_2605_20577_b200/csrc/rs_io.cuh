@@ -15,10 +15,11 @@ RS_HD int ev_token(int type) { return type <= 8 ? type : type - 1; }  // win eve
 
 // observe(state, seat) (observe.py:81-124), written into slot `o` of `obs`
 RS_HD void write_obs(const Engine& E, int seat, const rs_obs_out& obs, int64_t o) {
+  RS_ACC(4);
   const Soa& S = E.S;
   const Game& g = E.g;
   const int rule = E.C.rule;
-  const Hand h = load_hand(S, E.e, seat);
+  const Hand h = load_hand(E.bp, seat);
   if (obs.hand_tokens) {
     // sorted tokens (kinds ascending, then the held red fives 34..36), padded
     // with 37: the hand keeps them sorted incrementally (rs_hand.cuh
@@ -37,21 +38,30 @@ RS_HD void write_obs(const Engine& E, int seat, const rs_obs_out& obs, int64_t o
     const uint32_t len = g.events_len;
     const int pad = len >= 64u ? 0 : 64 - (int)len;
     uint4* dst = reinterpret_cast<uint4*>(obs.event_tokens + o * 192);
+    // two halves of 32 slots: all 32 loads are issued before the first
+    // store (stores to the output could alias the ring as far as the
+    // compiler knows, so interleaving them would serialise the loads)
     auto emit_window = [&](auto slot) {
 #pragma unroll
-      for (int q = 0; q < 4; q++) {
-        uint32_t w[12];
+      for (int half = 0; half < 2; half++) {
+        uint32_t v[32];
 #pragma unroll
-        for (int r = 0; r < 4; r++) {
-          const int i0 = 16 * q + 4 * r;
-          const uint32_t a = slot(i0), b = slot(i0 + 1), c = slot(i0 + 2), d = slot(i0 + 3);
-          w[3 * r] = byte_perm(a, b, 0x4210);
-          w[3 * r + 1] = byte_perm(b, c, 0x5421);
-          w[3 * r + 2] = byte_perm(c, d, 0x6542);
+        for (int i = 0; i < 32; i++) v[i] = slot(32 * half + i);
+#pragma unroll
+        for (int q = 0; q < 2; q++) {
+          uint32_t w[12];
+#pragma unroll
+          for (int r = 0; r < 4; r++) {
+            const int i0 = 16 * q + 4 * r;
+            w[3 * r] = byte_perm(v[i0], v[i0 + 1], 0x4210);
+            w[3 * r + 1] = byte_perm(v[i0 + 1], v[i0 + 2], 0x5421);
+            w[3 * r + 2] = byte_perm(v[i0 + 2], v[i0 + 3], 0x6542);
+          }
+          uint4* d = dst + 6 * half + 3 * q;
+          d[0] = make_uint4(w[0], w[1], w[2], w[3]);
+          d[1] = make_uint4(w[4], w[5], w[6], w[7]);
+          d[2] = make_uint4(w[8], w[9], w[10], w[11]);
         }
-        dst[3 * q] = make_uint4(w[0], w[1], w[2], w[3]);
-        dst[3 * q + 1] = make_uint4(w[4], w[5], w[6], w[7]);
-        dst[3 * q + 2] = make_uint4(w[8], w[9], w[10], w[11]);
       }
     };
     if (pad == 0)  // a full window (every step after the first 64 events)
@@ -120,7 +130,7 @@ RS_COLD void export_env(Engine& E, const Cfg& C, rs_env_rec& r) {
   for (int i = 0; i < 136; i++) r.wall[i] = (uint8_t)E.wall(i);
   r.cursor = g.cursor; r.kan_draws = g.kan_draws; r.dora_count = g.dora_count;
   for (int s = 0; s < 4; s++) {
-    const Hand h = load_hand(S, E.e, s);
+    const Hand h = load_hand(E.bp, s);
     rs_hand_rec& hr = r.hands[s];
     int n = 0;
     for (int t = 0; t < 136; t++)
@@ -188,7 +198,7 @@ RS_COLD void export_env(Engine& E, const Cfg& C, rs_env_rec& r) {
   r.n_results = g.n_results;
   r.last_result = S.results[E.e];
   const bool done = g.env_terminated || g.env_truncated;
-  for (int i = 0; i < 4; i++) r.legal_mask[i] = done ? 0u : S.legal[(size_t)i * S.n + E.e];
+  for (int i = 0; i < 4; i++) r.legal_mask[i] = done ? 0u : sword(E.bp, W_LEGAL + i);
   r.current_player = g.current_player;
   r.env_terminated = g.env_terminated;
   r.env_truncated = g.env_truncated;
@@ -207,7 +217,7 @@ RS_COLD void import_env(Engine& E, const rs_env_rec& r) {
   const Soa& S = E.S;
   const Tabs& T = E.T;
   Game& g = E.g;
-  uint8_t* w = S.wall + (size_t)E.e * WALL_STRIDE;
+  uint8_t* w = swall(E.bp);
   for (int i = 0; i < 136; i++) w[i] = r.wall[i];
   for (int i = 136; i < WALL_STRIDE; i++) w[i] = 0;
   g.cursor = r.cursor; g.kan_draws = r.kan_draws; g.dora_count = r.dora_count;
@@ -247,9 +257,9 @@ RS_COLD void import_env(Engine& E, const rs_env_rec& r) {
           (uint16_t)(hr.river_tile[i] | ((uint16_t)hr.river_flags[i] << 8));
       rk |= 1ull << (hr.river_tile[i] >> 2);
     }
-    S.hrkind[(size_t)s * S.n + E.e] = rk;
+    sdword(E.bp, W_HRKIND + 2 * s) = rk;
     finish_hand(T, h);
-    store_hand(S, E.e, s, h);
+    store_hand(E.bp, s, h);
   }
   for (int s = 0; s < 4; s++) g.scores[s] = r.scores[s];
   g.kyoku = r.kyoku; g.honba = r.honba; g.deposits = r.deposits; g.repeats = r.repeats;

@@ -331,6 +331,7 @@ RS_HD bool finalize_reading(const WinIn& w, Reading& r, uint64_t& key) {
 // `first_only` it stops at the first valid reading (the legality checks
 // _can_tsumo / _can_ron only need existence).
 RS_COLD bool score_win(const WinIn& w, Reading& best, bool first_only) {
+  RS_ACC(1);
   bool found = false;
   uint64_t best_key = 0;
   Reading r;

@@ -1,14 +1,18 @@
-// rs_state.cuh — structure-of-arrays env state in HBM.
+// rs_state.cuh — env state in HBM and its shared-memory stage.
 //
-// One thread owns one env; every per-env field is stored field-major
-// ([field][n]) so the 32 lanes of a warp touch 32 consecutive elements of
-// the same field: one 128-byte line per u32 field access.  The hot game
-// scalars are bit-packed into a 64-byte header (4 x uint4 loaded and stored
-// once per step); per-seat hands are 136-bit tile-id sets (5 words) with
-// their base-5 suit codes, table classes and a packed flag word.
+// The state a step touches on every transition (packed game header, scores,
+// the four hands' tile sets / suit codes / classes / flags / waits / river
+// kinds / observation tokens, the legal mask and the wall) is one
+// contiguous 544-byte block per env in HBM.  A stepping kernel moves an
+// env's block into shared memory with one TMA bulk copy, runs the
+// transition against shared memory (every access a ~30-cycle LDS/STS, and
+// shared-memory traffic cannot alias the global stores of the step, so the
+// dependent chain of a transition never waits on L2 / HBM), and moves the
+// block back with one bulk copy.  Rarely touched or write-mostly fields
+// (melds, river, event rings, kyoku result) stay field-major in HBM.
 //
 // Field inventory follows the reference GameState / HandState
-// (engine/types.py:72-158); `bytes_per_env()` is the S of the roofline.
+// (engine/types.py:72-158); `canonical_state_bytes()` is the S of the roofline.
 #pragma once
 
 #include <stdint.h>
@@ -23,18 +27,28 @@ constexpr int EVOBS_SLOTS = RS_EVENT_WINDOW;                 // per observer
 constexpr int EVOBS_BYTES = 4 * EVOBS_SLOTS * 4;             // per env
 constexpr uint32_t EVOBS_PAD = 37u << 16;                    // (0, 0, 37)
 
+// ------------------------------------------------ the env block (HBM)
+// 100 words then the 144-byte wall; in shared memory each env's slot adds
+// its mbarrier (the bulk copy's completion) and pads to 16 bytes
+constexpr uint32_t W_HDR = 0;      // 4 x uint4 packed game scalars (Game::pack)
+constexpr uint32_t W_SCORES = 16;  // int4
+constexpr uint32_t W_HTOK = 20;    // 4 seats x uint4 sorted hand tokens (observe.py:89-90), pad 37
+constexpr uint32_t W_HWAITS = 36;  // 4 seats x u64 34-bit wait mask (13-form tenpai)
+constexpr uint32_t W_HRKIND = 44;  // 4 seats x u64 kinds present in the river
+constexpr uint32_t W_HMASK = 52;   // 4 seats x 5 words: 136-bit concealed tile-id set
+constexpr uint32_t W_HCODE = 72;   // 4 seats x 4 base-5 codes m, p, s, z
+constexpr uint32_t W_HCLS = 88;    // 4 seats: table class per suit (4 x u8)
+constexpr uint32_t W_HINFO = 92;   // 4 seats: packed HandState flags
+constexpr uint32_t W_LEGAL = 96;   // 4 words env-view legal mask
+constexpr uint32_t W_WORDS = 100;
+constexpr uint32_t BLK_WALL = 4 * W_WORDS;               // 400: wall bytes
+constexpr uint32_t BLK_BYTES = BLK_WALL + WALL_STRIDE;   // 544 per env in HBM (34 x 16 B)
+constexpr uint32_t SLOT_BAR = BLK_BYTES;                 // mbarrier of the slot
+constexpr uint32_t SLOT_BYTES = BLK_BYTES + 16;          // 560 per env in shared memory
+
 struct Soa {
   int n;
-  uint4* hdr;        // [4][n]   packed game scalars (see Game::load/store)
-  int4* scores;      // [n]
-  uint8_t* wall;     // [n][144] shuffled tile ids
-  uint32_t* hmask;   // [4 seat][5][n] concealed tile-id set
-  uint32_t* hcode;   // [4 seat][4][n] base-5 codes m, p, s, z
-  uint32_t* hcls;    // [4 seat][n]    table class per suit (4 x u8)
-  uint32_t* hinfo;   // [4 seat][n]    packed HandState flags
-  uint4* htok;       // [4 seat][n]    sorted hand tokens (observe.py:89-90), pad 37, kept incrementally
-  uint64_t* hwaits;  // [4 seat][n]    34-bit wait mask (13-form tenpai)
-  uint64_t* hrkind;  // [4 seat][n]    kinds present in the river
+  uint8_t* blk;      // [n][544] env blocks (layout above)
   uint32_t* mtiles;  // [4 seat][4 meld][n] tile ids (4 x u8)
   uint32_t* minfo;   // [4 seat][4 meld][n] type | n | from | called
   uint16_t* river;   // [4 seat][40][n] tile | flags << 8
@@ -43,9 +57,21 @@ struct Soa {
   // observe() emits it (type token, relative actor, visible tile token);
   // observe() reads the window slots (len + i) & 63 and synthesizes pads
   uint32_t* evobs;
-  uint32_t* legal;   // [4][n] env-view legal mask
   rs_result_rec* results;  // [n] last kyoku result (written at kyoku end)
 };
+
+// An engine addresses its env's block through one base pointer: the
+// stage slot in shared memory (stepping kernels at small batches) or the
+// block in HBM; every field is an immediate offset from it.
+#if defined(__CUDACC__)
+extern __shared__ __align__(16) uint8_t g_smem[];
+#endif
+RS_HD uint32_t& sword(const uint8_t* b, uint32_t i) { return const_cast<uint32_t*>(reinterpret_cast<const uint32_t*>(b))[i]; }
+RS_HD uint64_t& sdword(const uint8_t* b, uint32_t i) {
+  return *const_cast<uint64_t*>(reinterpret_cast<const uint64_t*>(b + 4 * i));
+}
+RS_HD uint4& squad(const uint8_t* b, uint32_t i) { return *const_cast<uint4*>(reinterpret_cast<const uint4*>(b + 4 * i)); }
+RS_HD uint8_t* swall(const uint8_t* b) { return const_cast<uint8_t*>(b) + BLK_WALL; }
 
 // S of the roofline: the fields that define one env's game (header, scores,
 // wall, concealed sets, flags, waits, river kinds, melds, river, event ring,
@@ -57,8 +83,7 @@ constexpr int64_t canonical_state_bytes() {
 }
 
 inline int64_t bytes_per_env() {
-  return 4 * 16 + 16 + WALL_STRIDE + 4 * 5 * 4 + 4 * 4 * 4 + 4 * 4 + 4 * 4 + 4 * 16 + 4 * 8 + 4 * 8 +
-         4 * 4 * 4 + 4 * 4 * 4 + 4 * RS_MAX_RIVER * 2 + RS_EVENT_WINDOW * 2 + EVOBS_BYTES + 4 * 4 +
+  return BLK_BYTES + 4 * 4 * 4 + 4 * 4 * 4 + 4 * RS_MAX_RIVER * 2 + RS_EVENT_WINDOW * 2 + EVOBS_BYTES +
          (int64_t)sizeof(rs_result_rec);
 }
 

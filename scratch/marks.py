@@ -1,0 +1,26 @@
+"""Scratch: phase timing inside init_game (variant build with -DRS_PROFILE_MARKS)."""
+import os, sys, ctypes as C, torch
+os.environ['RINSHAN_LIB'] = 'build_variants/_rinshan_marks.so'
+sys.path.insert(0, '.')
+from paper_2605_20577_b200.env import BatchEnv, EnvConfig, alloc_observations, obs_struct
+n = 4096
+env = BatchEnv(n, EnvConfig(rule='no-red')).init(seed=0)
+env.rollout(50)
+marks = torch.zeros(200000 * 8, dtype=torch.int64, device='cuda')
+env._L.rs_debug_set_marks.argtypes = [C.c_void_p]
+env._L.rs_debug_set_marks(marks.data_ptr())
+obs = alloc_observations(n, env.device)
+rows = []
+for k in range(30):
+    marks.zero_()
+    env.rollout(1, obs=obs, obs_slots=1)
+    torch.cuda.synchronize()
+    m = marks.view(-1, 8).cpu()
+    sel = m[:, 1] != 0
+    mm = m[sel]
+    rows.append(mm)
+mm = torch.cat(rows)
+names = ['shuffle', 'deal 4 hands', 'draw', 'legal']
+for i, nm in enumerate(names):
+    d = (mm[:, i + 2] - mm[:, i + 1]).float()
+    print('%-14s median %8.0f  p90 %8.0f  (n=%d)' % (nm, d.median(), d.quantile(0.9), len(d)))

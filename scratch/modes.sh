@@ -1,0 +1,14 @@
+#!/bin/bash
+for m in 0 1 2; do
+  echo "== RINSHAN_STAGE=$m"
+  RINSHAN_STAGE=$m python bench.py --sweep 1024,4096,16384,65536,262144,1048576 --no-cpu-baseline --no-e2e --steps 50 --warmup 5 2>&1 | python -c "
+import sys,json
+out=[]
+for l in sys.stdin:
+  try: d=json.loads(l)
+  except Exception: continue
+  if d.get('sweep'): out.append('%d:%.1f' % (d['envs'], d['env_steps_per_s']/1e6))
+print('  sweep M/s', ' '.join(out))
+"
+  RINSHAN_STAGE=$m python scratch/kstep.py 4096 2>&1 | tail -2
+done

@@ -33,22 +33,12 @@ void* hc_create(int n, const rs_config* cfg) {
   std::vector<std::pair<void**, size_t>> plan;
   Soa& S = h->S;
   S.n = n;
-  plan.push_back({(void**)&S.hdr, sizeof(uint4) * 4 * n});
-  plan.push_back({(void**)&S.scores, sizeof(int4) * n});
-  plan.push_back({(void**)&S.wall, (size_t)WALL_STRIDE * n});
-  plan.push_back({(void**)&S.hmask, 4 * 20 * (size_t)n});
-  plan.push_back({(void**)&S.hcode, 4 * 16 * (size_t)n});
-  plan.push_back({(void**)&S.hcls, 4 * 4 * (size_t)n});
-  plan.push_back({(void**)&S.hinfo, 4 * 4 * (size_t)n});
-  plan.push_back({(void**)&S.hwaits, 4 * 8 * (size_t)n});
-  plan.push_back({(void**)&S.hrkind, 4 * 8 * (size_t)n});
+  plan.push_back({(void**)&S.blk, (size_t)BLK_BYTES * n});
   plan.push_back({(void**)&S.mtiles, 16 * 4 * (size_t)n});
   plan.push_back({(void**)&S.minfo, 16 * 4 * (size_t)n});
   plan.push_back({(void**)&S.river, 4 * RS_MAX_RIVER * 2 * (size_t)n});
   plan.push_back({(void**)&S.events, 64 * 2 * (size_t)n});
   plan.push_back({(void**)&S.evobs, (size_t)EVOBS_BYTES * n});
-  plan.push_back({(void**)&S.htok, 4 * 16 * (size_t)n});
-  plan.push_back({(void**)&S.legal, 4 * 4 * (size_t)n});
   plan.push_back({(void**)&S.results, sizeof(rs_result_rec) * (size_t)n});
   for (auto& p : plan) off += (p.second + 255) & ~(size_t)255;
   h->mem.assign(off + 256, 0);
@@ -63,11 +53,12 @@ void* hc_create(int n, const rs_config* cfg) {
 
 void hc_free(void* p) { delete (HC*)p; }
 
+
 // bench seeding (bench/runner.py:25-33)
 void hc_init_indexed(void* p, uint64_t seed, int64_t base, float* rewards) {
   HC* h = (HC*)p;
   for (int e = 0; e < h->S.n; e++) {
-    Engine E(h->S, h->T, h->C, e);
+    Engine E(h->S, h->T, h->C, e, h->S.blk + (size_t)e * BLK_BYTES);
     E.g.env_key = derive_key(mix64(seed), (uint64_t)(base + e));
     E.g.policy_key = derive_key(E.g.env_key, 1);
     E.g.policy_counter = 0;
@@ -80,7 +71,7 @@ void hc_init_indexed(void* p, uint64_t seed, int64_t base, float* rewards) {
 void hc_init_seeds(void* p, const uint64_t* seeds, float* rewards) {
   HC* h = (HC*)p;
   for (int e = 0; e < h->S.n; e++) {
-    Engine E(h->S, h->T, h->C, e);
+    Engine E(h->S, h->T, h->C, e, h->S.blk + (size_t)e * BLK_BYTES);
     E.g.env_key = seeds[e];
     E.g.policy_key = derive_key(seeds[e], 1);
     E.g.policy_counter = 0;
@@ -93,7 +84,7 @@ void hc_init_seeds(void* p, const uint64_t* seeds, float* rewards) {
 void hc_step(void* p, const int32_t* actions, uint8_t* status, float* rewards) {
   HC* h = (HC*)p;
   for (int e = 0; e < h->S.n; e++) {
-    Engine E(h->S, h->T, h->C, e);
+    Engine E(h->S, h->T, h->C, e, h->S.blk + (size_t)e * BLK_BYTES);
     E.load();
     Mask115 m;
     status[e] = (uint8_t)E.step(actions[e], m, rewards + 4 * e);
@@ -104,7 +95,7 @@ void hc_step(void* p, const int32_t* actions, uint8_t* status, float* rewards) {
 void hc_random_actions(void* p, int32_t* actions) {
   HC* h = (HC*)p;
   for (int e = 0; e < h->S.n; e++) {
-    Engine E(h->S, h->T, h->C, e);
+    Engine E(h->S, h->T, h->C, e, h->S.blk + (size_t)e * BLK_BYTES);
     E.load();
     actions[e] = E.random_action(E.load_legal());
     E.store();
@@ -113,13 +104,13 @@ void hc_random_actions(void* p, int32_t* actions) {
 
 void hc_export(void* p, int e, rs_env_rec* out) {
   HC* h = (HC*)p;
-  Engine E(h->S, h->T, h->C, e);
+  Engine E(h->S, h->T, h->C, e, h->S.blk + (size_t)e * BLK_BYTES);
   export_env(E, h->C, *out);
 }
 
 void hc_import(void* p, int e, const rs_env_rec* in) {
   HC* h = (HC*)p;
-  Engine E(h->S, h->T, h->C, e);
+  Engine E(h->S, h->T, h->C, e, h->S.blk + (size_t)e * BLK_BYTES);
   E.load();
   import_env(E, *in);
 }
@@ -128,7 +119,7 @@ void hc_observe(void* p, int e, int seat, uint8_t* hand, uint8_t* events, int8_t
                 uint8_t* misc /*round, seat, kyoku, live*/, int16_t* hd /*honba, deposits*/, uint8_t* dora,
                 uint8_t* riichi) {
   HC* h = (HC*)p;
-  Engine E(h->S, h->T, h->C, e);
+  Engine E(h->S, h->T, h->C, e, h->S.blk + (size_t)e * BLK_BYTES);
   E.load();
   rs_obs_out o;
   o.hand_tokens = hand; o.event_tokens = events; o.shanten = sh; o.scores = scores;
@@ -142,7 +133,7 @@ int64_t hc_rollout(void* p, int steps, uint64_t* digests, int16_t* actions_log) 
   HC* h = (HC*)p;
   int64_t games = 0;
   for (int e = 0; e < h->S.n; e++) {
-    Engine E(h->S, h->T, h->C, e);
+    Engine E(h->S, h->T, h->C, e, h->S.blk + (size_t)e * BLK_BYTES);
     E.load();
     uint64_t d = digests ? digests[e] : 0;
     float r[4];
