@@ -18,6 +18,8 @@
  *                     (engine/engine.py:405-422 apply_action, :105-122 _finish)
  *   rs_observe        env/observe.py:81-124   observe(state, seat)
  *   rs_policy_random  env/policies.py:17-22    random_policy(legal, rng)
+ *   rs_policy_heuristic env/policies.py:51-109 heuristic_policy(obs, legal)
+ *   rs_rollout_policy bench/runner.py:97-121   one_pass, random or heuristic policy
  *   rs_rollout        bench/runner.py:97-121   run_shard.one_pass (auto-reset +
  *                                              random_policy + step), fused
  *   rs_autoreset      bench/runner.py:107-109  auto-reset of finished envs
@@ -260,12 +262,19 @@ int rs_step(rs_handle* h, const int32_t* actions_dev, const rs_step_out* out, vo
  * each env's policy stream (policies.py:17-22), -1 for finished envs. */
 #define RS_STEP_AUTORESET 1
 #define RS_STEP_OBSERVE 2
+/* next_actions_dev from heuristic_policy instead of random_policy */
+#define RS_STEP_HEURISTIC 4
 int rs_step_ex(rs_handle* h, const int32_t* actions_dev, int32_t flags, const rs_step_out* out,
                const rs_obs_out* obs, int32_t* next_actions_dev, void* stream);
 /* seats_dev: device int8[n] or NULL for each env's current player */
 int rs_observe(rs_handle* h, const int8_t* seats_dev, const rs_obs_out* obs, void* stream);
 /* random policy over each env's legal list using its policy stream */
 int rs_policy_random(rs_handle* h, int32_t* actions_dev, void* stream);
+/* heuristic_policy (policies.py:51-109): win, riichi, else the discard
+ * minimising shanten (honors, terminals, then kind; plain before red), else
+ * the call that strictly lowers shanten, else pass; -1 for finished envs.
+ * Uses no randomness (the policy stream is untouched). */
+int rs_policy_heuristic(rs_handle* h, int32_t* actions_dev, void* stream);
 /* fused rollout: `steps` iterations of {auto-reset, random policy, step,
  * observe} per env (bench/runner.py:97-121).  obs (may be NULL) receives
  * the current player's observation: obs_slots = 1 keeps only the final
@@ -278,6 +287,14 @@ int rs_policy_random(rs_handle* h, int32_t* actions_dev, void* stream);
 int rs_rollout(rs_handle* h, int32_t steps, const rs_obs_out* obs, int32_t obs_slots,
                int16_t* actions_log, rs_rollout_stats* stats_dev, uint64_t* digests_dev,
                const rs_step_out* out, void* stream);
+/* rs_rollout with the acting policy chosen: RS_POLICY_RANDOM (= rs_rollout)
+ * or RS_POLICY_HEURISTIC (the one_pass loop with heuristic_policy acting:
+ * tenpai / riichi / win branches at scale) */
+#define RS_POLICY_RANDOM 0
+#define RS_POLICY_HEURISTIC 1
+int rs_rollout_policy(rs_handle* h, int32_t steps, int32_t policy, const rs_obs_out* obs, int32_t obs_slots,
+                      int16_t* actions_log, rs_rollout_stats* stats_dev, uint64_t* digests_dev,
+                      const rs_step_out* out, void* stream);
 
 /* auto-reset (bench/runner.py:107-109): every finished env starts its next
  * game from env_game_seed(seed, index, resets + 1); outputs for all envs */

@@ -318,7 +318,7 @@ __global__ void __launch_bounds__(ROLL_BLOCK, ROLL_MINB) k_step(const __grid_con
   if (flags & RS_STEP_OBSERVE) write_obs(E, E.g.current_player, obs, e);
   if (next_actions) {
     const bool done = E.g.env_terminated || E.g.env_truncated;
-    next_actions[e] = done ? -1 : E.random_action(m);
+    next_actions[e] = done ? -1 : (flags & RS_STEP_HEURISTIC) ? E.heuristic_action(m) : E.random_action(m);
     dirty |= !done;
   }
   if (dirty) {
@@ -335,13 +335,17 @@ __global__ void __launch_bounds__(ROLL_BLOCK, ROLL_MINB) k_step(const __grid_con
 }
 
 __global__ void __launch_bounds__(BLOCK) k_policy(const __grid_constant__ Soa S, const __grid_constant__ DevTables D,
-    const __grid_constant__ Cfg C, int32_t* actions) {
+    const __grid_constant__ Cfg C, int32_t* actions, int policy) {
   const Tabs T = stage_tables(D);
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= S.n) return;
   Engine E(S, T, C, e, S.blk + (size_t)e * BLK_BYTES);
   E.load();
   if (E.g.env_terminated || E.g.env_truncated) { actions[e] = -1; return; }
+  if (policy == RS_POLICY_HEURISTIC) {
+    actions[e] = E.heuristic_action(E.load_legal());
+    return;
+  }
   actions[e] = E.random_action(E.load_legal());
   E.store();
 }
@@ -363,7 +367,7 @@ __global__ void __launch_bounds__(ROLL_BLOCK, ROLL_MINB) k_rollout(const __grid_
     const __grid_constant__ Cfg C, int steps, rs_obs_out obs,
                                                    int obs_slots, int16_t* actions_log, rs_rollout_stats* stats,
                                                    uint64_t* digests, StepOut out, int epw,
-                                                   uint32_t* prof, int staged) {
+                                                   uint32_t* prof, int staged, int policy) {
   const uint32_t g_entry = prof ? globaltimer_lo() : 0u;
   const Tabs T = stage_tables(D);
   const uint32_t g_staged = prof ? globaltimer_lo() : 0u;
@@ -397,7 +401,7 @@ __global__ void __launch_bounds__(ROLL_BLOCK, ROLL_MINB) k_rollout(const __grid_
       }
       const long long t1 = prof ? clock64() : 0;
       RS_SMARK(0);
-      const int a = E.random_action(E.load_legal());
+      const int a = policy == RS_POLICY_HEURISTIC ? E.heuristic_action(E.load_legal()) : E.random_action(E.load_legal());
       st = E.step(a, m, r);
       if (actions_log) actions_log[(size_t)t * S.n + e] = (int16_t)a;
       if (E.g.env_terminated || E.g.env_truncated) games++;
@@ -805,14 +809,30 @@ int rs_observe(rs_handle* h, const int8_t* seats_dev, const rs_obs_out* obs, voi
 int rs_policy_random(rs_handle* h, int32_t* actions_dev, void* stream) {
   if (!h || !actions_dev) return set_err(RS_E_ARG, "rs_policy_random: null argument");
   cudaStream_t st = (cudaStream_t)stream;
-  k_policy<<<grid_of(h->n), BLOCK, smem_for(BLOCK), st>>>(h->S, h->D, h->cfg, actions_dev);
+  k_policy<<<grid_of(h->n), BLOCK, smem_for(BLOCK), st>>>(h->S, h->D, h->cfg, actions_dev, RS_POLICY_RANDOM);
+  CUDA_TRY(cudaGetLastError());
+  return 0;
+}
+
+int rs_policy_heuristic(rs_handle* h, int32_t* actions_dev, void* stream) {
+  if (!h || !actions_dev) return set_err(RS_E_ARG, "rs_policy_heuristic: null argument");
+  cudaStream_t st = (cudaStream_t)stream;
+  k_policy<<<grid_of(h->n), BLOCK, smem_for(BLOCK), st>>>(h->S, h->D, h->cfg, actions_dev, RS_POLICY_HEURISTIC);
   CUDA_TRY(cudaGetLastError());
   return 0;
 }
 
 int rs_rollout(rs_handle* h, int32_t steps, const rs_obs_out* obs, int32_t obs_slots, int16_t* actions_log,
                rs_rollout_stats* stats_dev, uint64_t* digests_dev, const rs_step_out* out, void* stream) {
+  return rs_rollout_policy(h, steps, RS_POLICY_RANDOM, obs, obs_slots, actions_log, stats_dev, digests_dev, out,
+                           stream);
+}
+
+int rs_rollout_policy(rs_handle* h, int32_t steps, int32_t policy, const rs_obs_out* obs, int32_t obs_slots,
+                      int16_t* actions_log, rs_rollout_stats* stats_dev, uint64_t* digests_dev,
+                      const rs_step_out* out, void* stream) {
   if (!h || steps < 0) return set_err(RS_E_ARG, "rs_rollout: bad arguments");
+  if (policy != RS_POLICY_RANDOM && policy != RS_POLICY_HEURISTIC) return set_err(RS_E_ARG, "rs_rollout: unknown policy");
   if (obs_slots < 0 || (obs_slots > 1 && obs_slots != steps)) return set_err(RS_E_ARG, "obs_slots must be 0, 1 or steps");
   if (obs_slots > 0 && !obs) return set_err(RS_E_ARG, "obs_slots > 0 needs obs buffers");
   cudaStream_t st = (cudaStream_t)stream;
@@ -823,7 +843,7 @@ int rs_rollout(rs_handle* h, int32_t steps, const rs_obs_out* obs, int32_t obs_s
   const Launch L = step_launch(h, true);
   CUDA_TRY(launch_tables(h, k_rollout, L.grid, L.block, L.smem, st, h->S, h->D, h->cfg, steps, o,
                          obs ? obs_slots : 0, actions_log, stats_dev, digests_dev, step_out(h, out), L.epw,
-                         nullptr, L.staged));
+                         nullptr, L.staged, policy));
   return finish_step_out(h, out, st);
 }
 
@@ -837,7 +857,7 @@ int rs_debug_rollout_cycles(rs_handle* h, int32_t steps, const rs_obs_out* obs, 
   if (obs) o = *obs;
   const Launch L = step_launch(h, true);
   CUDA_TRY(launch_tables(h, k_rollout, L.grid, L.block, L.smem, st, h->S, h->D, h->cfg, steps, o, obs ? 1 : 0,
-                         nullptr, nullptr, nullptr, StepOut{}, L.epw, prof_dev, L.staged));
+                         nullptr, nullptr, nullptr, StepOut{}, L.epw, prof_dev, L.staged, (int)RS_POLICY_RANDOM));
   CUDA_TRY(cudaGetLastError());
   return 0;
 }

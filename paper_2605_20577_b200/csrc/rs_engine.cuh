@@ -1053,6 +1053,59 @@ struct Engine {
     return 0;
   }
 
+  // env/policies.py:51-109 (heuristic_policy).  The reference rebuilds the
+  // current player's counts from its observation tokens and finds the
+  // called tile as the last discard / added-kan event of the window; here
+  // both come from the state: the concealed set of the actor and call_tile.
+  RS_HD int heuristic_action(const Mask115& legal) const {
+    if (legal.test(A_TSUMO)) return A_TSUMO;
+    if (legal.test(A_RON)) return A_RON;
+    if (legal.test(A_RIICHI)) return A_RIICHI;
+    const Hand h = load_hand(bp, g.current_player);
+    const int n = h.ntiles();
+    const int melds = n % 3 == 2 ? (14 - n) / 3 : (13 - n) / 3;  // policies.py:34-35
+    // discards (policies.py:67-78): minimise (shanten, honor/terminal/other,
+    // kind, red) over the legal discard ids
+    const uint64_t disc = (uint64_t)legal.m[0] | ((uint64_t)(legal.m[1] & 0x1Fu) << 32);
+    if (disc) {
+      int best_a = -1;
+      uint32_t best_key = 0xFFFFFFFFu;
+      uint64_t d = disc;
+      while (d) {
+        const int a = ctz64(d);
+        d &= d - 1;
+        const int kind = a < 34 ? a : (a == 34 ? 4 : a == 35 ? 13 : 22);
+        Hand x = h;
+        hand_take(T, x, x.lowest_of_kind(kind), -1);
+        const int sh = full_shanten(T, x, melds);
+        const uint32_t cls = kind >= 27 ? 0u : (is_terminal(kind) ? 1u : 2u);
+        const uint32_t key = ((uint32_t)(sh + 1) << 9) | (cls << 7) | ((uint32_t)kind << 1) | (a >= 34 ? 1u : 0u);
+        if (key < best_key) { best_key = key; best_a = a; }
+      }
+      return best_a;
+    }
+    // calls (policies.py:80-107): the first call (ascending ids) reaching
+    // the lowest shanten, only when strictly below the current one
+    if (legal.test(A_PASS)) {
+      const int current = full_shanten(T, h, melds);
+      const int ck = g.call_tile >> 2;
+      int best_call = -1, best_sh = 0;
+      for (int a = A_PON; a <= A_KAN_OPEN; a++) {
+        if (!legal.test(a)) continue;
+        Hand x = h;
+        const int take = a == A_PON ? 2 : (a == A_KAN_OPEN ? 3 : 0);
+        for (int j = 0; j < take; j++) hand_take(T, x, x.lowest_of_kind(ck), -1);
+        if (a == A_CHI_LOW) { hand_take(T, x, x.lowest_of_kind(ck + 1), -1); hand_take(T, x, x.lowest_of_kind(ck + 2), -1); }
+        if (a == A_CHI_MID) { hand_take(T, x, x.lowest_of_kind(ck - 1), -1); hand_take(T, x, x.lowest_of_kind(ck + 1), -1); }
+        if (a == A_CHI_HIGH) { hand_take(T, x, x.lowest_of_kind(ck - 2), -1); hand_take(T, x, x.lowest_of_kind(ck - 1), -1); }
+        const int sh = full_shanten(T, x, melds + 1);
+        if (sh < current && (best_call < 0 || sh < best_sh)) { best_sh = sh; best_call = a; }
+      }
+      return best_call >= 0 ? best_call : A_PASS;
+    }
+    return legal.nth(0);
+  }
+
   // env/policies.py:17-22 over the env-view mask
   RS_HD int random_action(const Mask115& legal) {
     RS_ACC(6);

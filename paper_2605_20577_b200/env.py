@@ -56,6 +56,13 @@ class EnvConfig:
             renchan_cap=self.renchan_cap)
 
 
+def _policy_id(policy: str) -> int:
+    ids = {"random": 0, "heuristic": 1}
+    if policy not in ids:
+        raise ValueError(f"unknown policy {policy!r} (random | heuristic)")
+    return ids[policy]
+
+
 def _ptr(t: torch.Tensor | None) -> int | None:
     return None if t is None else t.data_ptr()
 
@@ -165,7 +172,8 @@ class BatchEnv:
         return self
 
     def step(self, actions: torch.Tensor, *, autoreset: bool = False, observe: bool = False,
-             next_actions: torch.Tensor | None = None, out: abi.rs_step_out | None = None) -> "BatchEnv":
+             next_actions: torch.Tensor | None = None, out: abi.rs_step_out | None = None,
+             next_policy: str = "random") -> "BatchEnv":
         """step(state, action) for every env (env/core.py:85-94): illegal ids
         end the episode with the penalty at the offender; stepping a finished
         env sets RS_STATUS_CONTRACT in `status` and changes nothing.
@@ -174,11 +182,12 @@ class BatchEnv:
         flags still describe the transition, the mask / player / observation
         belong to the new game); `observe` fills `self.observe()`'s tensors
         for the current players; `next_actions` (int32[n]) receives the
-        random policy's next action (-1 for finished envs)."""
+        next action of `next_policy` ("random" or "heuristic"; -1 for
+        finished envs)."""
         actions = actions.to(device=self.device, dtype=torch.int32).contiguous()
         if actions.numel() != self.n:
             raise ValueError("need one action per env")
-        flags = (1 if autoreset else 0) | (2 if observe else 0)
+        flags = (1 if autoreset else 0) | (2 if observe else 0) | (4 if _policy_id(next_policy) else 0)
         ost = None
         if observe:
             if self._obs is None:
@@ -219,6 +228,15 @@ class BatchEnv:
         check(self._L.rs_policy_random(self._h, out.data_ptr(), self._stream()), "rs_policy_random")
         return out
 
+    def heuristic_actions(self, out: torch.Tensor | None = None) -> torch.Tensor:
+        """heuristic_policy for every env (env/policies.py:51-109): win,
+        riichi, shanten-minimising discard, improving call, else pass; -1
+        for finished envs.  Deterministic (no policy stream)."""
+        if out is None:
+            out = torch.empty(self.n, dtype=torch.int32, device=self.device)
+        check(self._L.rs_policy_heuristic(self._h, out.data_ptr(), self._stream()), "rs_policy_heuristic")
+        return out
+
     def autoreset(self) -> "BatchEnv":
         """Restart every finished env with its next bench seed
         (bench/runner.py:107-109); the output tensors are refreshed."""
@@ -227,14 +245,16 @@ class BatchEnv:
 
     def rollout(self, steps: int, obs: Observations | None = None, obs_slots: int = 0,
                 actions_log: torch.Tensor | None = None, stats: torch.Tensor | None = None,
-                digests: torch.Tensor | None = None) -> "BatchEnv":
-        """Fused `steps` x {auto-reset, random policy, step, observe} per env
-        in one kernel (bench/runner.py:97-121).  stats: int64[3] CUDA tensor
-        (steps, games_completed, illegal) accumulated; digests: int64[n]."""
+                digests: torch.Tensor | None = None, policy: str = "random") -> "BatchEnv":
+        """Fused `steps` x {auto-reset, policy, step, observe} per env in one
+        kernel (bench/runner.py:97-121); `policy` is "random" (the bench
+        loop) or "heuristic".  stats: int64[3] CUDA tensor (steps,
+        games_completed, illegal) accumulated; digests: int64[n]."""
         st = obs_struct(obs) if obs is not None else None
-        check(self._L.rs_rollout(
-            self._h, int(steps), C.byref(st) if st is not None else None, int(obs_slots if obs is not None else 0),
-            _ptr(actions_log), _ptr(stats), _ptr(digests), C.byref(self._out), self._stream()), "rs_rollout")
+        check(self._L.rs_rollout_policy(
+            self._h, int(steps), _policy_id(policy), C.byref(st) if st is not None else None,
+            int(obs_slots if obs is not None else 0), _ptr(actions_log), _ptr(stats), _ptr(digests),
+            C.byref(self._out), self._stream()), "rs_rollout")
         return self
 
     # -- projection records (parity harness) ----------------------------------

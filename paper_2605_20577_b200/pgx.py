@@ -192,6 +192,21 @@ def observe(state: EnvState, seat: int) -> Observation:
         riichi_flags=tuple(o["riichi_flags"][0].tolist()))
 
 
+def heuristic_policy(state: EnvState, legal: tuple | None = None) -> int:
+    """policies.py:51-109 heuristic_policy, evaluated on the device from
+    `state` (the reference takes observe(state, current_player) and the
+    legal ids; the hand and the called tile it reconstructs from them are
+    read from the state here).  `legal`, when given, must be state.legal."""
+    if legal is not None and tuple(legal) != tuple(state.legal):
+        raise ValueError("legal must be the state's legal ids")
+    if not state.legal:
+        raise ValueError("no legal actions")
+    r = _Runner.get(state.config, None)
+    r.load(state)
+    a = r.env.heuristic_actions()
+    return int(a[0].item())
+
+
 # --- rng.py:18-65 and policies.py:17-22 on the host (pure functions) ---
 
 class RngState(tuple):

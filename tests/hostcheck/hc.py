@@ -29,7 +29,7 @@ def lib():
         L.hc_import.argtypes = [vp, C.c_int, vp]
         L.hc_observe.argtypes = [vp, C.c_int, C.c_int] + [vp] * 8
         L.hc_rollout.restype = C.c_int64
-        L.hc_rollout.argtypes = [vp, C.c_int, vp, vp]
+        L.hc_rollout.argtypes = [vp, C.c_int, vp, vp, C.c_int]
         _lib = L
     return _lib
 
@@ -94,8 +94,8 @@ class HostBatch:
             "riichi_flags": list(ri),
         }
 
-    def rollout(self, steps: int, digests=None):
+    def rollout(self, steps: int, digests=None, policy: str = "random"):
         d = (C.c_uint64 * self.n)(*(digests or [0] * self.n))
         log = (C.c_int16 * (steps * self.n))()
-        games = self.L.hc_rollout(self.p, steps, d, log)
+        games = self.L.hc_rollout(self.p, steps, d, log, 0 if policy == "random" else 1)
         return games, list(d), [list(log[t * self.n:(t + 1) * self.n]) for t in range(steps)]

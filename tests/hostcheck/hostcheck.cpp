@@ -129,7 +129,7 @@ void hc_observe(void* p, int e, int seat, uint8_t* hand, uint8_t* events, int8_t
 }
 
 // fused rollout restated on the host: auto-reset + random policy + step
-int64_t hc_rollout(void* p, int steps, uint64_t* digests, int16_t* actions_log) {
+int64_t hc_rollout(void* p, int steps, uint64_t* digests, int16_t* actions_log, int policy) {
   HC* h = (HC*)p;
   int64_t games = 0;
   for (int e = 0; e < h->S.n; e++) {
@@ -142,7 +142,7 @@ int64_t hc_rollout(void* p, int steps, uint64_t* digests, int16_t* actions_log) 
         E.g.resets++;
         E.init_game(derive_key(E.g.env_key, 2 + (uint64_t)E.g.resets), r);
       }
-      const int a = E.random_action(E.load_legal());
+      const int a = policy ? E.heuristic_action(E.load_legal()) : E.random_action(E.load_legal());
       Mask115 m;
       E.step(a, m, r);
       if (actions_log) actions_log[(size_t)t * h->S.n + e] = (int16_t)a;

@@ -51,6 +51,7 @@ def test_reference_traces_through_pgx_facade(chunk):
                     assert a == row[7], where
                 else:
                     a = row[7]  # the reference heuristic's choice
+                    assert pgx.heuristic_policy(st) == a, where
                 st = pgx.step(st, a)
 
 

@@ -70,6 +70,44 @@ def test_shared_memory_stage_matches_oracle(rule, stage, monkeypatch):
 
 
 @pytest.mark.parametrize("rule", RULES)
+@pytest.mark.parametrize("mode", ("single", "half"))
+def test_heuristic_rollout_digests_match_oracle(rule, mode):
+    """fused rollout with heuristic_policy acting (policies.py:51-109) ==
+    oracle run_shard(policy=heuristic): tenpai / riichi / win / call paths
+    at a rate random play never reaches"""
+    n, steps = (2048, 400) if mode == "single" else (256, 1500)
+    cfg = EnvConfig(rule=rule, mode=mode)
+    env = BatchEnv(n, cfg).init(seed=17, index_base=0)
+    digests = torch.zeros(n, dtype=torch.int64, device="cuda")
+    stats = torch.zeros(3, dtype=torch.int64, device="cuda")
+    env.rollout(steps, digests=digests, stats=stats, policy="heuristic")
+    torch.cuda.synchronize()
+    games, ref = O.run_shard(_oracle_cfg(cfg), 17, 0, n, steps, policy="heuristic", digests=True)
+    got = [int(x) & ((1 << 64) - 1) for x in digests.cpu().tolist()]
+    bad = [i for i in range(n) if got[i] != ref[i]]
+    assert not bad, f"{len(bad)} envs diverge, first {bad[:8]}"
+    assert stats.cpu().tolist()[1] == games
+
+
+@pytest.mark.parametrize("rule", RULES)
+def test_heuristic_actions_and_next_actions(rule):
+    """rs_policy_heuristic + step_ex(next_policy=heuristic, autoreset) act
+    exactly like the heuristic rollout, step by step"""
+    n, steps = 512, 150
+    cfg = EnvConfig(rule=rule)
+    a = BatchEnv(n, cfg).init(seed=23)
+    b = BatchEnv(n, cfg).init(seed=23)
+    log = torch.zeros(steps, n, dtype=torch.int16, device="cuda")
+    b.rollout(steps, actions_log=log, policy="heuristic")
+    nxt = torch.empty(n, dtype=torch.int32, device="cuda")
+    acts = a.heuristic_actions()
+    for t in range(steps):
+        assert torch.equal(acts.to(torch.int16), log[t]), f"step {t}"
+        a.step(acts, autoreset=True, next_actions=nxt, next_policy="heuristic")
+        acts = nxt.clone()
+
+
+@pytest.mark.parametrize("rule", RULES)
 def test_rollout_chunks_equal_one_launch(rule):
     """K steps in one launch == K/3 steps in three launches (state fully in HBM between)."""
     n = 512

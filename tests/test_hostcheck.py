@@ -30,6 +30,21 @@ def test_rollout_digests(rule, mode):
     assert g2 == games
 
 
+@pytest.mark.parametrize("rule", ("no-red", "red"))
+@pytest.mark.parametrize("mode", ("single", "half"))
+def test_heuristic_rollout_digests(rule, mode):
+    """the engine's heuristic_policy (env/policies.py:51-109, from the state)
+    drives the same trajectories as the oracle's (from the observation)"""
+    cfg = O.make_config(rule=rule, mode=mode)
+    n, steps = (96, 500) if mode == "single" else (24, 1500)
+    games, ref = O.run_shard(cfg, 7, 0, n, steps, policy="heuristic", digests=True)
+    hb = hc.HostBatch(n, cfg)
+    hb.init_indexed(7, 0)
+    g2, got, _ = hb.rollout(steps, policy="heuristic")
+    assert got == ref
+    assert g2 == games
+
+
 def _game(rule, mode, seed, policy):
     cfg = O.make_config(rule=rule, mode=mode)
     hb = hc.HostBatch(1, cfg)
