@@ -292,9 +292,12 @@ int rs_rollout(rs_handle* h, int32_t steps, const rs_obs_out* obs, int32_t obs_s
  * tenpai / riichi / win branches at scale) */
 #define RS_POLICY_RANDOM 0
 #define RS_POLICY_HEURISTIC 1
+/* actors_log (may be NULL): [steps][n] int8, the seat that acted at each
+ * step (engine state.actor, the mjlog-lite [seat, action] pair) | 4 when
+ * the env was auto-reset just before that step (a new game starts there) */
 int rs_rollout_policy(rs_handle* h, int32_t steps, int32_t policy, const rs_obs_out* obs, int32_t obs_slots,
-                      int16_t* actions_log, rs_rollout_stats* stats_dev, uint64_t* digests_dev,
-                      const rs_step_out* out, void* stream);
+                      int16_t* actions_log, int8_t* actors_log, rs_rollout_stats* stats_dev,
+                      uint64_t* digests_dev, const rs_step_out* out, void* stream);
 
 /* auto-reset (bench/runner.py:107-109): every finished env starts its next
  * game from env_game_seed(seed, index, resets + 1); outputs for all envs */

@@ -365,7 +365,8 @@ __global__ void __launch_bounds__(BLOCK) k_observe(const __grid_constant__ Soa S
 // tables once and walks env tiles grid-stride.
 __global__ void __launch_bounds__(ROLL_BLOCK, ROLL_MINB) k_rollout(const __grid_constant__ Soa S, const __grid_constant__ DevTables D,
     const __grid_constant__ Cfg C, int steps, rs_obs_out obs,
-                                                   int obs_slots, int16_t* actions_log, rs_rollout_stats* stats,
+                                                   int obs_slots, int16_t* actions_log, int8_t* actors_log,
+                                                   rs_rollout_stats* stats,
                                                    uint64_t* digests, StepOut out, int epw,
                                                    uint32_t* prof, int staged, int policy) {
   const uint32_t g_entry = prof ? globaltimer_lo() : 0u;
@@ -402,8 +403,10 @@ __global__ void __launch_bounds__(ROLL_BLOCK, ROLL_MINB) k_rollout(const __grid_
       const long long t1 = prof ? clock64() : 0;
       RS_SMARK(0);
       const int a = policy == RS_POLICY_HEURISTIC ? E.heuristic_action(E.load_legal()) : E.random_action(E.load_legal());
+      const int actor = E.g.current_player;
       st = E.step(a, m, r);
       if (actions_log) actions_log[(size_t)t * S.n + e] = (int16_t)a;
+      if (actors_log) actors_log[(size_t)t * S.n + e] = (int8_t)(actor | (reset ? 4 : 0));
       if (E.g.env_terminated || E.g.env_truncated) games++;
       if (digests) d = digest_step(d, a, E, m, r);
       if (obs_slots > 0 && (obs_slots > 1 || t == steps - 1)) {
@@ -824,13 +827,13 @@ int rs_policy_heuristic(rs_handle* h, int32_t* actions_dev, void* stream) {
 
 int rs_rollout(rs_handle* h, int32_t steps, const rs_obs_out* obs, int32_t obs_slots, int16_t* actions_log,
                rs_rollout_stats* stats_dev, uint64_t* digests_dev, const rs_step_out* out, void* stream) {
-  return rs_rollout_policy(h, steps, RS_POLICY_RANDOM, obs, obs_slots, actions_log, stats_dev, digests_dev, out,
-                           stream);
+  return rs_rollout_policy(h, steps, RS_POLICY_RANDOM, obs, obs_slots, actions_log, nullptr, stats_dev,
+                           digests_dev, out, stream);
 }
 
 int rs_rollout_policy(rs_handle* h, int32_t steps, int32_t policy, const rs_obs_out* obs, int32_t obs_slots,
-                      int16_t* actions_log, rs_rollout_stats* stats_dev, uint64_t* digests_dev,
-                      const rs_step_out* out, void* stream) {
+                      int16_t* actions_log, int8_t* actors_log, rs_rollout_stats* stats_dev,
+                      uint64_t* digests_dev, const rs_step_out* out, void* stream) {
   if (!h || steps < 0) return set_err(RS_E_ARG, "rs_rollout: bad arguments");
   if (policy != RS_POLICY_RANDOM && policy != RS_POLICY_HEURISTIC) return set_err(RS_E_ARG, "rs_rollout: unknown policy");
   if (obs_slots < 0 || (obs_slots > 1 && obs_slots != steps)) return set_err(RS_E_ARG, "obs_slots must be 0, 1 or steps");
@@ -842,8 +845,8 @@ int rs_rollout_policy(rs_handle* h, int32_t steps, int32_t policy, const rs_obs_
   // envs walked grid-stride)
   const Launch L = step_launch(h, true);
   CUDA_TRY(launch_tables(h, k_rollout, L.grid, L.block, L.smem, st, h->S, h->D, h->cfg, steps, o,
-                         obs ? obs_slots : 0, actions_log, stats_dev, digests_dev, step_out(h, out), L.epw,
-                         nullptr, L.staged, policy));
+                         obs ? obs_slots : 0, actions_log, actors_log, stats_dev, digests_dev, step_out(h, out),
+                         L.epw, nullptr, L.staged, policy));
   return finish_step_out(h, out, st);
 }
 
@@ -857,7 +860,8 @@ int rs_debug_rollout_cycles(rs_handle* h, int32_t steps, const rs_obs_out* obs, 
   if (obs) o = *obs;
   const Launch L = step_launch(h, true);
   CUDA_TRY(launch_tables(h, k_rollout, L.grid, L.block, L.smem, st, h->S, h->D, h->cfg, steps, o, obs ? 1 : 0,
-                         nullptr, nullptr, nullptr, StepOut{}, L.epw, prof_dev, L.staged, (int)RS_POLICY_RANDOM));
+                         nullptr, nullptr, nullptr, nullptr, StepOut{}, L.epw, prof_dev, L.staged,
+                         (int)RS_POLICY_RANDOM));
   CUDA_TRY(cudaGetLastError());
   return 0;
 }

@@ -245,15 +245,18 @@ class BatchEnv:
 
     def rollout(self, steps: int, obs: Observations | None = None, obs_slots: int = 0,
                 actions_log: torch.Tensor | None = None, stats: torch.Tensor | None = None,
-                digests: torch.Tensor | None = None, policy: str = "random") -> "BatchEnv":
+                digests: torch.Tensor | None = None, policy: str = "random",
+                actors_log: torch.Tensor | None = None) -> "BatchEnv":
         """Fused `steps` x {auto-reset, policy, step, observe} per env in one
         kernel (bench/runner.py:97-121); `policy` is "random" (the bench
         loop) or "heuristic".  stats: int64[3] CUDA tensor (steps,
-        games_completed, illegal) accumulated; digests: int64[n]."""
+        games_completed, illegal) accumulated; digests: int64[n];
+        actions_log int16[steps, n] / actors_log int8[steps, n]: the action and
+        the acting seat of every step (| 4 where an auto-reset preceded it)."""
         st = obs_struct(obs) if obs is not None else None
         check(self._L.rs_rollout_policy(
             self._h, int(steps), _policy_id(policy), C.byref(st) if st is not None else None,
-            int(obs_slots if obs is not None else 0), _ptr(actions_log), _ptr(stats), _ptr(digests),
+            int(obs_slots if obs is not None else 0), _ptr(actions_log), _ptr(actors_log), _ptr(stats), _ptr(digests),
             C.byref(self._out), self._stream()), "rs_rollout")
         return self
 

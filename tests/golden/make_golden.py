@@ -15,6 +15,8 @@ Writes small, deterministic JSON(.gz) files next to this script:
                     modes): per step the action, legal ids, current player,
                     rewards and the sha256 state fingerprint prefix
                     (engine/state.py:276-278) and observation digest
+  logs.json.gz      mjlog-lite-v1 logs (engine/log.py) of the bench loop's
+                    games, canonical JSON
 """
 
 from __future__ import annotations
@@ -383,6 +385,39 @@ def make_scenarios():
     dump("scenarios.json.gz", out)
 
 
+def make_logs():
+    """mjlog-lite-v1 logs (engine/log.py) of the games the bench loop plays
+    (bench/runner.py:97-121: env_game_seed per reset, one continuing
+    env_policy_state per env), recorded with the reference GameRecorder;
+    a steps budget per env like a fused device rollout"""
+    from mjsim.engine.log import GameRecorder, log_to_json
+
+    out = []
+    for rule, mode, seed, n, steps in (("no-red", "single", 3, 4, 260), ("red", "single", 4, 4, 260),
+                                       ("red", "east", 5, 1, 700)):
+        cfg = EnvConfig(rule=rule, mode=mode)
+        for idx in range(n):
+            pol = env_policy_state(seed, idx)
+            r = 0
+            gseed = env_game_seed(seed, idx, r)
+            st = init(gseed, cfg)
+            rec = GameRecorder(st.game.config, gseed)
+            for _ in range(steps):
+                if st.terminated or st.truncated:
+                    r += 1
+                    gseed = env_game_seed(seed, idx, r)
+                    st = init(gseed, cfg)
+                    rec = GameRecorder(st.game.config, gseed)
+                a, pol = random_policy(st.legal, pol)
+                rec.record(st.game, a)
+                st = step(st, a)
+                if st.terminated or st.truncated:
+                    out.append({"rule": rule, "mode": mode, "seed": seed, "index": idx, "game": r,
+                                "steps": steps, "log": log_to_json(rec.to_log(st.game))})
+    print(f"logs: {len(out)} games")
+    dump("logs.json.gz", out)
+
+
 if __name__ == "__main__":
     if len(sys.argv) > 1:
         for name in sys.argv[1:]:
@@ -394,3 +429,4 @@ if __name__ == "__main__":
     make_scoring()
     make_traces()
     make_scenarios()
+    make_logs()

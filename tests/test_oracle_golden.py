@@ -146,3 +146,21 @@ def test_traces_full_fingerprints(chunk):
                 a = env.random_policy(kc) if g["policy"] == "random" else env.heuristic_policy()
                 assert a == row[7], where
                 env.step(a)
+
+
+def test_logs_replay_on_oracle():
+    """reference mjlog-lite-v1 logs (engine/log.py): the [seat, action] pairs
+    re-simulated on the oracle keep the actor in sync and end on the log's
+    state fingerprint"""
+    logs = load("logs.json.gz")
+    assert logs
+    for item in logs:
+        log = json.loads(item["log"])
+        assert log["version"] == "mjlog-lite-v1"
+        cfg = O.make_config(rule=log["config"]["rule"], mode=log["config"]["mode"])
+        env = O.OracleEnv(cfg).init(log["seed"])
+        for seat, action in log["actions"]:
+            assert env.record().actor == seat
+            env.step(action)
+        assert env.fingerprint() == log["fingerprint"]
+        assert list(env.record().scores) == log["final_scores"]
