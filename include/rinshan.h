@@ -23,6 +23,7 @@
  *   rs_rollout        bench/runner.py:97-121   run_shard.one_pass (auto-reset +
  *                                              random_policy + step), fused
  *   rs_autoreset      bench/runner.py:107-109  auto-reset of finished envs
+ *   rs_check_invariants engine/state.py:105-180 check_invariants (+ runner.py soak gates)
  *   rs_export_env     engine/state.py:191-242  serialize_state (projection record)
  *   rs_import_env     tests/engine_helpers.py:58-105 craft() (crafted states)
  *
@@ -63,6 +64,18 @@ extern "C" {
 /* per-env status bits written by rs_step (reference env/core.py:85-94) */
 #define RS_STATUS_ILLEGAL 1u  /* masked-off action: penalty, episode ends   */
 #define RS_STATUS_CONTRACT 2u /* stepped a finished env: state unchanged   */
+
+/* rs_check_invariants violation bits (engine/state.py:105-180,
+ * bench/runner.py:226-284) */
+#define RS_INV_SCORE_SUM 1u         /* scores + 1000 x deposits != 100000        */
+#define RS_INV_TILES 2u             /* the 136 tiles are not each held once      */
+#define RS_INV_EMPTY_LEGAL 4u       /* live game with no legal action            */
+#define RS_INV_TERMINAL_LEGAL 8u    /* finished game with legal actions          */
+#define RS_INV_FURITEN_RON 16u      /* ron offered to a furiten seat             */
+#define RS_INV_HAND_SYNC 32u        /* codes / classes / tokens / shanten /
+                                       waits / river kinds out of sync (full)   */
+#define RS_INV_HAND_SIZE 64u        /* tile-equivalents held != 13 / 14 (full)  */
+#define RS_INV_RIICHI_NOT_TENPAI 128u /* riichi with shanten > 0 (full)         */
 
 /* error codes */
 #define RS_OK 0
@@ -302,6 +315,12 @@ int rs_rollout_policy(rs_handle* h, int32_t steps, int32_t policy, const rs_obs_
 /* auto-reset (bench/runner.py:107-109): every finished env starts its next
  * game from env_game_seed(seed, index, resets + 1); outputs for all envs */
 int rs_autoreset(rs_handle* h, const rs_step_out* out, void* stream);
+
+/* check_invariants (engine/state.py:105-180) of every env; fast != 0 runs
+ * only conservation, the score identity, mask sanity and the furiten-ron
+ * gate (the soak suite's per-step check).  The RS_INV_* bits found are
+ * OR-ed into flags_dev[n] (u32, device), so calls accumulate. */
+int rs_check_invariants(rs_handle* h, int32_t fast, uint32_t* flags_dev, void* stream);
 
 int rs_export_env(rs_handle* h, int64_t env, rs_env_rec* out);
 int rs_import_env(rs_handle* h, int64_t env, const rs_env_rec* in);

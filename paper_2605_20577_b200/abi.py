@@ -25,6 +25,15 @@ REWARD_RANK = 1
 
 STATUS_ILLEGAL = 1
 STATUS_CONTRACT = 2
+# rs_check_invariants bits (include/rinshan.h RS_INV_*)
+INV_SCORE_SUM = 1
+INV_TILES = 2
+INV_EMPTY_LEGAL = 4
+INV_TERMINAL_LEGAL = 8
+INV_FURITEN_RON = 16
+INV_HAND_SYNC = 32
+INV_HAND_SIZE = 64
+INV_RIICHI_NOT_TENPAI = 128
 
 RES_KINDS = ("tsumo", "ron", "exhaustive", "abort_nine_terminals",
              "abort_triple_ron", "abort_four_riichi", "abort_four_kan")

@@ -20,6 +20,7 @@
 #include <mutex>
 #include <string>
 
+#include "rs_check.cuh"
 #include "rs_io.cuh"
 
 using namespace rs;
@@ -465,6 +466,17 @@ __global__ void __launch_bounds__(BLOCK) k_autoreset(const __grid_constant__ Soa
   write_step_out(out, e, E, E.load_legal(), r, st);
 }
 
+__global__ void __launch_bounds__(BLOCK) k_check(const __grid_constant__ Soa S, const __grid_constant__ DevTables D,
+    const __grid_constant__ Cfg C, int fast, uint32_t* flags) {
+  const Tabs T = stage_tables(D);
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= S.n) return;
+  Engine E(S, T, C, e, S.blk + (size_t)e * BLK_BYTES);
+  E.load();
+  const uint32_t bad = check_invariants(E, fast != 0);
+  if (bad) flags[e] |= bad;
+}
+
 __global__ void k_expand(const uint32_t* bits, uint8_t* bools, int n) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= (int64_t)n * RS_NUM_ACTIONS) return;
@@ -746,7 +758,7 @@ int rs_create(rs_handle** out, int64_t n_envs, const rs_config* cfg, int32_t dev
   if ((err = cudaMemset(h->mem, 0, total))) return cleanup(err, "state clear");
   const void* kernels[] = {(const void*)k_init, (const void*)k_step, (const void*)k_policy,
                            (const void*)k_observe, (const void*)k_rollout, (const void*)k_export,
-                           (const void*)k_import, (const void*)k_autoreset};
+                           (const void*)k_import, (const void*)k_autoreset, (const void*)k_check};
   for (const void* k : kernels)
     if ((err = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_staged(ROLL_BLOCK))))
       return cleanup(err, "cudaFuncSetAttribute");
@@ -871,6 +883,14 @@ extern "C" int rs_debug_set_marks(void* marks) {
   return (int)cudaMemcpyToSymbol(g_marks, &marks, sizeof(marks));
 }
 #endif
+
+int rs_check_invariants(rs_handle* h, int32_t fast, uint32_t* flags_dev, void* stream) {
+  if (!h || !flags_dev) return set_err(RS_E_ARG, "rs_check_invariants: null argument");
+  cudaStream_t st = (cudaStream_t)stream;
+  k_check<<<grid_of(h->n), BLOCK, smem_for(BLOCK), st>>>(h->S, h->D, h->cfg, fast, flags_dev);
+  CUDA_TRY(cudaGetLastError());
+  return 0;
+}
 
 int rs_autoreset(rs_handle* h, const rs_step_out* out, void* stream) {
   if (!h) return set_err(RS_E_ARG, "rs_autoreset: null handle");

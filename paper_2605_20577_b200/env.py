@@ -237,6 +237,26 @@ class BatchEnv:
         check(self._L.rs_policy_heuristic(self._h, out.data_ptr(), self._stream()), "rs_policy_heuristic")
         return out
 
+    def check_invariants(self, fast: bool = False, flags: torch.Tensor | None = None) -> torch.Tensor:
+        """check_invariants (engine/state.py:105-180) of every env on the
+        device: RS_INV_* bits per env (abi.INV_*), OR-ed into `flags` (int32[n])
+        when given.  `fast` = the soak suite's per-step subset."""
+        if flags is None:
+            flags = torch.zeros(self.n, dtype=torch.int32, device=self.device)
+        check(self._L.rs_check_invariants(self._h, 1 if fast else 0, flags.data_ptr(), self._stream()),
+              "rs_check_invariants")
+        return flags
+
+    def soak(self, steps: int, policy: str = "random", fast: bool = False) -> torch.Tensor:
+        """bench/runner.py:226-284 play_games on the device: `steps` fused
+        steps (auto-reset + policy + step), the invariants checked after
+        every one; returns the OR of the RS_INV_* bits per env."""
+        flags = self.check_invariants(fast)
+        for _ in range(steps):
+            self.rollout(1, policy=policy)
+            self.check_invariants(fast, flags)
+        return flags
+
     def autoreset(self) -> "BatchEnv":
         """Restart every finished env with its next bench seed
         (bench/runner.py:107-109); the output tensors are refreshed."""

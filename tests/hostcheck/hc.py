@@ -30,6 +30,8 @@ def lib():
         L.hc_observe.argtypes = [vp, C.c_int, C.c_int] + [vp] * 8
         L.hc_rollout.restype = C.c_int64
         L.hc_rollout.argtypes = [vp, C.c_int, vp, vp, C.c_int]
+        L.hc_check.restype = C.c_uint32
+        L.hc_check.argtypes = [vp, C.c_int, C.c_int]
         _lib = L
     return _lib
 
@@ -93,6 +95,9 @@ class HostBatch:
             "live_wall": misc[3],
             "riichi_flags": list(ri),
         }
+
+    def check(self, e: int, fast: bool = False) -> int:
+        return int(self.L.hc_check(self.p, e, 1 if fast else 0))
 
     def rollout(self, steps: int, digests=None, policy: str = "random"):
         d = (C.c_uint64 * self.n)(*(digests or [0] * self.n))

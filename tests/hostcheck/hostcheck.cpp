@@ -10,6 +10,7 @@
 
 #include <vector>
 
+#include "../../paper_2605_20577_b200/csrc/rs_check.cuh"
 #include "../../paper_2605_20577_b200/csrc/rs_io.cuh"
 
 using namespace rs;
@@ -153,6 +154,13 @@ int64_t hc_rollout(void* p, int steps, uint64_t* digests, int16_t* actions_log, 
     E.store();
   }
   return games;
+}
+
+uint32_t hc_check(void* p, int e, int fast) {
+  HC* h = (HC*)p;
+  Engine E(h->S, h->T, h->C, e, h->S.blk + (size_t)e * BLK_BYTES);
+  E.load();
+  return check_invariants(E, fast != 0);
 }
 
 }  // extern "C"

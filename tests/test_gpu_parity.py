@@ -236,3 +236,15 @@ def test_host_stepper_equals_fused_rollout(rule):
             d["internal"].pop("env_terminated"); d["internal"].pop("env_truncated")
         assert not diff(ra, rb), (i, diff(ra, rb)[:5])
     assert compared > 50
+
+
+@pytest.mark.parametrize("rule", RULES)
+@pytest.mark.parametrize("policy", ("random", "heuristic"))
+def test_device_soak_invariants(rule, policy):
+    """bench/runner.py:226-284 on the device: check_invariants (full) after
+    every fused step of random / heuristic play over many envs"""
+    env = BatchEnv(1024, EnvConfig(rule=rule, mode="half")).init(seed=41)
+    flags = env.soak(300, policy=policy)
+    torch.cuda.synchronize()
+    bad = torch.nonzero(flags).flatten().tolist()
+    assert not bad, f"{len(bad)} envs violate, first {bad[:4]} flags {flags[bad[0]].item() if bad else 0}"

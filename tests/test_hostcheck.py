@@ -45,6 +45,53 @@ def test_heuristic_rollout_digests(rule, mode):
     assert g2 == games
 
 
+@pytest.mark.parametrize("rule", ("no-red", "red"))
+@pytest.mark.parametrize("policy", ("random", "heuristic"))
+def test_invariants_hold_during_play(rule, policy):
+    """check_invariants (state.py:105-180, full) after every step of
+    random and heuristic play: no violation"""
+    cfg = O.make_config(rule=rule, mode="half")
+    n = 16
+    hb = hc.HostBatch(n, cfg)
+    hb.init_indexed(31, 0)
+    for t in range(400):
+        hb.rollout(1, policy=policy)
+        for e in range(n):
+            assert hb.check(e) == 0, (t, e, hb.check(e))
+
+
+def test_invariant_violations_are_detected():
+    """crafted broken states trip the matching bits"""
+    from paper_2605_20577_b200 import abi
+
+    cfg = O.make_config(rule="red", mode="single")
+    oe = O.OracleEnv(cfg).init(77)
+    for _ in range(30):
+        oe.step(oe.legal()[0])
+    base = oe.record()
+    hb = hc.HostBatch(1, cfg)
+
+    def copy():
+        return type(base).from_buffer_copy(base)
+
+    hb.load(0, base)
+    assert hb.check(0) == 0
+    bad = copy()
+    bad.scores[0] += 100
+    hb.load(0, bad)
+    assert hb.check(0) & abi.INV_SCORE_SUM
+    bad = copy()
+    h = bad.hands[0]
+    h.concealed[0] = h.concealed[1]  # a duplicated tile, one missing
+    hb.load(0, bad)
+    assert hb.check(0, fast=True) & abi.INV_TILES
+    bad = copy()
+    s = next(i for i in range(4) if bad.hands[i].shanten > 0 and i != bad.actor)
+    bad.hands[s].riichi = 1
+    hb.load(0, bad)
+    assert hb.check(0) & abi.INV_RIICHI_NOT_TENPAI
+
+
 def _game(rule, mode, seed, policy):
     cfg = O.make_config(rule=rule, mode=mode)
     hb = hc.HostBatch(1, cfg)
