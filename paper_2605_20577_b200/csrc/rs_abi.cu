@@ -163,10 +163,11 @@ struct StepOut {
 // One elected thread issues a single TMA bulk copy (cp.async.bulk, no tensor
 // map needed for a contiguous block) completing on an mbarrier; the other
 // warps spend no instructions on the copy and wait on the barrier phase.
-__device__ __forceinline__ Tabs stage_tables(const DevTables& D) {
+__device__ __forceinline__ Tabs stage_tables(const DevTables& D, int grp_log2 = 0) {
   __shared__ __align__(8) uint64_t bar;
   const uint32_t bar_addr = (uint32_t)__cvta_generic_to_shared(&bar);
   if (threadIdx.x == 0) {
+    s_grp_log2 = grp_log2;  // lanes per env (rs_common.cuh), published by the barrier below
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar_addr) : "memory");
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -293,11 +294,13 @@ __device__ __forceinline__ int env_of_thread(int gtid, int epw) {
 
 __global__ void __launch_bounds__(ROLL_BLOCK, ROLL_MINB) k_step(const __grid_constant__ Soa S, const __grid_constant__ DevTables D,
     const __grid_constant__ Cfg C, const int32_t* actions, int flags, rs_obs_out obs, int32_t* next_actions,
-    StepOut out, int epw, int staged) {
-  const Tabs T = stage_tables(D);
-  const int e = env_of_thread(blockIdx.x * blockDim.x + threadIdx.x, epw);
-  if (e < 0 || e >= S.n) return;
-  const uint32_t sb = slot_off((threadIdx.x >> 5) * epw + (threadIdx.x & 31));
+    StepOut out, int epw, int staged, int glog2) {
+  const Tabs T = stage_tables(D, glog2);
+  const int lane = threadIdx.x & 31;
+  if ((lane >> glog2) >= epw) return;
+  const int e = ((blockIdx.x * blockDim.x + threadIdx.x) >> 5) * epw + (lane >> glog2);
+  if (e >= S.n) return;
+  const uint32_t sb = slot_off((threadIdx.x >> 5) * epw + lane);
   if (staged) {
     slot_bar_init(sb);
     stage_in(S, e, sb, 0);
@@ -369,9 +372,9 @@ __global__ void __launch_bounds__(ROLL_BLOCK, ROLL_MINB) k_rollout(const __grid_
                                                    int obs_slots, int16_t* actions_log, int8_t* actors_log,
                                                    rs_rollout_stats* stats,
                                                    uint64_t* digests, StepOut out, int epw,
-                                                   uint32_t* prof, int staged, int policy) {
+                                                   uint32_t* prof, int staged, int policy, int glog2) {
   const uint32_t g_entry = prof ? globaltimer_lo() : 0u;
-  const Tabs T = stage_tables(D);
+  const Tabs T = stage_tables(D, glog2);
   const uint32_t g_staged = prof ? globaltimer_lo() : 0u;
   unsigned long long games = 0;
   const int lane = threadIdx.x & 31;
@@ -379,9 +382,10 @@ __global__ void __launch_bounds__(ROLL_BLOCK, ROLL_MINB) k_rollout(const __grid_
   const uint32_t sb = slot_off((threadIdx.x >> 5) * epw + lane);
   if (staged && lane < epw) slot_bar_init(sb);
   uint32_t phase = 0;
+  const int sub = lane & ((1 << glog2) - 1);  // the lane's index in its env's group
   for (int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; w * epw < S.n; w += warps) {
-    const int e = w * epw + lane;
-    if (lane >= epw || e >= S.n) continue;
+    const int e = w * epw + (lane >> glog2);
+    if ((lane >> glog2) >= epw || e >= S.n) continue;
     if (staged) {
       stage_wait_read();  // the slot's previous block has left
       stage_in(S, e, sb, phase);
@@ -408,7 +412,7 @@ __global__ void __launch_bounds__(ROLL_BLOCK, ROLL_MINB) k_rollout(const __grid_
       st = E.step(a, m, r);
       if (actions_log) actions_log[(size_t)t * S.n + e] = (int16_t)a;
       if (actors_log) actors_log[(size_t)t * S.n + e] = (int8_t)(actor | (reset ? 4 : 0));
-      if (E.g.env_terminated || E.g.env_truncated) games++;
+      if ((E.g.env_terminated || E.g.env_truncated) && sub == 0) games++;
       if (digests) d = digest_step(d, a, E, m, r);
       if (obs_slots > 0 && (obs_slots > 1 || t == steps - 1)) {
         const int slot = obs_slots > 1 ? t % obs_slots : 0;
@@ -523,6 +527,7 @@ struct rs_handle {
   // resident warps at large batches (4096 envs: 83 M steps/s unstaged vs
   // 78 M staged; 1M envs: 880 M vs 501 M)
   int stage_mode;
+  int groups;  // idle lanes of small-batch warps join their env (RINSHAN_GROUPS=0: off)
   int epw_override;         // RINSHAN_EPW (tuning experiments), 0 = heuristic
   bool persist;             // launch with the tables' L2 persisting window
   cudaAccessPolicyWindow window;
@@ -560,7 +565,7 @@ int warp_grid(const rs_handle* h, int epw, int block, int max_ctas) {
 // (spread over every SM), else ROLL_BLOCK-thread CTAs; one stage slot per
 // env of the CTA.  `ctas` = resident CTAs per SM (occupancy, cached).
 struct Launch {
-  int grid, block, smem, epw, ctas, staged;
+  int grid, block, smem, epw, ctas, staged, glog2;
 };
 int resident_ctas(rs_handle* h, int block, int smem) {
   const int key = block * 1048576 + smem;
@@ -586,6 +591,10 @@ Launch launch_at(rs_handle* h, int epw) {
   const int64_t warps = (h->n + epw - 1) / epw;
   L.block = warps * 32 >= (int64_t)h->num_sms * ROLL_BLOCK ? ROLL_BLOCK : BLOCK;
   L.staged = h->stage_mode == 2 || (h->stage_mode == 1 && epw < 32);
+  // idle lanes join their env as a lane group (not with the stage: one slot per lane)
+  L.glog2 = 0;
+  if (!L.staged && h->groups)
+    while ((epw << (L.glog2 + 1)) <= 32) L.glog2++;
   L.smem = L.staged ? smem_staged(L.block / 32 * epw) : smem_for(L.block);
   L.ctas = resident_ctas(h, L.block, L.smem);
   L.grid = warp_grid(h, epw, L.block, 0);
@@ -767,6 +776,8 @@ int rs_create(rs_handle** out, int64_t n_envs, const rs_config* cfg, int32_t dev
   for (int i = 0; i < 16; i++) h->occ_key[i] = h->occ_val[i] = 0;
   const char* stage_env = getenv("RINSHAN_STAGE");
   h->stage_mode = stage_env ? std::max(0, std::min(2, atoi(stage_env))) : 0;
+  const char* groups_env = getenv("RINSHAN_GROUPS");
+  h->groups = groups_env ? (atoi(groups_env) != 0) : 1;
   const char* epw_env = getenv("RINSHAN_EPW");
   h->epw_override = epw_env ? std::max(0, std::min(32, atoi(epw_env))) : 0;
   *out = h;
@@ -809,7 +820,7 @@ int rs_step_ex(rs_handle* h, const int32_t* actions_dev, int32_t flags, const rs
   if (obs) o = *obs;
   const Launch L = step_launch(h, false);
   CUDA_TRY(launch_tables(h, k_step, L.grid, L.block, L.smem, st, h->S, h->D, h->cfg, actions_dev, flags, o,
-                         next_actions_dev, step_out(h, out), L.epw, L.staged));
+                         next_actions_dev, step_out(h, out), L.epw, L.staged, L.glog2));
   return finish_step_out(h, out, st);
 }
 
@@ -858,7 +869,7 @@ int rs_rollout_policy(rs_handle* h, int32_t steps, int32_t policy, const rs_obs_
   const Launch L = step_launch(h, true);
   CUDA_TRY(launch_tables(h, k_rollout, L.grid, L.block, L.smem, st, h->S, h->D, h->cfg, steps, o,
                          obs ? obs_slots : 0, actions_log, actors_log, stats_dev, digests_dev, step_out(h, out),
-                         L.epw, nullptr, L.staged, policy));
+                         L.epw, nullptr, L.staged, policy, L.glog2));
   return finish_step_out(h, out, st);
 }
 
@@ -873,7 +884,7 @@ int rs_debug_rollout_cycles(rs_handle* h, int32_t steps, const rs_obs_out* obs, 
   const Launch L = step_launch(h, true);
   CUDA_TRY(launch_tables(h, k_rollout, L.grid, L.block, L.smem, st, h->S, h->D, h->cfg, steps, o, obs ? 1 : 0,
                          nullptr, nullptr, nullptr, nullptr, StepOut{}, L.epw, prof_dev, L.staged,
-                         (int)RS_POLICY_RANDOM));
+                         (int)RS_POLICY_RANDOM, L.glog2));
   CUDA_TRY(cudaGetLastError());
   return 0;
 }

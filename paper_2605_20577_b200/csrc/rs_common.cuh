@@ -48,6 +48,48 @@ struct AccTimer {
 
 constexpr uint64_t GOLDEN = 0x9E3779B97F4A7C15ull;
 
+// ------------------------------------------------------- lane groups
+// At small batches a warp holds fewer envs than lanes; the stepping kernels
+// then give each env a group of G = 2^s_grp_log2 consecutive lanes that run
+// the engine redundantly (identical data, identical control flow) and
+// split the long loops of the rare paths (wait scans, riichi filters,
+// the observation window) between them, combining with warp reductions.
+// G = 1 everywhere else (and on the host).
+#if defined(__CUDACC__)
+__shared__ int s_grp_log2;
+#endif
+RS_HD int grp_size() {
+#if defined(__CUDA_ARCH__)
+  return 1 << s_grp_log2;
+#else
+  return 1;
+#endif
+}
+RS_HD int grp_sub() {
+#if defined(__CUDA_ARCH__)
+  return (int)(threadIdx.x & 31) & (grp_size() - 1);
+#else
+  return 0;
+#endif
+}
+RS_HD uint32_t grp_mask() {
+#if defined(__CUDA_ARCH__)
+  const int G = grp_size();
+  return G == 32 ? 0xFFFFFFFFu : (((1u << G) - 1u) << ((threadIdx.x & 31) & ~(uint32_t)(G - 1)));
+#else
+  return 1u;
+#endif
+}
+RS_HD uint64_t grp_or64(uint64_t x) {
+#if defined(__CUDA_ARCH__)
+  if (grp_size() == 1) return x;
+  const uint32_t m = grp_mask();
+  return (uint64_t)__reduce_or_sync(m, (uint32_t)x) | ((uint64_t)__reduce_or_sync(m, (uint32_t)(x >> 32)) << 32);
+#else
+  return x;
+#endif
+}
+
 // ---------------------------------------------------------------- bit ops
 RS_HD int popc32(uint32_t x) {
 #if defined(__CUDA_ARCH__)

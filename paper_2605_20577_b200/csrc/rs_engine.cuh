@@ -350,13 +350,15 @@ struct Engine {
   RS_HD void discard_bits(const Hand& h, bool only_tenpai, Mask115& m) const {
     uint64_t present = h.kinds_ge(1);
     if (only_tenpai) {
+      // the group's lanes take every G-th held kind
+      const int G = grp_size(), sub = grp_sub();
       uint64_t keep = 0, p = present;
-      while (p) {
+      for (int j = 0; p; j++) {
         const int k = ctz64(p);
         p &= p - 1;
-        if (shanten_minus_kind(T, h, k) == 0) keep |= 1ull << k;
+        if ((j & (G - 1)) == sub && shanten_minus_kind(T, h, k) == 0) keep |= 1ull << k;
       }
-      present = keep;
+      present = grp_or64(keep);
     }
     uint64_t kinds = present;
     if (C.rule == RS_RULE_RED) {

@@ -281,6 +281,22 @@ RS_HD uint64_t compute_waits_impl(const Tabs& T, const Hand& h, int melds) {
   const int a_cur = t1_at(T, c0 * NS + c1), b_cur = t2_at(T, c2 * NH + c3);
   const uint64_t full = h.kinds_ge(4);
   uint64_t mask = 0;
+  const int G = grp_size();
+  if (G > 1) {
+    // the lanes of the env's group split the 34 kinds
+    for (int k = grp_sub(); k < 34; k += G) {
+      if ((full >> k) & 1) continue;
+      const int s = kind_suit(k);
+      const int nc = (int)class_of(T, s, h.code(s) + kind_pow(k));
+      int a = a_cur, b = b_cur;
+      if (s == 0) a = t1_at(T, nc * NS + c1);
+      else if (s == 1) a = t1_at(T, c0 * NS + nc);
+      else if (s == 2) b = t2_at(T, nc * NH + c3);
+      else b = t2_at(T, c2 * NH + nc);
+      if ((int)((t3_at(T, a * NB + b) >> (4 * budget)) & 15) >= target) mask |= 1ull << k;
+    }
+    mask = grp_or64(mask);
+  } else {
   // issue the 34 class loads independently: the suit codes are known
 #pragma unroll
   for (int s = 0; s < 4; s++) {
@@ -303,6 +319,7 @@ RS_HD uint64_t compute_waits_impl(const Tabs& T, const Hand& h, int melds) {
         p /= 5u;
       }
     }
+  }
   }
   if (melds == 0) {
     const uint64_t one = h.kinds_eq(1), two = h.kinds_eq(2), three_up = h.kinds_ge(3);

@@ -41,9 +41,12 @@ RS_HD void write_obs(const Engine& E, int seat, const rs_obs_out& obs, int64_t o
     // two halves of 32 slots: all 32 loads are issued before the first
     // store (stores to the output could alias the ring as far as the
     // compiler knows, so interleaving them would serialise the loads)
+    // with a lane group, lanes 0 and 1 of the group write one half each
+    const int G = grp_size(), sub = grp_sub();
     auto emit_window = [&](auto slot) {
 #pragma unroll
       for (int half = 0; half < 2; half++) {
+        if (G > 1 && half != sub) continue;
         uint32_t v[32];
 #pragma unroll
         for (int i = 0; i < 32; i++) v[i] = slot(32 * half + i);
