@@ -153,20 +153,43 @@ struct Engine {
       for (int i = 0; i < 34; i++) w32[i] = 0x03020100u + 0x04040404u * (uint32_t)i;
       w32[34] = w32[35] = 0;
     }
-    // Fisher-Yates (rng.py:59-65): the draws are counter-based, so five are
+    // Fisher-Yates (rng.py:59-65): the draws are counter-based, so they are
     // computed ahead (independent multiplies) and then swapped in order
     uint64_t c = g.rng_counter;
-    for (int i = 135; i > 0; i -= 5) {
-      int j[5];
+#if defined(__CUDA_ARCH__)
+    if (grp_size() > 1) {
+      // the env's lanes compute the draws of G swaps at once and every lane
+      // replays the swap chain on its own copy (shuffle broadcast)
+      const int G = grp_size(), sub = grp_sub();
+      const uint32_t gm = grp_mask();
+      const int base = (int)(threadIdx.x & 31) - sub;
+      for (int i0 = 135; i0 > 0; i0 -= G) {
+        const int i = i0 - sub;
+        const int mine = i > 0 ? (int)randbelow_from(stream_value(g.rng_key, c + 1 + (uint64_t)sub), (uint32_t)(i + 1)) : 0;
+        const int nu = i0 < G ? i0 : G;
+        for (int u = 0; u < nu; u++) {
+          const int j = __shfl_sync(gm, mine, base + u);
+          const uint8_t t = w[i0 - u];
+          w[i0 - u] = w[j];
+          w[j] = t;
+        }
+        c += (uint64_t)nu;
+      }
+    } else
+#endif
+    {
+      for (int i = 135; i > 0; i -= 5) {
+        int j[5];
 #pragma unroll
-      for (int u = 0; u < 5; u++)
-        j[u] = (int)randbelow_from(stream_value(g.rng_key, c + 1 + u), (uint32_t)(i - u + 1));
-      c += 5;
+        for (int u = 0; u < 5; u++)
+          j[u] = (int)randbelow_from(stream_value(g.rng_key, c + 1 + u), (uint32_t)(i - u + 1));
+        c += 5;
 #pragma unroll
-      for (int u = 0; u < 5; u++) {
-        const uint8_t t = w[i - u];
-        w[i - u] = w[j[u]];
-        w[j[u]] = t;
+        for (int u = 0; u < 5; u++) {
+          const uint8_t t = w[i - u];
+          w[i - u] = w[j[u]];
+          w[j[u]] = t;
+        }
       }
     }
     g.rng_counter = (uint32_t)c;
@@ -195,8 +218,8 @@ struct Engine {
       deal_tile(h, w[48 + i]);
       h.cls = class_of(T, 0, h.cm) | (class_of(T, 1, h.cp) << 8) | (class_of(T, 2, h.cs) << 16) |
               (class_of(T, 3, h.cz) << 24);
-      h.info = hi::set_nconc(hi::set_riichi_index(0u, -1), 13);
       tokens_from_set(h, C.rule == RS_RULE_RED);
+      h.info = hi::set_nconc(hi::set_riichi_index(0u, -1), 13);
       finish_hand(T, h);
       store_hand(bp, s, h);
       sdword(bp, W_HRKIND + 2 * s) = 0ull;

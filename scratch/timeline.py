@@ -4,7 +4,7 @@ sys.path.insert(0, '.')
 from paper_2605_20577_b200.env import BatchEnv, EnvConfig, alloc_observations, obs_struct
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 4096
 env = BatchEnv(n, EnvConfig(rule='no-red')).init(seed=0)
-env.rollout(50)
+env.rollout(int(sys.argv[2]) if len(sys.argv) > 2 else 50)
 obs = alloc_observations(n, env.device); ost = obs_struct(obs)
 flush = torch.empty(256 << 20, dtype=torch.uint8, device='cuda')
 prof = torch.zeros(2 * n * 4, dtype=torch.int32, device='cuda')
@@ -29,7 +29,7 @@ for name, idx in (('entry', 0), ('staged', 1), ('first step', 2), ('end', 3)):
 stage = [float((tl[:, 1] - tl[:, 0]).float().median()) for tl, _ in rows]
 print('staging (per CTA) median %.0f ns' % st.median(stage))
 # the slowest envs: were they resetting?
-for tl, cyc in rows[:3]:
+for tl, cyc in rows[:6]:
     end = tl[:, 3]
     top = end.argsort(descending=True)[:5]
     print('slowest envs:', [(int(e), int(end[e]), int(cyc[e, 0]), int(cyc[e, 1]), int(cyc[e, 2]) & 255, (int(cyc[e, 2]) >> 8) & 1) for e in top])
