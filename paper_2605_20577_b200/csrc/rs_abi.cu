@@ -163,9 +163,21 @@ struct StepOut {
 // One elected thread issues a single TMA bulk copy (cp.async.bulk, no tensor
 // map needed for a contiguous block) completing on an mbarrier; the other
 // warps spend no instructions on the copy and wait on the barrier phase.
-__device__ __forceinline__ Tabs stage_tables(const DevTables& D, int grp_log2 = 0) {
-  __shared__ __align__(8) uint64_t bar;
-  const uint32_t bar_addr = (uint32_t)__cvta_generic_to_shared(&bar);
+__shared__ __align__(8) uint64_t s_tables_bar;
+__device__ __forceinline__ void tables_wait() {
+  const uint32_t bar_addr = (uint32_t)__cvta_generic_to_shared(&s_tables_bar);
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(bar_addr)
+      : "memory");
+}
+// issue the copy; the caller waits (tables_wait) before the first table read
+__device__ __forceinline__ void tables_begin(const DevTables& D, int grp_log2) {
+  const uint32_t bar_addr = (uint32_t)__cvta_generic_to_shared(&s_tables_bar);
   if (threadIdx.x == 0) {
     s_grp_log2 = grp_log2;  // lanes per env (rs_common.cuh), published by the barrier below
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar_addr) : "memory");
@@ -180,14 +192,10 @@ __device__ __forceinline__ Tabs stage_tables(const DevTables& D, int grp_log2 = 
         : "memory");
   }
   __syncthreads();
-  asm volatile(
-      "{\n"
-      ".reg .pred p;\n"
-      "WAIT_%=:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n"
-      "@!p bra WAIT_%=;\n"
-      "}\n" ::"r"(bar_addr)
-      : "memory");
+}
+__device__ __forceinline__ Tabs stage_tables(const DevTables& D, int grp_log2 = 0) {
+  tables_begin(D, grp_log2);
+  tables_wait();
   return Tabs{};
 }
 
@@ -374,8 +382,10 @@ __global__ void __launch_bounds__(ROLL_BLOCK, ROLL_MINB) k_rollout(const __grid_
                                                    uint64_t* digests, StepOut out, int epw,
                                                    uint32_t* prof, int staged, int policy, int glog2) {
   const uint32_t g_entry = prof ? globaltimer_lo() : 0u;
-  const Tabs T = stage_tables(D, glog2);
-  const uint32_t g_staged = prof ? globaltimer_lo() : 0u;
+  tables_begin(D, glog2);  // the first env tile's header loads overlap the copy
+  const Tabs T{};
+  bool tables_ready = false;
+  uint32_t g_staged = 0u;
   unsigned long long games = 0;
   const int lane = threadIdx.x & 31;
   const int warps = (gridDim.x * blockDim.x) >> 5;
@@ -394,6 +404,11 @@ __global__ void __launch_bounds__(ROLL_BLOCK, ROLL_MINB) k_rollout(const __grid_
     Engine E(S, T, C, e, staged ? g_smem + sb : S.blk + (size_t)e * BLK_BYTES);
     E.load();
     uint64_t d = digests ? digests[e] : 0ull;
+    if (!tables_ready) {
+      tables_wait();
+      tables_ready = true;
+      if (prof) g_staged = globaltimer_lo();
+    }
     float r[4] = {0.f, 0.f, 0.f, 0.f};
     Mask115 m;
     int st = 0;

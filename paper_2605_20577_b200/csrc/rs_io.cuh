@@ -20,6 +20,12 @@ RS_HD void write_obs(const Engine& E, int seat, const rs_obs_out& obs, int64_t o
   const Game& g = E.g;
   const int rule = E.C.rule;
   const Hand h = load_hand(E.bp, seat);
+  // every block read of the observation before its first store (the output
+  // stores could alias the block as far as the compiler knows)
+  const uint32_t inf0 = E.info(seat), inf1 = E.info((seat + 1) & 3), inf2 = E.info((seat + 2) & 3),
+                 inf3 = E.info((seat + 3) & 3);
+  const uint32_t* wall_w = reinterpret_cast<const uint32_t*>(swall(E.bp));
+  const uint32_t dw0 = wall_w[30], dw1 = wall_w[31], dw2 = wall_w[32];  // wall bytes 120..131
   if (obs.hand_tokens) {
     // sorted tokens (kinds ascending, then the held red fives 34..36), padded
     // with 37: the hand keeps them sorted incrementally (rs_hand.cuh
@@ -83,12 +89,20 @@ RS_HD void write_obs(const Engine& E, int seat, const rs_obs_out& obs, int64_t o
   if (obs.kyoku) obs.kyoku[o] = (uint8_t)g.kyoku;
   if (obs.honba) obs.honba[o] = (int16_t)g.honba;
   if (obs.deposits) obs.deposits[o] = (int16_t)g.deposits;
-  if (obs.dora_tokens)
-    for (int i = 0; i < 5; i++)
-      obs.dora_tokens[o * 5 + i] = (uint8_t)(i < g.dora_count ? tile_token(E.wall(122 + 2 * i), rule) : 37);
+  if (obs.dora_tokens) {
+    // indicators at wall positions 122, 124, ..., 130 (tiles.py:118-144)
+    const int ind[5] = {(int)(dw0 >> 16) & 255, (int)dw1 & 255, (int)(dw1 >> 16) & 255, (int)dw2 & 255,
+                        (int)(dw2 >> 16) & 255};
+#pragma unroll
+    for (int i = 0; i < 5; i++) obs.dora_tokens[o * 5 + i] = (uint8_t)(i < g.dora_count ? tile_token(ind[i], rule) : 37);
+  }
   if (obs.live_wall) obs.live_wall[o] = (uint8_t)g.live();
-  if (obs.riichi_flags)
-    for (int i = 0; i < 4; i++) obs.riichi_flags[o * 4 + i] = (uint8_t)(hi::riichi(E.info((seat + i) & 3)) ? 1 : 0);
+  if (obs.riichi_flags) {
+    obs.riichi_flags[o * 4 + 0] = (uint8_t)(hi::riichi(inf0) ? 1 : 0);
+    obs.riichi_flags[o * 4 + 1] = (uint8_t)(hi::riichi(inf1) ? 1 : 0);
+    obs.riichi_flags[o * 4 + 2] = (uint8_t)(hi::riichi(inf2) ? 1 : 0);
+    obs.riichi_flags[o * 4 + 3] = (uint8_t)(hi::riichi(inf3) ? 1 : 0);
+  }
 }
 
 // trajectory digest (identical to oracle/mjoracle.c orc_digest_step)
