@@ -695,28 +695,35 @@ struct Engine {
   // engine.py:498-531
   RS_HD bool begin_call_phase(int tile, int discarder, bool chankan) {
     const int kind = tile >> 2;
-    int qs[5], qt[5], n = 0;
+    // the queue is packed as it is built (Game::queue layout): no arrays,
+    // so nothing goes through local memory
+    uint32_t q = 0;
+    int n = 0;
+    auto push = [&](int s, int stage) {
+      q |= ((uint32_t)s | ((uint32_t)stage << 2)) << (3 + 4 * n);
+      n++;
+    };
     for (int off = 1; off <= 3; off++) {
       const int s = (discarder + off) & 3;
-      if (can_ron(s, tile, chankan)) { qs[n] = s; qt[n] = ST_RON; n++; }
+      if (can_ron(s, tile, chankan)) push(s, ST_RON);
     }
     if (!chankan && g.live() >= 1) {
       for (int off = 1; off <= 3; off++) {
         const int s = (discarder + off) & 3;
         if (hi::riichi(info(s))) continue;
-        if (count_of(s, kind) >= 2) { qs[n] = s; qt[n] = ST_PONKAN; n++; }
+        if (count_of(s, kind) >= 2) push(s, ST_PONKAN);
       }
       const int s = (discarder + 1) & 3;
-      if (kind < 27 && !hi::riichi(info(s)) && can_chi(s, kind)) { qs[n] = s; qt[n] = ST_CHI; n++; }
+      if (kind < 27 && !hi::riichi(info(s)) && can_chi(s, kind)) push(s, ST_CHI);
     }
     if (!n) return false;
     g.phase = PH_CALL;
     g.call_tile = tile;
     g.call_from = discarder;
-    g.qset(n, qs, qt);
+    g.queue = q | (uint32_t)n;
     g.rons = 0;
     g.call_chankan = chankan;
-    g.actor = qs[0];
+    g.actor = (int)((q >> 3) & 3);
     return true;
   }
 
@@ -939,10 +946,14 @@ struct Engine {
   // engine.py:552-558
   RS_HD void advance_call_queue() {
     if (g.rn()) {
-      int qs[5], qt[5], n = 0;
+      uint32_t q = 0;
+      int n = 0;
       for (int i = 0; i < g.qn(); i++)
-        if (g.qstage(i) == ST_RON) { qs[n] = g.qseat(i); qt[n] = ST_RON; n++; }
-      g.qset(n, qs, qt);
+        if (g.qstage(i) == ST_RON) {
+          q |= ((uint32_t)g.qseat(i) | ((uint32_t)ST_RON << 2)) << (3 + 4 * n);
+          n++;
+        }
+      g.queue = q | (uint32_t)n;
     }
     if (g.qn()) { g.actor = g.qseat(0); return; }
     resolve_call_end();
