@@ -10,5 +10,5 @@ for l in sys.stdin:
   if d.get('sweep'): out.append('%d:%.1f' % (d['envs'], d['env_steps_per_s']/1e6))
 print('  sweep M/s', ' '.join(out))
 "
-  RINSHAN_STAGE=$m python scratch/kstep.py 4096 2>&1 | tail -2
+  RINSHAN_STAGE=$m python tools/kstep.py 4096 2>&1 | tail -2
 done

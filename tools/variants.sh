@@ -13,6 +13,6 @@ for l in sys.stdin:
   if d.get('sweep'): out.append('%d:%.1f' % (d['envs'], d['env_steps_per_s']/1e6))
 print('  sweep M/s', ' '.join(out))
 "
-  env $envs RINSHAN_LIB=build_variants/$v.so python scratch/e2e_parts.py 4096 2>&1 | grep -E "kernel device|rollout K=1" | tr '\n' ' '; echo
+  env $envs RINSHAN_LIB=build_variants/$v.so python tools/e2e_parts.py 4096 2>&1 | grep -E "kernel device|rollout K=1" | tr '\n' ' '; echo
 done
 done
