@@ -1,4 +1,4 @@
-"""Scratch: per-function cycle accumulators (variant build -DRS_PROFILE_MARKS=3), steady state."""
+"""Profiling tool: per-function cycle accumulators (variant build -DRS_PROFILE_MARKS=3), steady state."""
 import os, sys, ctypes as C, torch
 os.environ.setdefault('RINSHAN_LIB', 'build_variants/_rinshan_acc.so')
 sys.path.insert(0, '.')

@@ -1,5 +1,5 @@
 #!/bin/bash
-# scratch: bench.py value / e2e for build variants, alternating
+# profiling tool: bench.py value / e2e for build variants, alternating
 for rep in 1 2 3; do
 for v in "$@"; do
   RINSHAN_LIB=build_variants/$v.so python bench.py --steps 200 --warmup 10 --no-cpu-baseline 2>&1 | python -c "

@@ -1,5 +1,5 @@
 #!/bin/bash
-# scratch: build_variant.sh NAME "-DFOO=1 ..." -> build_variants/NAME.so from the current csrc
+# profiling tool: build_variant.sh NAME "-DFOO=1 ..." -> build_variants/NAME.so from the current csrc
 set -e
 name=$1; shift
 rm -rf /tmp/vb_$name && mkdir -p /tmp/vb_$name/p /tmp/vb_$name/include

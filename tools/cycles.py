@@ -1,4 +1,4 @@
-"""Scratch: per-env per-step cycle profile of the fused rollout (rs_debug_rollout_cycles)."""
+"""Profiling tool: per-env per-step cycle profile of the fused rollout (rs_debug_rollout_cycles)."""
 import sys, ctypes as C, torch, collections
 sys.path.insert(0, '.')
 from paper_2605_20577_b200.env import BatchEnv, EnvConfig, alloc_observations, obs_struct

@@ -1,4 +1,4 @@
-"""Scratch: where does the e2e step time go? (not part of the product)"""
+"""Profiling tool: where does the e2e step time go? (not part of the product)"""
 import sys, time, torch
 sys.path.insert(0, '.')
 from paper_2605_20577_b200.env import BatchEnv, EnvConfig, HostStepper

@@ -1,4 +1,4 @@
-"""Scratch: steady-state device time of k_step (HostStepper kernel) and k_rollout K=1, L2 flushed."""
+"""Profiling tool: steady-state device time of k_step (HostStepper kernel) and k_rollout K=1, L2 flushed."""
 import sys, torch
 sys.path.insert(0, '.')
 from paper_2605_20577_b200.env import BatchEnv, EnvConfig, HostStepper, alloc_observations

@@ -1,4 +1,4 @@
-"""Scratch: phase timing inside init_game (variant build with -DRS_PROFILE_MARKS)."""
+"""Profiling tool: phase timing inside init_game (variant build with -DRS_PROFILE_MARKS)."""
 import os, sys, ctypes as C, torch
 os.environ['RINSHAN_LIB'] = 'build_variants/_rinshan_marks.so'
 sys.path.insert(0, '.')

@@ -1,4 +1,4 @@
-"""Scratch: phase timing of one step (variant build with -DRS_PROFILE_MARKS=2)."""
+"""Profiling tool: phase timing of one step (variant build with -DRS_PROFILE_MARKS=2)."""
 import os, sys, ctypes as C, torch
 os.environ.setdefault('RINSHAN_LIB', 'build_variants/_rinshan_smarks.so')
 sys.path.insert(0, '.')

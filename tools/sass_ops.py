@@ -1,4 +1,4 @@
-"""Scratch: per-opcode executed counts and stall samples from an ncu cuda,sass source csv."""
+"""Profiling tool: per-opcode executed counts and stall samples from an ncu cuda,sass source csv."""
 import csv, sys, collections, re
 rows = csv.reader(open(sys.argv[1]))
 hdr = None; ex = collections.Counter(); st = collections.Counter(); thr = collections.Counter()

@@ -1,4 +1,4 @@
-"""Scratch: aggregate ncu cuda,sass source-page stall samples per source line."""
+"""Profiling tool: aggregate ncu cuda,sass source-page stall samples per source line."""
 import csv, sys, collections
 rows = csv.reader(open(sys.argv[1]))
 cur = None; hdr = None; agg = collections.Counter(); inst = collections.Counter(); src = {}

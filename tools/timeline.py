@@ -1,4 +1,4 @@
-"""Scratch: per-env globaltimer timeline of one k_rollout K=1 launch (L2 flushed before)."""
+"""Profiling tool: per-env globaltimer timeline of one k_rollout K=1 launch (L2 flushed before)."""
 import sys, ctypes as C, torch
 sys.path.insert(0, '.')
 from paper_2605_20577_b200.env import BatchEnv, EnvConfig, alloc_observations, obs_struct

@@ -1,5 +1,5 @@
 #!/bin/bash
-# scratch: A/B build variants: args are NAME or NAME:VAR=VAL (not part of the product)
+# profiling tool: A/B build variants: args are NAME or NAME:VAR=VAL (not part of the product)
 for rep in 1 2; do
 for spec in "$@"; do
   v=${spec%%:*}; envs=""; [[ "$spec" == *:* ]] && envs=${spec#*:}

@@ -1,5 +1,5 @@
 #!/bin/bash
-# scratch: A/B build variants (sweep + steady-state k_step / rollout)
+# profiling tool: A/B build variants (sweep + steady-state k_step / rollout)
 for rep in 1 2; do
 for spec in "$@"; do
   v=${spec%%:*}; envs=""; [[ "$spec" == *:* ]] && envs=${spec#*:}
