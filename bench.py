@@ -162,9 +162,13 @@ def cpu_rollout(args, n_envs, seconds=None, steps=None, warmup=0):
 
 
 def reference_arm(args, rank, world):
+    """The reference's CPU path (the oracle port, all host threads) on this
+    arm's whole-job workload: world x batch envs per bench step.  Under
+    torchrun rank 0 alone runs it; the other ranks exit without work."""
     if rank != 0:
         return 0
-    sps, threads, done, wall, per_step = cpu_rollout(args, args.batch, steps=args.steps, warmup=args.warmup)
+    n = args.batch * world
+    sps, threads, done, wall, per_step = cpu_rollout(args, n, steps=args.steps, warmup=args.warmup)
     line = {
         "impl": "reference",
         "metric": METRIC,
@@ -179,10 +183,10 @@ def reference_arm(args, rank, world):
         "vs_baseline": None,
         "dtype": "int32",
         "data": "synthetic",
-        "config": workload(args, 1),
+        "config": workload(args, world),
         "cpu_baseline": {
             "value": sps, "unit": UNIT, "cores": threads, "kind": "port",
-            "sample": f"{args.batch} envs x {done} bench steps (+{args.warmup} warm-up) of the C oracle "
+            "sample": f"{n} envs x {done} bench steps (+{args.warmup} warm-up) of the C oracle "
                       f"port (oracle/mjoracle.c: auto-reset, random policy, step, observe), {threads} threads",
         },
         "e2e": {"value": sps, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
