@@ -383,11 +383,12 @@ def ours_arm(args, rank, world, local_rank):
 def e2e_run(args, env, dev, world):
     """Same metric through the public API with host buffers
     (paper_2605_20577_b200.HostStepper): per step the host writes the
-    actions into pinned memory, they are copied H2D, one fused kernel steps
-    every env (auto-reset, observation of the current player, the random
-    policy's next action), and the result (rewards, flags, player, packed
-    legal mask, next action) is copied D2H into pinned memory; the three
-    are one CUDA-graph replay.  The host feeds the next actions back."""
+    actions into pinned memory, one fused kernel reads them across the host
+    link, steps every env (auto-reset, observation of the current player,
+    the random policy's next action) and writes the result (rewards, flags,
+    player, packed legal mask, next action) into pinned host memory; one
+    CUDA-graph replay and a stream sync per step.  The host feeds the next
+    actions back."""
     import torch
     import torch.distributed as dist
 
@@ -424,8 +425,9 @@ def e2e_run(args, env, dev, world):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     value = n * world * steps / (float(t.item()) / 1000.0)
     return {"value": value, "unit": UNIT, "h2d_bytes_per_step": hs.bytes_h2d, "d2h_bytes_per_step": hs.bytes_d2h,
-            "api": "HostStepper.step (CUDA graph: pinned H2D actions, fused step+autoreset+observe+policy "
-                   "kernel, pinned D2H result)", "steps": steps}
+            "api": "HostStepper.step (one-node CUDA graph: the fused step+autoreset+observe+policy kernel "
+                   "reads the actions from and writes the result block to mapped pinned host memory)",
+            "steps": steps}
 
 
 def main():

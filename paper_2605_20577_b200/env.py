@@ -296,11 +296,14 @@ class HostStepper:
     """Host-driven stepping through pinned memory, one CUDA graph per step.
 
     Per `step()`: the actions in `actions` (pinned int32[n], written by the
-    caller) are copied to the device, one fused kernel steps every env
-    (optionally auto-resetting, observing and sampling the random policy's
-    next action), and the step result is copied back into pinned host
-    buffers.  The H2D copy, the kernel and the D2H copy are captured once
-    into a CUDA graph and replayed, so a step costs one graph launch.
+    caller) reach the device, one fused kernel steps every env (optionally
+    auto-resetting, observing and sampling the random policy's next action),
+    and the step result lands in pinned host buffers.  With `zero_copy`
+    (default) the kernel reads the actions and writes the result block
+    directly in the pinned host buffers (mapped host memory: the bytes cross
+    the host link inside the kernel, no copy engines, a one-node graph);
+    otherwise an H2D copy, the kernel and a D2H copy are captured into the
+    graph.  Either way a step costs one graph launch.
 
     Host result views (valid after `step()` returns): rewards f32[n,4],
     legal_bits i32[n,4], next_actions i32[n], current_player i8[n],
@@ -310,15 +313,19 @@ class HostStepper:
     BYTES_PER_ENV = 40
 
     def __init__(self, env: BatchEnv, *, autoreset: bool = True, observe: bool = True, policy: bool = True,
-                 graph: bool = True):
+                 graph: bool = True, zero_copy: bool = True):
         n, dev = env.n, env.device
         self.env = env
         self.n = n
         self.autoreset, self.observe, self.policy = autoreset, observe, policy
+        self.zero_copy = zero_copy
         self.actions = torch.zeros(n, dtype=torch.int32, pin_memory=True)
-        self._act_dev = torch.zeros(n, dtype=torch.int32, device=dev)
-        self._res_dev = torch.zeros(n * self.BYTES_PER_ENV, dtype=torch.uint8, device=dev)
         self._res_host = torch.zeros(n * self.BYTES_PER_ENV, dtype=torch.uint8, pin_memory=True)
+        if zero_copy:  # the kernel addresses the pinned buffers directly (unified addressing)
+            self._act_dev, self._res_dev = self.actions, self._res_host
+        else:
+            self._act_dev = torch.zeros(n, dtype=torch.int32, device=dev)
+            self._res_dev = torch.zeros(n * self.BYTES_PER_ENV, dtype=torch.uint8, device=dev)
         d, h = self._views(self._res_dev), self._views(self._res_host)
         self.rewards, self.legal_bits, self.next_actions = h["rewards"], h["legal_bits"], h["next_actions"]
         self.current_player, self.terminated = h["current_player"], h["terminated"]
@@ -356,6 +363,17 @@ class HostStepper:
         }
 
     def _body(self):
+        if self.zero_copy:
+            env = self.env
+            if env._obs is None:
+                env._obs = alloc_observations(env.n, env.device)
+            ost = obs_struct(env._obs) if self.observe else None
+            flags = (1 if self.autoreset else 0) | (2 if self.observe else 0)
+            check(env._L.rs_step_ex(env._h, self.actions.data_ptr(), flags, C.byref(self._out),
+                                    C.byref(ost) if ost is not None else None,
+                                    self._dev_views["next_actions"].data_ptr() if self.policy else None,
+                                    env._stream()), "rs_step_ex")
+            return
         self._act_dev.copy_(self.actions, non_blocking=True)
         self.env.step(self._act_dev, autoreset=self.autoreset, observe=self.observe,
                       next_actions=self._dev_views["next_actions"] if self.policy else None, out=self._out)

@@ -199,10 +199,12 @@ def test_step_tensors_match_records():
         assert bool(env.terminated[i]) == bool(r.env_terminated)
 
 
+@pytest.mark.parametrize("zero_copy", (True, False))
 @pytest.mark.parametrize("rule", RULES)
-def test_host_stepper_equals_fused_rollout(rule):
-    """HostStepper (CUDA graph: H2D actions, fused step+autoreset+observe+
-    policy, D2H results) follows the same trajectories as k_rollout."""
+def test_host_stepper_equals_fused_rollout(rule, zero_copy):
+    """HostStepper (CUDA graph: actions in, fused step+autoreset+observe+
+    policy, result block out -- through mapped pinned memory or explicit
+    copies) follows the same trajectories as k_rollout."""
     from paper_2605_20577_b200.env import HostStepper
 
     n, steps = 300, 150
@@ -210,7 +212,7 @@ def test_host_stepper_equals_fused_rollout(rule):
     a = BatchEnv(n, cfg).init(seed=9)
     b = BatchEnv(n, cfg).init(seed=9)
     a.rollout(steps)
-    hs = HostStepper(b, autoreset=True, observe=True, policy=True)
+    hs = HostStepper(b, autoreset=True, observe=True, policy=True, zero_copy=zero_copy)
     first = torch.empty(n, dtype=torch.int32, device="cuda")
     b.random_actions(out=first)
     hs.actions.copy_(first.cpu())
