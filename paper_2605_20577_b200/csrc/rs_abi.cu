@@ -303,7 +303,8 @@ __device__ __forceinline__ int env_of_thread(int gtid, int epw) {
 __global__ void __launch_bounds__(ROLL_BLOCK, ROLL_MINB) k_step(const __grid_constant__ Soa S, const __grid_constant__ DevTables D,
     const __grid_constant__ Cfg C, const int32_t* actions, int flags, rs_obs_out obs, int32_t* next_actions,
     StepOut out, int epw, int staged, int glog2) {
-  const Tabs T = stage_tables(D, glog2);
+  tables_begin(D, glog2);  // the action and header loads overlap the table copy
+  const Tabs T{};
   const int lane = threadIdx.x & 31;
   if ((lane >> glog2) >= epw) return;
   const int e = ((blockIdx.x * blockDim.x + threadIdx.x) >> 5) * epw + (lane >> glog2);
@@ -313,11 +314,13 @@ __global__ void __launch_bounds__(ROLL_BLOCK, ROLL_MINB) k_step(const __grid_con
     slot_bar_init(sb);
     stage_in(S, e, sb, 0);
   }
+  const int action = actions[e];  // may live in mapped host memory (HostStepper)
   Engine E(S, T, C, e, staged ? g_smem + sb : S.blk + (size_t)e * BLK_BYTES);
   E.load();
+  tables_wait();
   Mask115 m;
   float r[4];
-  const int st = E.step(actions[e], m, r);
+  const int st = E.step(action, m, r);
   const int term = E.g.env_terminated, trunc = E.g.env_truncated;
   bool dirty = st != RS_STATUS_CONTRACT;
   if ((flags & RS_STEP_AUTORESET) && (term || trunc)) {
