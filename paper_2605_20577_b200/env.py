@@ -313,19 +313,23 @@ class HostStepper:
     BYTES_PER_ENV = 40
 
     def __init__(self, env: BatchEnv, *, autoreset: bool = True, observe: bool = True, policy: bool = True,
-                 graph: bool = True, zero_copy: bool = True):
+                 graph: bool = True, zero_copy: bool | str = True):
         n, dev = env.n, env.device
         self.env = env
         self.n = n
         self.autoreset, self.observe, self.policy = autoreset, observe, policy
-        self.zero_copy = zero_copy
+        # "both" (True): actions and results through mapped pinned memory;
+        # "actions": actions mapped, results copied D2H; "none" (False): copies
+        mode = {True: "both", False: "none"}.get(zero_copy, zero_copy)
+        if mode not in ("both", "actions", "none"):
+            raise ValueError(f"bad zero_copy mode {zero_copy!r}")
+        self.zero_copy = mode
         self.actions = torch.zeros(n, dtype=torch.int32, pin_memory=True)
         self._res_host = torch.zeros(n * self.BYTES_PER_ENV, dtype=torch.uint8, pin_memory=True)
-        if zero_copy:  # the kernel addresses the pinned buffers directly (unified addressing)
-            self._act_dev, self._res_dev = self.actions, self._res_host
-        else:
-            self._act_dev = torch.zeros(n, dtype=torch.int32, device=dev)
-            self._res_dev = torch.zeros(n * self.BYTES_PER_ENV, dtype=torch.uint8, device=dev)
+        # the kernel addresses mapped pinned buffers directly (unified addressing)
+        self._act_dev = self.actions if mode != "none" else torch.zeros(n, dtype=torch.int32, device=dev)
+        self._res_dev = self._res_host if mode == "both" else torch.zeros(n * self.BYTES_PER_ENV, dtype=torch.uint8,
+                                                                          device=dev)
         d, h = self._views(self._res_dev), self._views(self._res_host)
         self.rewards, self.legal_bits, self.next_actions = h["rewards"], h["legal_bits"], h["next_actions"]
         self.current_player, self.terminated = h["current_player"], h["terminated"]
@@ -363,7 +367,7 @@ class HostStepper:
         }
 
     def _body(self):
-        if self.zero_copy:
+        if self.zero_copy != "none":
             env = self.env
             if env._obs is None:
                 env._obs = alloc_observations(env.n, env.device)
@@ -373,6 +377,8 @@ class HostStepper:
                                     C.byref(ost) if ost is not None else None,
                                     self._dev_views["next_actions"].data_ptr() if self.policy else None,
                                     env._stream()), "rs_step_ex")
+            if self.zero_copy == "actions":
+                self._res_host.copy_(self._res_dev, non_blocking=True)
             return
         self._act_dev.copy_(self.actions, non_blocking=True)
         self.env.step(self._act_dev, autoreset=self.autoreset, observe=self.observe,
