@@ -64,6 +64,9 @@ extern "C" {
 /* per-env status bits written by rs_step (reference env/core.py:85-94) */
 #define RS_STATUS_ILLEGAL 1u  /* masked-off action: penalty, episode ends   */
 #define RS_STATUS_CONTRACT 2u /* stepped a finished env: state unchanged   */
+#define RS_STATUS_INVARIANT 4u /* check_invariants failed after the step
+                                  (only when the handle checks every step:
+                                  RINSHAN_CHECK=1 at rs_create)            */
 
 /* rs_check_invariants violation bits (engine/state.py:105-180,
  * bench/runner.py:226-284) */

@@ -25,6 +25,7 @@ REWARD_RANK = 1
 
 STATUS_ILLEGAL = 1
 STATUS_CONTRACT = 2
+STATUS_INVARIANT = 4
 # rs_check_invariants bits (include/rinshan.h RS_INV_*)
 INV_SCORE_SUM = 1
 INV_TILES = 2

@@ -302,7 +302,7 @@ __device__ __forceinline__ int env_of_thread(int gtid, int epw) {
 
 __global__ void __launch_bounds__(ROLL_BLOCK, ROLL_MINB) k_step(const __grid_constant__ Soa S, const __grid_constant__ DevTables D,
     const __grid_constant__ Cfg C, const int32_t* actions, int flags, rs_obs_out obs, int32_t* next_actions,
-    StepOut out, int epw, int staged, int glog2) {
+    StepOut out, int epw, int staged, int glog2, int check) {
   tables_begin(D, glog2);  // the action and header loads overlap the table copy
   const Tabs T{};
   const int lane = threadIdx.x & 31;
@@ -336,6 +336,8 @@ __global__ void __launch_bounds__(ROLL_BLOCK, ROLL_MINB) k_step(const __grid_con
     next_actions[e] = done ? -1 : (flags & RS_STEP_HEURISTIC) ? E.heuristic_action(m) : E.random_action(m);
     dirty |= !done;
   }
+  int st_out = st;
+  if (check && check_invariants(E, true)) st_out |= (int)RS_STATUS_INVARIANT;  // debug: every step
   if (dirty) {
     E.store();
     if (staged) stage_out(S, e, sb);
@@ -345,7 +347,7 @@ __global__ void __launch_bounds__(ROLL_BLOCK, ROLL_MINB) k_step(const __grid_con
   if (out.rewards) reinterpret_cast<float4*>(out.rewards)[e] = make_float4(r[0], r[1], r[2], r[3]);
   if (out.terminated) out.terminated[e] = (uint8_t)term;
   if (out.truncated) out.truncated[e] = (uint8_t)trunc;
-  if (out.status) out.status[e] = (uint8_t)st;
+  if (out.status) out.status[e] = (uint8_t)st_out;
   if (staged && dirty) stage_wait_all();
 }
 
@@ -383,7 +385,8 @@ __global__ void __launch_bounds__(ROLL_BLOCK, ROLL_MINB) k_rollout(const __grid_
                                                    int obs_slots, int16_t* actions_log, int8_t* actors_log,
                                                    rs_rollout_stats* stats,
                                                    uint64_t* digests, StepOut out, int epw,
-                                                   uint32_t* prof, int staged, int policy, int glog2) {
+                                                   uint32_t* prof, int staged, int policy, int glog2,
+                                                   int check) {
   const uint32_t g_entry = prof ? globaltimer_lo() : 0u;
   tables_begin(D, glog2);  // the first env tile's header loads overlap the copy
   const Tabs T{};
@@ -415,6 +418,7 @@ __global__ void __launch_bounds__(ROLL_BLOCK, ROLL_MINB) k_rollout(const __grid_
     float r[4] = {0.f, 0.f, 0.f, 0.f};
     Mask115 m;
     int st = 0;
+    bool inv = false;
     const uint32_t g_first = prof ? globaltimer_lo() : 0u;
     for (int t = 0; t < steps; t++) {
       const long long t0 = prof ? clock64() : 0;
@@ -428,6 +432,7 @@ __global__ void __launch_bounds__(ROLL_BLOCK, ROLL_MINB) k_rollout(const __grid_
       const int a = policy == RS_POLICY_HEURISTIC ? E.heuristic_action(E.load_legal()) : E.random_action(E.load_legal());
       const int actor = E.g.current_player;
       st = E.step(a, m, r);
+      if (check && check_invariants(E, true)) inv = true;  // debug: every step
       if (actions_log) actions_log[(size_t)t * S.n + e] = (int16_t)a;
       if (actors_log) actors_log[(size_t)t * S.n + e] = (int8_t)(actor | (reset ? 4 : 0));
       if ((E.g.env_terminated || E.g.env_truncated) && sub == 0) games++;
@@ -449,7 +454,7 @@ __global__ void __launch_bounds__(ROLL_BLOCK, ROLL_MINB) k_rollout(const __grid_
     E.store();
     if (staged) stage_out(S, e, sb);
     if (digests) digests[e] = d;
-    write_step_out(out, e, E, m, r, st);
+    write_step_out(out, e, E, m, r, st | (inv ? (int)RS_STATUS_INVARIANT : 0));
     RS_SMARK(7);
     if (prof) {
       uint32_t* p = prof + ((size_t)steps * S.n + e) * 4;
@@ -546,6 +551,7 @@ struct rs_handle {
   // 78 M staged; 1M envs: 880 M vs 501 M)
   int stage_mode;
   int groups;  // idle lanes of small-batch warps join their env (RINSHAN_GROUPS=0: off)
+  int check_steps;  // RINSHAN_CHECK=1: fast invariants after every step -> RS_STATUS_INVARIANT
   int epw_override;         // RINSHAN_EPW (tuning experiments), 0 = heuristic
   bool persist;             // launch with the tables' L2 persisting window
   cudaAccessPolicyWindow window;
@@ -796,6 +802,8 @@ int rs_create(rs_handle** out, int64_t n_envs, const rs_config* cfg, int32_t dev
   h->stage_mode = stage_env ? std::max(0, std::min(2, atoi(stage_env))) : 0;
   const char* groups_env = getenv("RINSHAN_GROUPS");
   h->groups = groups_env ? (atoi(groups_env) != 0) : 1;
+  const char* check_env = getenv("RINSHAN_CHECK");
+  h->check_steps = check_env ? (atoi(check_env) != 0) : 0;
   const char* epw_env = getenv("RINSHAN_EPW");
   h->epw_override = epw_env ? std::max(0, std::min(32, atoi(epw_env))) : 0;
   *out = h;
@@ -838,7 +846,7 @@ int rs_step_ex(rs_handle* h, const int32_t* actions_dev, int32_t flags, const rs
   if (obs) o = *obs;
   const Launch L = step_launch(h, false);
   CUDA_TRY(launch_tables(h, k_step, L.grid, L.block, L.smem, st, h->S, h->D, h->cfg, actions_dev, flags, o,
-                         next_actions_dev, step_out(h, out), L.epw, L.staged, L.glog2));
+                         next_actions_dev, step_out(h, out), L.epw, L.staged, L.glog2, h->check_steps));
   return finish_step_out(h, out, st);
 }
 
@@ -887,7 +895,7 @@ int rs_rollout_policy(rs_handle* h, int32_t steps, int32_t policy, const rs_obs_
   const Launch L = step_launch(h, true);
   CUDA_TRY(launch_tables(h, k_rollout, L.grid, L.block, L.smem, st, h->S, h->D, h->cfg, steps, o,
                          obs ? obs_slots : 0, actions_log, actors_log, stats_dev, digests_dev, step_out(h, out),
-                         L.epw, nullptr, L.staged, policy, L.glog2));
+                         L.epw, nullptr, L.staged, policy, L.glog2, h->check_steps));
   return finish_step_out(h, out, st);
 }
 
@@ -902,7 +910,7 @@ int rs_debug_rollout_cycles(rs_handle* h, int32_t steps, const rs_obs_out* obs, 
   const Launch L = step_launch(h, true);
   CUDA_TRY(launch_tables(h, k_rollout, L.grid, L.block, L.smem, st, h->S, h->D, h->cfg, steps, o, obs ? 1 : 0,
                          nullptr, nullptr, nullptr, nullptr, StepOut{}, L.epw, prof_dev, L.staged,
-                         (int)RS_POLICY_RANDOM, L.glog2));
+                         (int)RS_POLICY_RANDOM, L.glog2, 0));
   CUDA_TRY(cudaGetLastError());
   return 0;
 }

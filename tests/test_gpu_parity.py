@@ -250,3 +250,29 @@ def test_device_soak_invariants(rule, policy):
     torch.cuda.synchronize()
     bad = torch.nonzero(flags).flatten().tolist()
     assert not bad, f"{len(bad)} envs violate, first {bad[:4]} flags {flags[bad[0]].item() if bad else 0}"
+
+
+def test_status_invariant_bit_when_checking_every_step(monkeypatch):
+    """SURVEY 8(b) status bit 2 (debug): with RINSHAN_CHECK=1 every step runs
+    the fast invariants; clean play never sets RS_STATUS_INVARIANT, a
+    corrupted state does"""
+    from paper_2605_20577_b200 import abi
+
+    monkeypatch.setenv("RINSHAN_CHECK", "1")
+    env = BatchEnv(256, EnvConfig(rule="red")).init(seed=31)
+    for _ in range(60):
+        env.rollout(1)
+        torch.cuda.synchronize()
+        assert int((env.status.int() & abi.STATUS_INVARIANT).sum().item()) == 0
+    for _ in range(20):
+        env.step(env.random_actions(), autoreset=True)
+        torch.cuda.synchronize()
+        assert int((env.status.int() & abi.STATUS_INVARIANT).sum().item()) == 0
+    i = next(i for i in range(256) if not env.export(i).env_terminated)
+    rec = env.export(i)
+    rec.scores[0] += 100  # the score identity no longer holds
+    env.load(i, rec)
+    acts = env.random_actions()
+    env.step(acts)
+    torch.cuda.synchronize()
+    assert int(env.status[i].item()) & abi.STATUS_INVARIANT
