@@ -46,6 +46,7 @@ def parse():
     p.add_argument("--cpu-seconds", type=float, default=12.0, help="CPU baseline sample budget")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-fused", action="store_true", help="skip the fused 100-step rollout timing")
     p.add_argument("--sweep", type=str, default="",
                    help="comma list of envs/GPU: one extra JSON line each (BASELINE configs[2])")
     p.add_argument("--fuse", type=int, default=1, help="env steps per k_rollout launch in --sweep")
@@ -323,6 +324,9 @@ def ours_arm(args, rank, world, local_rank):
     if not args.no_e2e:
         e2e = e2e_run(args, env, dev, world)
 
+    # ---- the same env steps fused 100 per launch ----
+    fused = None if args.no_fused else fused_run(args, dev, rank, world)
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         sps, threads, done, wall, _ = cpu_rollout(args, n, seconds=args.cpu_seconds, warmup=2)
@@ -369,6 +373,7 @@ def ours_arm(args, rank, world, local_rank):
                          "peak_source": "MEASURED_PEAKS.json hbm_gbs (burst copy)" if peaks else "fallback 6650"},
             "cpu_baseline": cpu,
             "e2e": e2e,
+            "fused_rollout": fused,
             "clocks": clk.summary(),
             "gpu_launches": args.steps,
             "games_completed": games,
@@ -378,6 +383,44 @@ def ours_arm(args, rank, world, local_rank):
         print(json.dumps(line), flush=True)
     env.close()
     return 0
+
+
+def fused_run(args, dev, rank, world, k=100):
+    """The bench workload as the reference's bench runs it (100 batch steps,
+    bench/runner.py:97-121) in one k_rollout launch of k env
+    steps per env: auto-reset, random policy, step, legal mask and the
+    current player's observation written EVERY step into a [k][n]
+    trajectory buffer; fresh envs, a 10-step warm-up launch, then 2 timed
+    launches (the same step range as the K=1 timing), L2 flushed between."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2605_20577_b200.env import BatchEnv, EnvConfig, alloc_observations
+
+    n = args.batch
+    env = BatchEnv(n, EnvConfig(rule=args.rule, mode=args.mode), device=dev).init(seed=args.seed,
+                                                                                   index_base=rank * n)
+    obs = alloc_observations(n, dev, slots=k)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream(dev)
+    env.rollout(10, obs=obs, obs_slots=1)
+    reps = 2
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(reps)]
+    torch.cuda.synchronize()
+    for i in range(reps):
+        flush.fill_(i & 255)
+        ev[i][0].record(stream)
+        env.rollout(k, obs=obs, obs_slots=k)
+        ev[i][1].record(stream)
+    torch.cuda.synchronize()
+    t = torch.tensor([sum(a.elapsed_time(b) for a, b in ev)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    env.close()
+    return {"value": n * world * k * reps / (float(t.item()) / 1000.0), "unit": UNIT, "steps_per_launch": k,
+            "launches": reps, "gpu_launches": reps,
+            "work": "auto-reset + random policy + step + legal mask + observation of the current player "
+                    "written every step into a [k][n] trajectory buffer; rewards / flags of the last step"}
 
 
 def e2e_run(args, env, dev, world):

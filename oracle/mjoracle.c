@@ -815,7 +815,7 @@ static int o_score_win(const orc_winctx* c, rs_win_rec* out, int8_t* order, int3
   o_dora_parts(c, &dora, &ura, &reds);
   int bonus = dora + ura + reds;
   OCand best;
-  best.valid = 0;
+  memset(&best, 0, sizeof(best));
 #define CONSIDER(YK, FU, FORM)                                                         \
   do {                                                                                 \
     OCand cd;                                                                          \
