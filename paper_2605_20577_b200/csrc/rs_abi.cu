@@ -41,7 +41,9 @@ constexpr int BLOCK = 128;
 // dynamic shared memory: the staged tables, then either one stage slot per
 // env of the CTA (staged stepping kernels) or a 144-byte shuffle scratch
 // per thread (kernels working on the blocks in HBM)
-constexpr int smem_staged(int slots) { return WALL_SLOT_OFF + slots * (int)SLOT_BYTES; }
+constexpr int smem_staged(int block, int slots) {
+  return WALL_SLOT_OFF + block * WALL_STRIDE + slots * (int)SLOT_BYTES;
+}
 constexpr int smem_for(int block) { return WALL_SLOT_OFF + block * WALL_STRIDE; }
 // bytes of the staged t3 | t1 | t2 block (a TMA bulk copy is a multiple of 16 B)
 constexpr uint32_t STAGE_BYTES = (SMEM_TABLE_BYTES + 15u) & ~15u;
@@ -204,8 +206,8 @@ __device__ __forceinline__ Tabs stage_tables(const DevTables& D, int grp_log2 = 
 // (rs_state.cuh): its 544-byte block moves HBM -> slot with one TMA bulk
 // copy completing on the slot's mbarrier, the step runs on shared memory,
 // and the block moves back with one bulk copy (bulk_group).
-__device__ __forceinline__ uint32_t slot_off(int slot) {
-  return (uint32_t)WALL_SLOT_OFF + (uint32_t)slot * SLOT_BYTES;
+__device__ __forceinline__ uint32_t slot_off(int slot) {  // after the per-thread shuffle scratch
+  return (uint32_t)WALL_SLOT_OFF + blockDim.x * (uint32_t)WALL_STRIDE + (uint32_t)slot * SLOT_BYTES;
 }
 __device__ __forceinline__ uint32_t smem_addr(uint32_t off) {
   return (uint32_t)__cvta_generic_to_shared(g_smem) + off;
@@ -215,12 +217,17 @@ __device__ __forceinline__ void slot_bar_init(uint32_t sb) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(sb + SLOT_BAR)) : "memory");
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
 }
-__device__ __forceinline__ void stage_in(const Soa& S, int e, uint32_t sb, uint32_t phase) {
+// one thread of the env's lane group issues the copy ...
+__device__ __forceinline__ void stage_issue(const Soa& S, int e, uint32_t sb) {
   const uint32_t dst = smem_addr(sb), bar = smem_addr(sb + SLOT_BAR);
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(BLK_BYTES) : "memory");
   asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
                "l"(S.blk + (size_t)e * BLK_BYTES), "r"(BLK_BYTES), "r"(bar)
                : "memory");
+}
+// ... and every lane of the group waits for the phase
+__device__ __forceinline__ void stage_wait(uint32_t sb, uint32_t phase) {
+  const uint32_t bar = smem_addr(sb + SLOT_BAR);
   asm volatile(
       "{\n"
       ".reg .pred p;\n"
@@ -309,10 +316,17 @@ __global__ void __launch_bounds__(ROLL_BLOCK, ROLL_MINB) k_step(const __grid_con
   if ((lane >> glog2) >= epw) return;
   const int e = ((blockIdx.x * blockDim.x + threadIdx.x) >> 5) * epw + (lane >> glog2);
   if (e >= S.n) return;
-  const uint32_t sb = slot_off((threadIdx.x >> 5) * epw + lane);
+  // one stage slot per env, shared by the env's lane group
+  const uint32_t sb = slot_off((threadIdx.x >> 5) * epw + (lane >> glog2));
+  const int sub = lane & ((1 << glog2) - 1);
+  const uint32_t gm = glog2 >= 5 ? 0xFFFFFFFFu : (((1u << (1 << glog2)) - 1u) << (lane - sub));
   if (staged) {
-    slot_bar_init(sb);
-    stage_in(S, e, sb, 0);
+    if (sub == 0) {
+      slot_bar_init(sb);
+      stage_issue(S, e, sb);
+    }
+    __syncwarp(gm);  // the slot's barrier is initialised for the whole group
+    stage_wait(sb, 0);
   }
   const int action = actions[e];  // may live in mapped host memory (HostStepper)
   Engine E(S, T, C, e, staged ? g_smem + sb : S.blk + (size_t)e * BLK_BYTES);
@@ -340,7 +354,10 @@ __global__ void __launch_bounds__(ROLL_BLOCK, ROLL_MINB) k_step(const __grid_con
   if (check && check_invariants(E, true)) st_out |= (int)RS_STATUS_INVARIANT;  // debug: every step
   if (dirty) {
     E.store();
-    if (staged) stage_out(S, e, sb);
+    if (staged) {
+      __syncwarp(gm);  // every lane's writes to the slot precede the bulk store
+      if (sub == 0) stage_out(S, e, sb);
+    }
   }
   if (out.legal_bits) reinterpret_cast<uint4*>(out.legal_bits)[e] = make_uint4(m.m[0], m.m[1], m.m[2], m.m[3]);
   if (out.current_player) out.current_player[e] = (int8_t)E.g.current_player;
@@ -348,7 +365,7 @@ __global__ void __launch_bounds__(ROLL_BLOCK, ROLL_MINB) k_step(const __grid_con
   if (out.terminated) out.terminated[e] = (uint8_t)term;
   if (out.truncated) out.truncated[e] = (uint8_t)trunc;
   if (out.status) out.status[e] = (uint8_t)st_out;
-  if (staged && dirty) stage_wait_all();
+  if (staged && dirty && sub == 0) stage_wait_all();
 }
 
 __global__ void __launch_bounds__(BLOCK) k_policy(const __grid_constant__ Soa S, const __grid_constant__ DevTables D,
@@ -395,16 +412,22 @@ __global__ void __launch_bounds__(ROLL_BLOCK, ROLL_MINB) k_rollout(const __grid_
   unsigned long long games = 0;
   const int lane = threadIdx.x & 31;
   const int warps = (gridDim.x * blockDim.x) >> 5;
-  const uint32_t sb = slot_off((threadIdx.x >> 5) * epw + lane);
-  if (staged && lane < epw) slot_bar_init(sb);
-  uint32_t phase = 0;
   const int sub = lane & ((1 << glog2) - 1);  // the lane's index in its env's group
+  const uint32_t gm = glog2 >= 5 ? 0xFFFFFFFFu : (((1u << (1 << glog2)) - 1u) << (lane - sub));
+  // one stage slot per env, shared by the env's lane group
+  const uint32_t sb = slot_off((threadIdx.x >> 5) * epw + (lane >> glog2));
+  if (staged && (lane >> glog2) < epw && sub == 0) slot_bar_init(sb);
+  uint32_t phase = 0;
   for (int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; w * epw < S.n; w += warps) {
     const int e = w * epw + (lane >> glog2);
     if ((lane >> glog2) >= epw || e >= S.n) continue;
     if (staged) {
-      stage_wait_read();  // the slot's previous block has left
-      stage_in(S, e, sb, phase);
+      if (sub == 0) {
+        stage_wait_read();  // the slot's previous block has left
+        stage_issue(S, e, sb);
+      }
+      __syncwarp(gm);  // (first tile: the slot's barrier is initialised)
+      stage_wait(sb, phase);
       phase ^= 1u;
     }
     Engine E(S, T, C, e, staged ? g_smem + sb : S.blk + (size_t)e * BLK_BYTES);
@@ -452,7 +475,10 @@ __global__ void __launch_bounds__(ROLL_BLOCK, ROLL_MINB) k_rollout(const __grid_
       }
     }
     E.store();
-    if (staged) stage_out(S, e, sb);
+    if (staged) {
+      __syncwarp(gm);  // every lane's writes to the slot precede the bulk store
+      if (sub == 0) stage_out(S, e, sb);
+    }
     if (digests) digests[e] = d;
     write_step_out(out, e, E, m, r, st | (inv ? (int)RS_STATUS_INVARIANT : 0));
     RS_SMARK(7);
@@ -461,7 +487,7 @@ __global__ void __launch_bounds__(ROLL_BLOCK, ROLL_MINB) k_rollout(const __grid_
       p[0] = g_entry; p[1] = g_staged; p[2] = g_first; p[3] = globaltimer_lo();
     }
   }
-  if (staged) stage_wait_all();
+  if (staged && sub == 0) stage_wait_all();
   if (stats) {
     unsigned long long g = games;
     for (int off = 16; off > 0; off >>= 1) g += __shfl_down_sync(0xffffffffu, g, off);
@@ -617,9 +643,9 @@ Launch launch_at(rs_handle* h, int epw) {
   L.staged = h->stage_mode == 2 || (h->stage_mode == 1 && epw < 32);
   // idle lanes join their env as a lane group (not with the stage: one slot per lane)
   L.glog2 = 0;
-  if (!L.staged && h->groups)
+  if (h->groups)
     while ((epw << (L.glog2 + 1)) <= 32) L.glog2++;
-  L.smem = L.staged ? smem_staged(L.block / 32 * epw) : smem_for(L.block);
+  L.smem = L.staged ? smem_staged(L.block, L.block / 32 * epw) : smem_for(L.block);
   L.ctas = resident_ctas(h, L.block, L.smem);
   L.grid = warp_grid(h, epw, L.block, 0);
   return L;
@@ -793,7 +819,7 @@ int rs_create(rs_handle** out, int64_t n_envs, const rs_config* cfg, int32_t dev
                            (const void*)k_observe, (const void*)k_rollout, (const void*)k_export,
                            (const void*)k_import, (const void*)k_autoreset, (const void*)k_check};
   for (const void* k : kernels)
-    if ((err = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_staged(ROLL_BLOCK))))
+    if ((err = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_staged(ROLL_BLOCK, ROLL_BLOCK))))
       return cleanup(err, "cudaFuncSetAttribute");
   if ((err = cudaDeviceGetAttribute(&h->num_sms, cudaDevAttrMultiProcessorCount, device)))
     return cleanup(err, "device query");

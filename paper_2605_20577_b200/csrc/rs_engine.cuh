@@ -141,7 +141,8 @@ struct Engine {
     // 144-byte scratch after the tables (copied to the block afterwards)
     uint8_t* const wall_dst = swall(bp);
 #if defined(__CUDA_ARCH__)
-    const bool in_place = __isShared(wall_dst);
+    // (a staged wall is shared by the env's lane group: lanes shuffle privately)
+    const bool in_place = __isShared(wall_dst) && grp_size() == 1;
     uint8_t* w = in_place ? wall_dst : g_smem + WALL_SLOT_OFF + threadIdx.x * WALL_STRIDE;
 #else
     const bool in_place = true;
