@@ -395,12 +395,13 @@ def fused_run(args, dev, rank, world, k=100):
     import torch
     import torch.distributed as dist
 
-    from paper_2605_20577_b200.env import BatchEnv, EnvConfig, alloc_observations
+    from paper_2605_20577_b200.env import BatchEnv, EnvConfig, alloc_observations, alloc_trajectory
 
     n = args.batch
     env = BatchEnv(n, EnvConfig(rule=args.rule, mode=args.mode), device=dev).init(seed=args.seed,
                                                                                    index_base=rank * n)
     obs = alloc_observations(n, dev, slots=k)
+    traj = alloc_trajectory(k, n, dev)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream(dev)
     env.rollout(10, obs=obs, obs_slots=1)
@@ -410,7 +411,7 @@ def fused_run(args, dev, rank, world, k=100):
     for i in range(reps):
         flush.fill_(i & 255)
         ev[i][0].record(stream)
-        env.rollout(k, obs=obs, obs_slots=k)
+        env.rollout(k, obs=obs, obs_slots=k, traj=traj)
         ev[i][1].record(stream)
     torch.cuda.synchronize()
     t = torch.tensor([sum(a.elapsed_time(b) for a, b in ev)], dtype=torch.float64, device=dev)
@@ -419,8 +420,9 @@ def fused_run(args, dev, rank, world, k=100):
     env.close()
     return {"value": n * world * k * reps / (float(t.item()) / 1000.0), "unit": UNIT, "steps_per_launch": k,
             "launches": reps, "gpu_launches": reps,
-            "work": "auto-reset + random policy + step + legal mask + observation of the current player "
-                    "written every step into a [k][n] trajectory buffer; rewards / flags of the last step"}
+            "work": "auto-reset + random policy + step, and every step's outputs (packed legal mask, "
+                    "current player, rewards, flags, observation of the current player) written into "
+                    "[k][n] trajectory buffers"}
 
 
 def e2e_run(args, env, dev, world):

@@ -310,10 +310,15 @@ int rs_rollout(rs_handle* h, int32_t steps, const rs_obs_out* obs, int32_t obs_s
 #define RS_POLICY_HEURISTIC 1
 /* actors_log (may be NULL): [steps][n] int8, the seat that acted at each
  * step (engine state.actor, the mjlog-lite [seat, action] pair) | 4 when
- * the env was auto-reset just before that step (a new game starts there) */
+ * the env was auto-reset just before that step (a new game starts there).
+ * traj (may be NULL): the per-step outputs of every step (packed
+ * legal_bits [steps][n][4], current_player [steps][n], rewards
+ * [steps][n][4], terminated / truncated / status [steps][n]; any field may
+ * be NULL, legal_mask must be), i.e. with obs_slots = steps a complete
+ * trajectory buffer of the rollout. */
 int rs_rollout_policy(rs_handle* h, int32_t steps, int32_t policy, const rs_obs_out* obs, int32_t obs_slots,
-                      int16_t* actions_log, int8_t* actors_log, rs_rollout_stats* stats_dev,
-                      uint64_t* digests_dev, const rs_step_out* out, void* stream);
+                      int16_t* actions_log, int8_t* actors_log, const rs_step_out* traj,
+                      rs_rollout_stats* stats_dev, uint64_t* digests_dev, const rs_step_out* out, void* stream);
 
 /* auto-reset (bench/runner.py:107-109): every finished env starts its next
  * game from env_game_seed(seed, index, resets + 1); outputs for all envs */

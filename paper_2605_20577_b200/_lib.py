@@ -85,7 +85,7 @@ def lib():
         L.rs_observe.argtypes = [vp, vp, vp, vp]
         L.rs_policy_random.argtypes = [vp, vp, vp]
         L.rs_rollout.argtypes = [vp, i32, vp, i32, vp, vp, vp, vp, vp]
-        L.rs_rollout_policy.argtypes = [vp, i32, i32, vp, i32, vp, vp, vp, vp, vp, vp]
+        L.rs_rollout_policy.argtypes = [vp, i32, i32, vp, i32, vp, vp, vp, vp, vp, vp, vp]
         L.rs_policy_heuristic.argtypes = [vp, vp, vp]
         L.rs_autoreset.argtypes = [vp, vp, vp]
         L.rs_check_invariants.argtypes = [vp, i32, vp, vp]

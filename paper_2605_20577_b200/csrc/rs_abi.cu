@@ -256,7 +256,7 @@ __device__ __forceinline__ uint32_t globaltimer_lo() {
   return t;
 }
 
-__device__ __forceinline__ void write_step_out(const StepOut& o, int e, const Engine& E, const Mask115& m,
+__device__ __forceinline__ void write_step_out(const StepOut& o, int64_t e, const Engine& E, const Mask115& m,
                                                const float* r, int status) {
   if (o.legal_bits) {
     reinterpret_cast<uint4*>(o.legal_bits)[e] = make_uint4(m.m[0], m.m[1], m.m[2], m.m[3]);
@@ -400,7 +400,7 @@ __global__ void __launch_bounds__(BLOCK) k_observe(const __grid_constant__ Soa S
 __global__ void __launch_bounds__(ROLL_BLOCK, ROLL_MINB) k_rollout(const __grid_constant__ Soa S, const __grid_constant__ DevTables D,
     const __grid_constant__ Cfg C, int steps, rs_obs_out obs,
                                                    int obs_slots, int16_t* actions_log, int8_t* actors_log,
-                                                   rs_rollout_stats* stats,
+                                                   StepOut traj, rs_rollout_stats* stats,
                                                    uint64_t* digests, StepOut out, int epw,
                                                    uint32_t* prof, int staged, int policy, int glog2,
                                                    int check) {
@@ -458,6 +458,9 @@ __global__ void __launch_bounds__(ROLL_BLOCK, ROLL_MINB) k_rollout(const __grid_
       if (check && check_invariants(E, true)) inv = true;  // debug: every step
       if (actions_log) actions_log[(size_t)t * S.n + e] = (int16_t)a;
       if (actors_log) actors_log[(size_t)t * S.n + e] = (int8_t)(actor | (reset ? 4 : 0));
+      // per-step outputs into [steps][n] trajectory buffers (rs_rollout_policy traj)
+      if (traj.legal_bits || traj.rewards || traj.current_player || traj.terminated || traj.status)
+        write_step_out(traj, (int64_t)t * S.n + e, E, m, r, st);
       if ((E.g.env_terminated || E.g.env_truncated) && sub == 0) games++;
       if (digests) d = digest_step(d, a, E, m, r);
       if (obs_slots > 0 && (obs_slots > 1 || t == steps - 1)) {
@@ -578,6 +581,7 @@ struct rs_handle {
   int stage_mode;
   int groups;  // idle lanes of small-batch warps join their env (RINSHAN_GROUPS=0: off)
   int check_steps;  // RINSHAN_CHECK=1: fast invariants after every step -> RS_STATUS_INVARIANT
+  int block_override;  // RINSHAN_BLOCK (tuning experiments): stepping-kernel CTA size
   int epw_override;         // RINSHAN_EPW (tuning experiments), 0 = heuristic
   bool persist;             // launch with the tables' L2 persisting window
   cudaAccessPolicyWindow window;
@@ -640,6 +644,7 @@ Launch launch_at(rs_handle* h, int epw) {
   L.epw = epw;
   const int64_t warps = (h->n + epw - 1) / epw;
   L.block = warps * 32 >= (int64_t)h->num_sms * ROLL_BLOCK ? ROLL_BLOCK : BLOCK;
+  if (h->block_override > 0) L.block = h->block_override;
   L.staged = h->stage_mode == 2 || (h->stage_mode == 1 && epw < 32);
   // idle lanes join their env as a lane group (not with the stage: one slot per lane)
   L.glog2 = 0;
@@ -830,6 +835,8 @@ int rs_create(rs_handle** out, int64_t n_envs, const rs_config* cfg, int32_t dev
   h->groups = groups_env ? (atoi(groups_env) != 0) : 1;
   const char* check_env = getenv("RINSHAN_CHECK");
   h->check_steps = check_env ? (atoi(check_env) != 0) : 0;
+  const char* block_env = getenv("RINSHAN_BLOCK");
+  h->block_override = block_env ? std::max(0, std::min(ROLL_BLOCK, atoi(block_env) & ~31)) : 0;
   const char* epw_env = getenv("RINSHAN_EPW");
   h->epw_override = epw_env ? std::max(0, std::min(32, atoi(epw_env))) : 0;
   *out = h;
@@ -902,13 +909,14 @@ int rs_policy_heuristic(rs_handle* h, int32_t* actions_dev, void* stream) {
 
 int rs_rollout(rs_handle* h, int32_t steps, const rs_obs_out* obs, int32_t obs_slots, int16_t* actions_log,
                rs_rollout_stats* stats_dev, uint64_t* digests_dev, const rs_step_out* out, void* stream) {
-  return rs_rollout_policy(h, steps, RS_POLICY_RANDOM, obs, obs_slots, actions_log, nullptr, stats_dev,
+  return rs_rollout_policy(h, steps, RS_POLICY_RANDOM, obs, obs_slots, actions_log, nullptr, nullptr, stats_dev,
                            digests_dev, out, stream);
 }
 
 int rs_rollout_policy(rs_handle* h, int32_t steps, int32_t policy, const rs_obs_out* obs, int32_t obs_slots,
-                      int16_t* actions_log, int8_t* actors_log, rs_rollout_stats* stats_dev,
-                      uint64_t* digests_dev, const rs_step_out* out, void* stream) {
+                      int16_t* actions_log, int8_t* actors_log, const rs_step_out* traj,
+                      rs_rollout_stats* stats_dev, uint64_t* digests_dev, const rs_step_out* out, void* stream) {
+  if (traj && traj->legal_mask) return set_err(RS_E_ARG, "rs_rollout: traj takes packed legal_bits, not legal_mask");
   if (!h || steps < 0) return set_err(RS_E_ARG, "rs_rollout: bad arguments");
   if (policy != RS_POLICY_RANDOM && policy != RS_POLICY_HEURISTIC) return set_err(RS_E_ARG, "rs_rollout: unknown policy");
   if (obs_slots < 0 || (obs_slots > 1 && obs_slots != steps)) return set_err(RS_E_ARG, "obs_slots must be 0, 1 or steps");
@@ -920,7 +928,8 @@ int rs_rollout_policy(rs_handle* h, int32_t steps, int32_t policy, const rs_obs_
   // envs walked grid-stride)
   const Launch L = step_launch(h, true);
   CUDA_TRY(launch_tables(h, k_rollout, L.grid, L.block, L.smem, st, h->S, h->D, h->cfg, steps, o,
-                         obs ? obs_slots : 0, actions_log, actors_log, stats_dev, digests_dev, step_out(h, out),
+                         obs ? obs_slots : 0, actions_log, actors_log, step_out(h, traj), stats_dev, digests_dev,
+                         step_out(h, out),
                          L.epw, nullptr, L.staged, policy, L.glog2, h->check_steps));
   return finish_step_out(h, out, st);
 }
@@ -935,7 +944,7 @@ int rs_debug_rollout_cycles(rs_handle* h, int32_t steps, const rs_obs_out* obs, 
   if (obs) o = *obs;
   const Launch L = step_launch(h, true);
   CUDA_TRY(launch_tables(h, k_rollout, L.grid, L.block, L.smem, st, h->S, h->D, h->cfg, steps, o, obs ? 1 : 0,
-                         nullptr, nullptr, nullptr, nullptr, StepOut{}, L.epw, prof_dev, L.staged,
+                         nullptr, nullptr, StepOut{}, nullptr, nullptr, StepOut{}, L.epw, prof_dev, L.staged,
                          (int)RS_POLICY_RANDOM, L.glog2, 0));
   CUDA_TRY(cudaGetLastError());
   return 0;

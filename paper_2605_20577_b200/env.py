@@ -90,6 +90,19 @@ def alloc_observations(n: int, device, slots: int | None = None) -> Observations
     )
 
 
+def alloc_trajectory(steps: int, n: int, device) -> dict:
+    """per-step output buffers of a fused rollout (BatchEnv.rollout traj=)"""
+    kw = dict(device=device)
+    return {
+        "legal_bits": torch.empty(steps, n, 4, dtype=torch.int32, **kw),
+        "current_player": torch.empty(steps, n, dtype=torch.int8, **kw),
+        "rewards": torch.empty(steps, n, 4, dtype=torch.float32, **kw),
+        "terminated": torch.empty(steps, n, dtype=torch.uint8, **kw),
+        "truncated": torch.empty(steps, n, dtype=torch.uint8, **kw),
+        "status": torch.empty(steps, n, dtype=torch.uint8, **kw),
+    }
+
+
 def obs_struct(o: Observations) -> abi.rs_obs_out:
     return abi.rs_obs_out(
         hand_tokens=_ptr(o["hand_tokens"]), event_tokens=_ptr(o["event_tokens"]),
@@ -266,17 +279,28 @@ class BatchEnv:
     def rollout(self, steps: int, obs: Observations | None = None, obs_slots: int = 0,
                 actions_log: torch.Tensor | None = None, stats: torch.Tensor | None = None,
                 digests: torch.Tensor | None = None, policy: str = "random",
-                actors_log: torch.Tensor | None = None) -> "BatchEnv":
+                actors_log: torch.Tensor | None = None, traj: dict | None = None) -> "BatchEnv":
         """Fused `steps` x {auto-reset, policy, step, observe} per env in one
         kernel (bench/runner.py:97-121); `policy` is "random" (the bench
         loop) or "heuristic".  stats: int64[3] CUDA tensor (steps,
         games_completed, illegal) accumulated; digests: int64[n];
         actions_log int16[steps, n] / actors_log int8[steps, n]: the action and
-        the acting seat of every step (| 4 where an auto-reset preceded it)."""
+        the acting seat of every step (| 4 where an auto-reset preceded it);
+        traj: per-step outputs, a dict of [steps, n, ...] CUDA tensors with any
+        of legal_bits (int32 [.., 4]), current_player (int8), rewards
+        (float32 [.., 4]), terminated / truncated / status (uint8) --
+        `alloc_trajectory(steps, n)` makes one."""
         st = obs_struct(obs) if obs is not None else None
+        tr = None
+        if traj is not None:
+            tr = abi.rs_step_out(legal_mask=None, legal_bits=_ptr(traj.get("legal_bits")),
+                                 current_player=_ptr(traj.get("current_player")), rewards=_ptr(traj.get("rewards")),
+                                 terminated=_ptr(traj.get("terminated")), truncated=_ptr(traj.get("truncated")),
+                                 status=_ptr(traj.get("status")))
         check(self._L.rs_rollout_policy(
             self._h, int(steps), _policy_id(policy), C.byref(st) if st is not None else None,
-            int(obs_slots if obs is not None else 0), _ptr(actions_log), _ptr(actors_log), _ptr(stats), _ptr(digests),
+            int(obs_slots if obs is not None else 0), _ptr(actions_log), _ptr(actors_log),
+            C.byref(tr) if tr is not None else None, _ptr(stats), _ptr(digests),
             C.byref(self._out), self._stream()), "rs_rollout")
         return self
 

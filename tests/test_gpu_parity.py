@@ -276,3 +276,32 @@ def test_status_invariant_bit_when_checking_every_step(monkeypatch):
     env.step(acts)
     torch.cuda.synchronize()
     assert int(env.status[i].item()) & abi.STATUS_INVARIANT
+
+
+@pytest.mark.parametrize("rule", RULES)
+def test_fused_trajectory_equals_single_steps(rule):
+    """rs_rollout_policy traj: the per-step outputs of one K-step launch
+    (mask, player, rewards, flags, and the observation with obs_slots = K)
+    equal those of K one-step launches"""
+    from paper_2605_20577_b200.env import alloc_observations, alloc_trajectory
+
+    n, k = 512, 40
+    cfg = EnvConfig(rule=rule)
+    a = BatchEnv(n, cfg).init(seed=19)
+    b = BatchEnv(n, cfg).init(seed=19)
+    a.rollout(100)
+    b.rollout(100)
+    traj = alloc_trajectory(k, n, a.device)
+    obs_a = alloc_observations(n, a.device, slots=k)
+    a.rollout(k, obs=obs_a, obs_slots=k, traj=traj)
+    obs_b = alloc_observations(n, b.device)
+    for t in range(k):
+        b.rollout(1, obs=obs_b, obs_slots=1)
+        torch.cuda.synchronize()
+        assert torch.equal(traj["legal_bits"][t], b.legal_bits), t
+        assert torch.equal(traj["current_player"][t], b.current_player), t
+        assert torch.equal(traj["rewards"][t], b.rewards), t
+        assert torch.equal(traj["terminated"][t], b.terminated.to(torch.uint8)), t
+        assert torch.equal(traj["status"][t], b.status), t
+        for key in ("hand_tokens", "event_tokens", "scores", "dora_indicator_tokens"):
+            assert torch.equal(obs_a[key][t], obs_b[key]), (t, key)
