@@ -44,33 +44,29 @@ RS_HD void write_obs(const Engine& E, int seat, const rs_obs_out& obs, int64_t o
     const uint32_t len = g.events_len;
     const int pad = len >= 64u ? 0 : 64 - (int)len;
     uint4* dst = reinterpret_cast<uint4*>(obs.event_tokens + o * 192);
-    // two halves of 32 slots: all 32 loads are issued before the first
-    // store (stores to the output could alias the ring as far as the
-    // compiler knows, so interleaving them would serialise the loads)
-    // with a lane group, lanes 0 and 1 of the group write one half each
+    // four quarters of 16 slots, each loaded completely before its stores
+    // (stores to the output could alias the ring as far as the compiler
+    // knows); with a lane group, lanes 0-3 of the group take one quarter
+    // each -- the same instructions on different data, so the warp runs
+    // the quarter body once
     const int G = grp_size(), sub = grp_sub();
     auto emit_window = [&](auto slot) {
+      for (int q = sub; q < 4; q += G) {
+        uint32_t v[16];
 #pragma unroll
-      for (int half = 0; half < 2; half++) {
-        if (G > 1 && half != sub) continue;
-        uint32_t v[32];
+        for (int j = 0; j < 16; j++) v[j] = slot(16 * q + j);
+        uint32_t w[12];
 #pragma unroll
-        for (int i = 0; i < 32; i++) v[i] = slot(32 * half + i);
-#pragma unroll
-        for (int q = 0; q < 2; q++) {
-          uint32_t w[12];
-#pragma unroll
-          for (int r = 0; r < 4; r++) {
-            const int i0 = 16 * q + 4 * r;
-            w[3 * r] = byte_perm(v[i0], v[i0 + 1], 0x4210);
-            w[3 * r + 1] = byte_perm(v[i0 + 1], v[i0 + 2], 0x5421);
-            w[3 * r + 2] = byte_perm(v[i0 + 2], v[i0 + 3], 0x6542);
-          }
-          uint4* d = dst + 6 * half + 3 * q;
-          d[0] = make_uint4(w[0], w[1], w[2], w[3]);
-          d[1] = make_uint4(w[4], w[5], w[6], w[7]);
-          d[2] = make_uint4(w[8], w[9], w[10], w[11]);
+        for (int r = 0; r < 4; r++) {
+          const int i0 = 4 * r;
+          w[3 * r] = byte_perm(v[i0], v[i0 + 1], 0x4210);
+          w[3 * r + 1] = byte_perm(v[i0 + 1], v[i0 + 2], 0x5421);
+          w[3 * r + 2] = byte_perm(v[i0 + 2], v[i0 + 3], 0x6542);
         }
+        uint4* d = dst + 3 * q;
+        d[0] = make_uint4(w[0], w[1], w[2], w[3]);
+        d[1] = make_uint4(w[4], w[5], w[6], w[7]);
+        d[2] = make_uint4(w[8], w[9], w[10], w[11]);
       }
     };
     if (pad == 0)  // a full window (every step after the first 64 events)
