@@ -68,8 +68,12 @@ struct Mask115 {
       uint32_t x = w == 0 ? m[0] : w == 1 ? m[1] : w == 2 ? m[2] : m[3];
       const int c = popc32(x);
       if (i < c) {
+#if defined(__CUDA_ARCH__)
+        return 32 * w + (int)__fns(x, 0u, i + 1);  // the (i+1)-th set bit from bit 0
+#else
         for (int j = 0; j < i; j++) x &= x - 1;
         return 32 * w + ctz32(x);
+#endif
       }
       i -= c;
     }
@@ -374,13 +378,15 @@ struct Engine {
   RS_HD void discard_bits(const Hand& h, bool only_tenpai, Mask115& m) const {
     uint64_t present = h.kinds_ge(1);
     if (only_tenpai) {
-      // the group's lanes take every G-th held kind
+      // lane `sub` of the group takes held kinds sub, sub + G, ... (one
+      // evaluation per lane and round: the same instructions, different kinds)
       const int G = grp_size(), sub = grp_sub();
       uint64_t keep = 0, p = present;
-      for (int j = 0; p; j++) {
+      for (int j = 0; j < sub && p; j++) p &= p - 1;  // drop the kinds of the lanes before
+      while (p) {
         const int k = ctz64(p);
-        p &= p - 1;
-        if ((j & (G - 1)) == sub && shanten_minus_kind(T, h, k) == 0) keep |= 1ull << k;
+        if (shanten_minus_kind(T, h, k) == 0) keep |= 1ull << k;
+        for (int j = 0; j < G && p; j++) p &= p - 1;  // this lane's next kind
       }
       present = grp_or64(keep);
     }
