@@ -68,12 +68,9 @@ struct Mask115 {
       uint32_t x = w == 0 ? m[0] : w == 1 ? m[1] : w == 2 ? m[2] : m[3];
       const int c = popc32(x);
       if (i < c) {
-#if defined(__CUDA_ARCH__)
-        return 32 * w + (int)__fns(x, 0u, i + 1);  // the (i+1)-th set bit from bit 0
-#else
+        // (a loop: __fns is emulated in software on sm_100 and costs more)
         for (int j = 0; j < i; j++) x &= x - 1;
         return 32 * w + ctz32(x);
-#endif
       }
       i -= c;
     }
