@@ -5,7 +5,7 @@ sys.path.insert(0, '.')
 from paper_2605_20577_b200.env import BatchEnv, EnvConfig, alloc_observations
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 4096
 env = BatchEnv(n, EnvConfig(rule='no-red')).init(seed=0)
-env.rollout(50)
+env.rollout(300)
 marks = torch.zeros(64 * n * 8 + 8 * 200000, dtype=torch.int64, device='cuda')
 env._L.rs_debug_set_marks.argtypes = [C.c_void_p]
 env._L.rs_debug_set_marks(marks.data_ptr())
