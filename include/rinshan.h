@@ -213,6 +213,19 @@ typedef struct rs_step_out {
   uint8_t* status;       /* [n] RS_STATUS_* bits, may be NULL               */
 } rs_step_out;
 
+/* one env's step result as one 40-byte record (rs_step_rec_out): what a
+ * host-driven actor reads back per step, packed so the writes of an env
+ * are contiguous (e.g. into mapped pinned host memory) */
+typedef struct rs_step_rec {
+  float rewards[4];
+  uint32_t legal_bits[4];
+  int32_t next_action;   /* the policy's next action, -1 for finished envs  */
+  int8_t current_player;
+  uint8_t terminated;
+  uint8_t truncated;
+  uint8_t status;
+} rs_step_rec;
+
 /* observation tensors (reference docs/formats.md:32-52, env/observe.py:50-62) */
 typedef struct rs_obs_out {
   uint8_t* hand_tokens;  /* [n][14]                                         */
@@ -282,6 +295,11 @@ int rs_step(rs_handle* h, const int32_t* actions_dev, const rs_step_out* out, vo
 #define RS_STEP_HEURISTIC 4
 int rs_step_ex(rs_handle* h, const int32_t* actions_dev, int32_t flags, const rs_step_out* out,
                const rs_obs_out* obs, int32_t* next_actions_dev, void* stream);
+/* rs_step_ex with the per-env outputs and the next action (random, or
+ * heuristic with RS_STEP_HEURISTIC) written as one rs_step_rec per env into
+ * recs[n] (device or mapped pinned host memory) */
+int rs_step_rec_out(rs_handle* h, const int32_t* actions, int32_t flags, rs_step_rec* recs,
+                    const rs_obs_out* obs, void* stream);
 /* seats_dev: device int8[n] or NULL for each env's current player */
 int rs_observe(rs_handle* h, const int8_t* seats_dev, const rs_obs_out* obs, void* stream);
 /* random policy over each env's legal list using its policy stream */
@@ -333,8 +351,8 @@ int rs_check_invariants(rs_handle* h, int32_t fast, uint32_t* flags_dev, void* s
 int rs_export_env(rs_handle* h, int64_t env, rs_env_rec* out);
 int rs_import_env(rs_handle* h, int64_t env, const rs_env_rec* in);
 /* sizeof of the records above, for binding checks: config, meld, hand,
- * win, result, env */
-int rs_record_sizes(int32_t* out /*[6]*/);
+ * win, result, env, step */
+int rs_record_sizes(int32_t* out /*[7]*/);
 
 /* profiling hook: a fused rollout recording, per env and step, the clock64
  * cycles of the auto-reset and of policy + step + observe, the action and

@@ -25,7 +25,8 @@ INCLUDE = PKG_DIR.parent / "include" / "rinshan.h"
 SYMBOLS = (
     "rs_last_error", "rs_abi_version", "rs_tables_build", "rs_tables_load", "rs_tables_blob",
     "rs_tables_crc", "rs_tables_info", "rs_tables_shanten_std", "rs_create", "rs_destroy",
-    "rs_num_envs", "rs_state_bytes", "rs_init", "rs_init_indexed", "rs_step", "rs_step_ex", "rs_observe",
+    "rs_num_envs", "rs_state_bytes", "rs_init", "rs_init_indexed", "rs_step", "rs_step_ex", "rs_step_rec_out",
+    "rs_observe",
     "rs_policy_random", "rs_policy_heuristic", "rs_rollout", "rs_rollout_policy", "rs_autoreset", "rs_check_invariants", "rs_export_env", "rs_import_env", "rs_record_sizes", "rs_debug_rollout_cycles",
 )
 
@@ -82,6 +83,7 @@ def lib():
         L.rs_init_indexed.argtypes = [vp, u64, i64, vp, vp]
         L.rs_step.argtypes = [vp, vp, vp, vp]
         L.rs_step_ex.argtypes = [vp, vp, i32, vp, vp, vp, vp]
+        L.rs_step_rec_out.argtypes = [vp, vp, i32, vp, vp, vp]
         L.rs_observe.argtypes = [vp, vp, vp, vp]
         L.rs_policy_random.argtypes = [vp, vp, vp]
         L.rs_rollout.argtypes = [vp, i32, vp, i32, vp, vp, vp, vp, vp]
@@ -106,11 +108,11 @@ def check(rc: int, what: str = "") -> None:
 
 
 def record_sizes() -> list[int]:
-    out = (C.c_int32 * 6)()
+    out = (C.c_int32 * 7)()
     check(lib().rs_record_sizes(out), "rs_record_sizes")
     return list(out)
 
 
 def ctypes_record_sizes() -> list[int]:
     return [C.sizeof(t) for t in (abi.rs_config, abi.rs_meld_rec, abi.rs_hand_rec,
-                                  abi.rs_win_rec, abi.rs_result_rec, abi.rs_env_rec)]
+                                  abi.rs_win_rec, abi.rs_result_rec, abi.rs_env_rec, abi.rs_step_rec)]

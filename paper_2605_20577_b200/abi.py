@@ -119,6 +119,19 @@ class rs_result_rec(C.Structure):
     ]
 
 
+class rs_step_rec(C.Structure):
+    """include/rinshan.h rs_step_rec (40 bytes)"""
+    _fields_ = [
+        ("rewards", C.c_float * 4),
+        ("legal_bits", C.c_uint32 * 4),
+        ("next_action", C.c_int32),
+        ("current_player", C.c_int8),
+        ("terminated", C.c_uint8),
+        ("truncated", C.c_uint8),
+        ("status", C.c_uint8),
+    ]
+
+
 class rs_env_rec(C.Structure):
     _fields_ = [
         ("abi_version", C.c_int32),

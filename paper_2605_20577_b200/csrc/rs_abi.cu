@@ -309,7 +309,7 @@ __device__ __forceinline__ int env_of_thread(int gtid, int epw) {
 
 __global__ void __launch_bounds__(ROLL_BLOCK, ROLL_MINB) k_step(const __grid_constant__ Soa S, const __grid_constant__ DevTables D,
     const __grid_constant__ Cfg C, const int32_t* actions, int flags, rs_obs_out obs, int32_t* next_actions,
-    StepOut out, int epw, int staged, int glog2, int check) {
+    StepOut out, int epw, int staged, int glog2, int check, rs_step_rec* recs) {
   tables_begin(D, glog2);  // the action and header loads overlap the table copy
   const Tabs T{};
   const int lane = threadIdx.x & 31;
@@ -345,9 +345,11 @@ __global__ void __launch_bounds__(ROLL_BLOCK, ROLL_MINB) k_step(const __grid_con
     dirty = true;
   }
   if (flags & RS_STEP_OBSERVE) write_obs(E, E.g.current_player, obs, e);
-  if (next_actions) {
+  int next = -1;
+  if (next_actions || recs) {
     const bool done = E.g.env_terminated || E.g.env_truncated;
-    next_actions[e] = done ? -1 : (flags & RS_STEP_HEURISTIC) ? E.heuristic_action(m) : E.random_action(m);
+    next = done ? -1 : (flags & RS_STEP_HEURISTIC) ? E.heuristic_action(m) : E.random_action(m);
+    if (next_actions) next_actions[e] = next;
     dirty |= !done;
   }
   int st_out = st;
@@ -365,6 +367,20 @@ __global__ void __launch_bounds__(ROLL_BLOCK, ROLL_MINB) k_step(const __grid_con
   if (out.terminated) out.terminated[e] = (uint8_t)term;
   if (out.truncated) out.truncated[e] = (uint8_t)trunc;
   if (out.status) out.status[e] = (uint8_t)st_out;
+  if (recs) {
+    // the record's 10 words from the lanes of the env's group (one store
+    // instruction per 10 lanes: the env's 40 bytes leave as one burst)
+    auto word = [&](int i) -> uint32_t {
+      union { float f; uint32_t u; } cv;
+      if (i < 4) { cv.f = r[i]; return cv.u; }
+      if (i < 8) return m.m[i - 4];
+      if (i == 8) return (uint32_t)next;
+      return (uint32_t)(uint8_t)E.g.current_player | ((uint32_t)(uint8_t)term << 8) | ((uint32_t)(uint8_t)trunc << 16) |
+             ((uint32_t)(uint8_t)st_out << 24);
+    };
+    uint32_t* dst = reinterpret_cast<uint32_t*>(recs + e);
+    for (int i = lane & ((1 << glog2) - 1); i < 10; i += 1 << glog2) dst[i] = word(i);
+  }
   if (staged && dirty && sub == 0) stage_wait_all();
 }
 
@@ -879,8 +895,22 @@ int rs_step_ex(rs_handle* h, const int32_t* actions_dev, int32_t flags, const rs
   if (obs) o = *obs;
   const Launch L = step_launch(h, false);
   CUDA_TRY(launch_tables(h, k_step, L.grid, L.block, L.smem, st, h->S, h->D, h->cfg, actions_dev, flags, o,
-                         next_actions_dev, step_out(h, out), L.epw, L.staged, L.glog2, h->check_steps));
+                         next_actions_dev, step_out(h, out), L.epw, L.staged, L.glog2, h->check_steps,
+                         (rs_step_rec*)nullptr));
   return finish_step_out(h, out, st);
+}
+
+int rs_step_rec_out(rs_handle* h, const int32_t* actions, int32_t flags, rs_step_rec* recs,
+                    const rs_obs_out* obs, void* stream) {
+  if (!h || !actions || !recs) return set_err(RS_E_ARG, "rs_step_rec_out: null argument");
+  if ((flags & RS_STEP_OBSERVE) && !obs) return set_err(RS_E_ARG, "RS_STEP_OBSERVE needs obs buffers");
+  cudaStream_t st = (cudaStream_t)stream;
+  rs_obs_out o{};
+  if (obs) o = *obs;
+  const Launch L = step_launch(h, false);
+  CUDA_TRY(launch_tables(h, k_step, L.grid, L.block, L.smem, st, h->S, h->D, h->cfg, actions, flags, o,
+                         (int32_t*)nullptr, StepOut{}, L.epw, L.staged, L.glog2, h->check_steps, recs));
+  return 0;
 }
 
 int rs_observe(rs_handle* h, const int8_t* seats_dev, const rs_obs_out* obs, void* stream) {
@@ -991,13 +1021,14 @@ int rs_import_env(rs_handle* h, int64_t env, const rs_env_rec* in) {
   return 0;
 }
 
-int rs_record_sizes(int32_t* out /*[6]*/) {
+int rs_record_sizes(int32_t* out /*[7]*/) {
   out[0] = (int32_t)sizeof(rs_config);
   out[1] = (int32_t)sizeof(rs_meld_rec);
   out[2] = (int32_t)sizeof(rs_hand_rec);
   out[3] = (int32_t)sizeof(rs_win_rec);
   out[4] = (int32_t)sizeof(rs_result_rec);
   out[5] = (int32_t)sizeof(rs_env_rec);
+  out[6] = (int32_t)sizeof(rs_step_rec);
   return 0;
 }
 

@@ -354,7 +354,11 @@ class HostStepper:
         self._act_dev = self.actions if mode != "none" else torch.zeros(n, dtype=torch.int32, device=dev)
         self._res_dev = self._res_host if mode == "both" else torch.zeros(n * self.BYTES_PER_ENV, dtype=torch.uint8,
                                                                           device=dev)
-        d, h = self._views(self._res_dev), self._views(self._res_host)
+        # "both": one rs_step_rec (40 B) per env, written as a burst per env;
+        # otherwise field-major arrays (rs_step_out)
+        self._packed = mode == "both" and policy  # (the record always carries the next action)
+        views = self._rec_views if self._packed else self._views
+        d, h = views(self._res_dev), views(self._res_host)
         self.rewards, self.legal_bits, self.next_actions = h["rewards"], h["legal_bits"], h["next_actions"]
         self.current_player, self.terminated = h["current_player"], h["terminated"]
         self.truncated, self.status = h["truncated"], h["status"]
@@ -378,6 +382,21 @@ class HostStepper:
             self._graph = g
             self._stream = s
 
+    def _rec_views(self, buf: torch.Tensor) -> dict:
+        """views of an rs_step_rec[n] buffer (include/rinshan.h)"""
+        n = self.n
+        w = buf.view(torch.int32).view(n, 10)
+        b = buf.view(n, 40)
+        return {
+            "rewards": buf.view(torch.float32).view(n, 10)[:, 0:4],
+            "legal_bits": w[:, 4:8],
+            "next_actions": w[:, 8],
+            "current_player": b[:, 36].view(torch.int8),
+            "terminated": b[:, 37],
+            "truncated": b[:, 38],
+            "status": b[:, 39],
+        }
+
     def _views(self, buf: torch.Tensor) -> dict:
         n = self.n
         return {
@@ -391,6 +410,16 @@ class HostStepper:
         }
 
     def _body(self):
+        if self._packed:
+            env = self.env
+            if env._obs is None:
+                env._obs = alloc_observations(env.n, env.device)
+            ost = obs_struct(env._obs) if self.observe else None
+            flags = (1 if self.autoreset else 0) | (2 if self.observe else 0)
+            check(env._L.rs_step_rec_out(env._h, self.actions.data_ptr(), flags, self._res_host.data_ptr(),
+                                         C.byref(ost) if ost is not None else None, env._stream()),
+                  "rs_step_rec_out")
+            return
         if self.zero_copy != "none":
             env = self.env
             if env._obs is None:
