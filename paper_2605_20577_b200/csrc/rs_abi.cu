@@ -714,6 +714,20 @@ cudaError_t launch_tables(const rs_handle* h, void (*kernel)(KArgs...), int grid
   return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
 }
 
+// launches go to the handle's device whatever the caller's current device
+// (restored afterwards: the entry points are stream-ordered calls the
+// caller may make from a thread working with another device)
+struct DeviceScope {
+  int prev = -1;
+  explicit DeviceScope(int device) {
+    if (cudaGetDevice(&prev) == cudaSuccess && prev != device) cudaSetDevice(device);
+    else prev = -1;
+  }
+  ~DeviceScope() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+
 StepOut step_out(rs_handle* h, const rs_step_out* o) {
   StepOut s{};
   if (!o) return s;
@@ -869,6 +883,7 @@ int rs_destroy(rs_handle* h) {
 
 int rs_init(rs_handle* h, const uint64_t* seeds_dev, const rs_step_out* out, void* stream) {
   if (!h || !seeds_dev) return set_err(RS_E_ARG, "rs_init: null argument");
+  const DeviceScope device_scope(h->device);
   cudaStream_t st = (cudaStream_t)stream;
   k_init<<<grid_of(h->n), BLOCK, smem_for(BLOCK), st>>>(h->S, h->D, h->cfg, seeds_dev, 0, 0, 0, step_out(h, out));
   return finish_step_out(h, out, st);
@@ -876,6 +891,7 @@ int rs_init(rs_handle* h, const uint64_t* seeds_dev, const rs_step_out* out, voi
 
 int rs_init_indexed(rs_handle* h, uint64_t seed, int64_t index_base, const rs_step_out* out, void* stream) {
   if (!h) return set_err(RS_E_ARG, "rs_init_indexed: null handle");
+  const DeviceScope device_scope(h->device);
   cudaStream_t st = (cudaStream_t)stream;
   k_init<<<grid_of(h->n), BLOCK, smem_for(BLOCK), st>>>(h->S, h->D, h->cfg, nullptr, seed, index_base, 1,
                                                   step_out(h, out));
@@ -890,6 +906,7 @@ int rs_step_ex(rs_handle* h, const int32_t* actions_dev, int32_t flags, const rs
                const rs_obs_out* obs, int32_t* next_actions_dev, void* stream) {
   if (!h || !actions_dev) return set_err(RS_E_ARG, "rs_step: null argument");
   if ((flags & RS_STEP_OBSERVE) && !obs) return set_err(RS_E_ARG, "RS_STEP_OBSERVE needs obs buffers");
+  const DeviceScope device_scope(h->device);
   cudaStream_t st = (cudaStream_t)stream;
   rs_obs_out o{};
   if (obs) o = *obs;
@@ -904,6 +921,7 @@ int rs_step_rec_out(rs_handle* h, const int32_t* actions, int32_t flags, rs_step
                     const rs_obs_out* obs, void* stream) {
   if (!h || !actions || !recs) return set_err(RS_E_ARG, "rs_step_rec_out: null argument");
   if ((flags & RS_STEP_OBSERVE) && !obs) return set_err(RS_E_ARG, "RS_STEP_OBSERVE needs obs buffers");
+  const DeviceScope device_scope(h->device);
   cudaStream_t st = (cudaStream_t)stream;
   rs_obs_out o{};
   if (obs) o = *obs;
@@ -915,6 +933,7 @@ int rs_step_rec_out(rs_handle* h, const int32_t* actions, int32_t flags, rs_step
 
 int rs_observe(rs_handle* h, const int8_t* seats_dev, const rs_obs_out* obs, void* stream) {
   if (!h || !obs) return set_err(RS_E_ARG, "rs_observe: null argument");
+  const DeviceScope device_scope(h->device);
   cudaStream_t st = (cudaStream_t)stream;
   k_observe<<<grid_of(h->n), BLOCK, smem_for(BLOCK), st>>>(h->S, h->D, h->cfg, seats_dev, *obs);
   CUDA_TRY(cudaGetLastError());
@@ -923,6 +942,7 @@ int rs_observe(rs_handle* h, const int8_t* seats_dev, const rs_obs_out* obs, voi
 
 int rs_policy_random(rs_handle* h, int32_t* actions_dev, void* stream) {
   if (!h || !actions_dev) return set_err(RS_E_ARG, "rs_policy_random: null argument");
+  const DeviceScope device_scope(h->device);
   cudaStream_t st = (cudaStream_t)stream;
   k_policy<<<grid_of(h->n), BLOCK, smem_for(BLOCK), st>>>(h->S, h->D, h->cfg, actions_dev, RS_POLICY_RANDOM);
   CUDA_TRY(cudaGetLastError());
@@ -931,6 +951,7 @@ int rs_policy_random(rs_handle* h, int32_t* actions_dev, void* stream) {
 
 int rs_policy_heuristic(rs_handle* h, int32_t* actions_dev, void* stream) {
   if (!h || !actions_dev) return set_err(RS_E_ARG, "rs_policy_heuristic: null argument");
+  const DeviceScope device_scope(h->device);
   cudaStream_t st = (cudaStream_t)stream;
   k_policy<<<grid_of(h->n), BLOCK, smem_for(BLOCK), st>>>(h->S, h->D, h->cfg, actions_dev, RS_POLICY_HEURISTIC);
   CUDA_TRY(cudaGetLastError());
@@ -951,6 +972,7 @@ int rs_rollout_policy(rs_handle* h, int32_t steps, int32_t policy, const rs_obs_
   if (policy != RS_POLICY_RANDOM && policy != RS_POLICY_HEURISTIC) return set_err(RS_E_ARG, "rs_rollout: unknown policy");
   if (obs_slots < 0 || (obs_slots > 1 && obs_slots != steps)) return set_err(RS_E_ARG, "obs_slots must be 0, 1 or steps");
   if (obs_slots > 0 && !obs) return set_err(RS_E_ARG, "obs_slots > 0 needs obs buffers");
+  const DeviceScope device_scope(h->device);
   cudaStream_t st = (cudaStream_t)stream;
   rs_obs_out o{};
   if (obs) o = *obs;
@@ -969,6 +991,7 @@ int rs_rollout_policy(rs_handle* h, int32_t steps, int32_t policy, const rs_obs_
 // and flags, into prof_dev[steps][n][4] (u32)
 int rs_debug_rollout_cycles(rs_handle* h, int32_t steps, const rs_obs_out* obs, uint32_t* prof_dev, void* stream) {
   if (!h || !prof_dev || steps < 1) return set_err(RS_E_ARG, "rs_debug_rollout_cycles: bad arguments");
+  const DeviceScope device_scope(h->device);
   cudaStream_t st = (cudaStream_t)stream;
   rs_obs_out o{};
   if (obs) o = *obs;
@@ -988,6 +1011,7 @@ extern "C" int rs_debug_set_marks(void* marks) {
 
 int rs_check_invariants(rs_handle* h, int32_t fast, uint32_t* flags_dev, void* stream) {
   if (!h || !flags_dev) return set_err(RS_E_ARG, "rs_check_invariants: null argument");
+  const DeviceScope device_scope(h->device);
   cudaStream_t st = (cudaStream_t)stream;
   k_check<<<grid_of(h->n), BLOCK, smem_for(BLOCK), st>>>(h->S, h->D, h->cfg, fast, flags_dev);
   CUDA_TRY(cudaGetLastError());
@@ -996,6 +1020,7 @@ int rs_check_invariants(rs_handle* h, int32_t fast, uint32_t* flags_dev, void* s
 
 int rs_autoreset(rs_handle* h, const rs_step_out* out, void* stream) {
   if (!h) return set_err(RS_E_ARG, "rs_autoreset: null handle");
+  const DeviceScope device_scope(h->device);
   cudaStream_t st = (cudaStream_t)stream;
   k_autoreset<<<grid_of(h->n), BLOCK, smem_for(BLOCK), st>>>(h->S, h->D, h->cfg, step_out(h, out));
   return finish_step_out(h, out, st);
