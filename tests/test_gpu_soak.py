@@ -39,3 +39,24 @@ def test_bit_exact_on_1e5_hands(rule):
     assert games >= 100_000, f"only {games} hands played"
     bad = [i for i in range(n) if got[i] != ref[i]]
     assert not bad, f"{len(bad)} of {n} envs diverge, first {bad[:8]}"
+
+
+@pytest.mark.parametrize("n", (4096, 8192, 16384, 65536))
+def test_lane_group_sizes_match_oracle(n):
+    """every lane-group size the launch heuristic picks (16, 8, 4, 1 lanes
+    per env at these batch sizes) gives the oracle's trajectories; 4096 is
+    the bench configuration"""
+    steps, seed, chunk = 250, 77, 1024
+    rule = "red" if n % 8192 else "no-red"
+    env = BatchEnv(n, EnvConfig(rule=rule)).init(seed=seed, index_base=0)
+    digests = torch.zeros(n, dtype=torch.int64, device="cuda")
+    env.rollout(steps, digests=digests)
+    torch.cuda.synchronize()
+    got = [int(x) & ((1 << 64) - 1) for x in digests.cpu().tolist()]
+    env.close()
+    cfg = O.make_config(rule=rule)
+    with ThreadPoolExecutor(max_workers=os.cpu_count() or 4) as ex:
+        parts = list(ex.map(lambda b: O.run_shard(cfg, seed, b, chunk, steps, digests=True), range(0, n, chunk)))
+    ref = [d for _, ds in parts for d in ds]
+    bad = [i for i in range(n) if got[i] != ref[i]]
+    assert not bad, f"{len(bad)} of {n} envs diverge, first {bad[:8]}"
