@@ -20,6 +20,8 @@
 #include <mutex>
 #include <string>
 
+#include <cub/device/device_radix_sort.cuh>
+
 #include "rs_check.cuh"
 #include "rs_io.cuh"
 
@@ -268,6 +270,20 @@ __device__ __forceinline__ void write_step_out(const StepOut& o, int64_t e, cons
   if (o.status) o.status[e] = (uint8_t)status;
 }
 
+// the kind of an env's next step, for grouping envs with the same branch
+// structure into the same warps (large batches): 0 auto-reset, 1 call
+// phase, 2 turn with a drawn tile, 3 other turn (after a call)
+__device__ __forceinline__ uint8_t next_kind(const Engine& E) {
+  if (E.g.env_terminated || E.g.env_truncated) return 0;
+  if (E.g.phase == PH_CALL) return 1;
+  return E.g.drawn >= 0 ? 2 : 3;
+}
+
+__global__ void k_iota(int32_t* a, int n) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) a[i] = i;
+}
+
 __global__ void __launch_bounds__(BLOCK) k_init(const __grid_constant__ Soa S, const __grid_constant__ DevTables D,
     const __grid_constant__ Cfg C, const uint64_t* seeds, uint64_t seed,
                                                 int64_t base, int indexed, StepOut out) {
@@ -309,13 +325,15 @@ __device__ __forceinline__ int env_of_thread(int gtid, int epw) {
 
 __global__ void __launch_bounds__(ROLL_BLOCK, ROLL_MINB) k_step(const __grid_constant__ Soa S, const __grid_constant__ DevTables D,
     const __grid_constant__ Cfg C, const int32_t* actions, int flags, rs_obs_out obs, int32_t* next_actions,
-    StepOut out, int epw, int staged, int glog2, int check, rs_step_rec* recs) {
+    StepOut out, int epw, int staged, int glog2, int check, rs_step_rec* recs, const int32_t* order,
+    uint8_t* kind_out) {
   tables_begin(D, glog2);  // the action and header loads overlap the table copy
   const Tabs T{};
   const int lane = threadIdx.x & 31;
   if ((lane >> glog2) >= epw) return;
-  const int e = ((blockIdx.x * blockDim.x + threadIdx.x) >> 5) * epw + (lane >> glog2);
-  if (e >= S.n) return;
+  const int q = ((blockIdx.x * blockDim.x + threadIdx.x) >> 5) * epw + (lane >> glog2);
+  if (q >= S.n) return;
+  const int e = order ? order[q] : q;  // envs grouped by the kind of their step (large batches)
   // one stage slot per env, shared by the env's lane group
   const uint32_t sb = slot_off((threadIdx.x >> 5) * epw + (lane >> glog2));
   const int sub = lane & ((1 << glog2) - 1);
@@ -361,6 +379,7 @@ __global__ void __launch_bounds__(ROLL_BLOCK, ROLL_MINB) k_step(const __grid_con
       if (sub == 0) stage_out(S, e, sb);
     }
   }
+  if (kind_out && (lane & ((1 << glog2) - 1)) == 0) kind_out[e] = next_kind(E);
   if (out.legal_bits) reinterpret_cast<uint4*>(out.legal_bits)[e] = make_uint4(m.m[0], m.m[1], m.m[2], m.m[3]);
   if (out.current_player) out.current_player[e] = (int8_t)E.g.current_player;
   if (out.rewards) reinterpret_cast<float4*>(out.rewards)[e] = make_float4(r[0], r[1], r[2], r[3]);
@@ -419,7 +438,7 @@ __global__ void __launch_bounds__(ROLL_BLOCK, ROLL_MINB) k_rollout(const __grid_
                                                    StepOut traj, rs_rollout_stats* stats,
                                                    uint64_t* digests, StepOut out, int epw,
                                                    uint32_t* prof, int staged, int policy, int glog2,
-                                                   int check) {
+                                                   int check, const int32_t* order, uint8_t* kind_out) {
   const uint32_t g_entry = prof ? globaltimer_lo() : 0u;
   tables_begin(D, glog2);  // the first env tile's header loads overlap the copy
   const Tabs T{};
@@ -435,8 +454,9 @@ __global__ void __launch_bounds__(ROLL_BLOCK, ROLL_MINB) k_rollout(const __grid_
   if (staged && (lane >> glog2) < epw && sub == 0) slot_bar_init(sb);
   uint32_t phase = 0;
   for (int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; w * epw < S.n; w += warps) {
-    const int e = w * epw + (lane >> glog2);
-    if ((lane >> glog2) >= epw || e >= S.n) continue;
+    const int q = w * epw + (lane >> glog2);
+    if ((lane >> glog2) >= epw || q >= S.n) continue;
+    const int e = order ? order[q] : q;  // envs grouped by the kind of their step (large batches)
     if (staged) {
       if (sub == 0) {
         stage_wait_read();  // the slot's previous block has left
@@ -498,6 +518,7 @@ __global__ void __launch_bounds__(ROLL_BLOCK, ROLL_MINB) k_rollout(const __grid_
       __syncwarp(gm);  // every lane's writes to the slot precede the bulk store
       if (sub == 0) stage_out(S, e, sb);
     }
+    if (kind_out && sub == 0) kind_out[e] = next_kind(E);
     if (digests) digests[e] = d;
     write_step_out(out, e, E, m, r, st | (inv ? (int)RS_STATUS_INVARIANT : 0));
     RS_SMARK(7);
@@ -598,6 +619,16 @@ struct rs_handle {
   int groups;  // idle lanes of small-batch warps join their env (RINSHAN_GROUPS=0: off)
   int check_steps;  // RINSHAN_CHECK=1: fast invariants after every step -> RS_STATUS_INVARIANT
   int block_override;  // RINSHAN_BLOCK (tuning experiments): stepping-kernel CTA size
+  // env ordering (large batches): each stepping launch records the kind of
+  // every env's next step; the next launch first sorts the envs by kind
+  // (CUB radix sort, 2 key bits) so a warp's envs share a branch structure
+  int ordering;            // RINSHAN_ORDER: 0 off, 1 at >= 262144 envs (default), 2 always
+  uint8_t* kind;           // [n] next-step kind per env (k_rollout / k_step write it)
+  uint8_t* kind_sorted;    // [n] sort scratch
+  int32_t* iota;           // [n] 0..n-1
+  int32_t* order;          // [n] env processed by slot q
+  void* sort_tmp;
+  size_t sort_tmp_bytes;
   int epw_override;         // RINSHAN_EPW (tuning experiments), 0 = heuristic
   bool persist;             // launch with the tables' L2 persisting window
   cudaAccessPolicyWindow window;
@@ -635,7 +666,7 @@ int warp_grid(const rs_handle* h, int epw, int block, int max_ctas) {
 // (spread over every SM), else ROLL_BLOCK-thread CTAs; one stage slot per
 // env of the CTA.  `ctas` = resident CTAs per SM (occupancy, cached).
 struct Launch {
-  int grid, block, smem, epw, ctas, staged, glog2;
+  int grid, block, smem, epw, ctas, staged, glog2, ordered;
 };
 int resident_ctas(rs_handle* h, int block, int smem) {
   const int key = block * 1048576 + smem;
@@ -666,6 +697,10 @@ Launch launch_at(rs_handle* h, int epw) {
   L.glog2 = 0;
   if (h->groups)
     while ((epw << (L.glog2 + 1)) <= 32) L.glog2++;
+  // measured on B200 (fresh games / steady state after 150 steps): 1 M envs
+  // +4 % / +75 %, 262 K -1.5 % / +50 %, 131 K -11 % / +25 %, below 64 K a
+  // loss either way (the sort's launches cost more than the divergence saved)
+  L.ordered = h->ordering == 2 || (h->ordering == 1 && h->n >= (1 << 18));
   L.smem = L.staged ? smem_staged(L.block, L.block / 32 * epw) : smem_for(L.block);
   L.ctas = resident_ctas(h, L.block, L.smem);
   L.grid = warp_grid(h, epw, L.block, 0);
@@ -693,6 +728,14 @@ Launch step_launch(rs_handle* h, bool persistent) {
   Launch L = launch_at(h, envs_per_warp(h));
   if (persistent) L.grid = std::min(L.grid, h->num_sms * L.ctas);
   return L;
+}
+
+// the envs of the coming launch, sorted by the kind of their next step
+int order_envs(rs_handle* h, cudaStream_t st) {
+  size_t bytes = h->sort_tmp_bytes;
+  CUDA_TRY(cub::DeviceRadixSort::SortPairs(h->sort_tmp, bytes, h->kind, h->kind_sorted, h->iota, h->order, h->n, 0,
+                                           2, st));
+  return 0;
 }
 
 // launch with the table block's L2 access policy window (DeviceTables)
@@ -830,6 +873,8 @@ int rs_create(rs_handle** out, int64_t n_envs, const rs_config* cfg, int32_t dev
       {(void**)&S.evobs, (size_t)EVOBS_BYTES * n},
       {(void**)&S.results, sizeof(rs_result_rec) * n},
       {(void**)&h->legal_bits_tmp, 16 * n},  {(void**)&h->rec_dev, sizeof(rs_env_rec)},
+      {(void**)&h->kind, n},                 {(void**)&h->kind_sorted, n},
+      {(void**)&h->iota, 4 * n},             {(void**)&h->order, 4 * n},
   };
   size_t total = 0;
   for (auto& p : parts) total += (p.bytes + 255) & ~(size_t)255;
@@ -850,6 +895,15 @@ int rs_create(rs_handle** out, int64_t n_envs, const rs_config* cfg, int32_t dev
     return set_err((int)e2, "%s: %s", what, cudaGetErrorString(e2));
   };
   if ((err = cudaMemset(h->mem, 0, total))) return cleanup(err, "state clear");
+  if ((err = cudaMemset(h->kind, 2, n))) return cleanup(err, "kind init");
+  k_iota<<<(unsigned)((n + 255) / 256), 256>>>(h->iota, (int)n);
+  if ((err = cudaGetLastError())) return cleanup(err, "iota");
+  h->sort_tmp = nullptr;
+  h->sort_tmp_bytes = 0;
+  if ((err = cub::DeviceRadixSort::SortPairs(nullptr, h->sort_tmp_bytes, h->kind, h->kind_sorted, h->iota, h->order,
+                                             (int)n, 0, 2)))
+    return cleanup(err, "sort size query");
+  if ((err = cudaMalloc(&h->sort_tmp, std::max<size_t>(h->sort_tmp_bytes, 16)))) return cleanup(err, "sort scratch");
   const void* kernels[] = {(const void*)k_init, (const void*)k_step, (const void*)k_policy,
                            (const void*)k_observe, (const void*)k_rollout, (const void*)k_export,
                            (const void*)k_import, (const void*)k_autoreset, (const void*)k_check};
@@ -865,6 +919,8 @@ int rs_create(rs_handle** out, int64_t n_envs, const rs_config* cfg, int32_t dev
   h->groups = groups_env ? (atoi(groups_env) != 0) : 1;
   const char* check_env = getenv("RINSHAN_CHECK");
   h->check_steps = check_env ? (atoi(check_env) != 0) : 0;
+  const char* order_env = getenv("RINSHAN_ORDER");
+  h->ordering = order_env ? std::max(0, std::min(2, atoi(order_env))) : 1;
   const char* block_env = getenv("RINSHAN_BLOCK");
   h->block_override = block_env ? std::max(0, std::min(ROLL_BLOCK, atoi(block_env) & ~31)) : 0;
   const char* epw_env = getenv("RINSHAN_EPW");
@@ -877,6 +933,7 @@ int rs_destroy(rs_handle* h) {
   if (!h) return 0;
   cudaSetDevice(h->device);
   cudaFree(h->mem);
+  cudaFree(h->sort_tmp);
   delete h;
   return 0;
 }
@@ -911,9 +968,14 @@ int rs_step_ex(rs_handle* h, const int32_t* actions_dev, int32_t flags, const rs
   rs_obs_out o{};
   if (obs) o = *obs;
   const Launch L = step_launch(h, false);
+  if (L.ordered) {
+    const int rc = order_envs(h, st);
+    if (rc) return rc;
+  }
   CUDA_TRY(launch_tables(h, k_step, L.grid, L.block, L.smem, st, h->S, h->D, h->cfg, actions_dev, flags, o,
                          next_actions_dev, step_out(h, out), L.epw, L.staged, L.glog2, h->check_steps,
-                         (rs_step_rec*)nullptr));
+                         (rs_step_rec*)nullptr, L.ordered ? (const int32_t*)h->order : nullptr,
+                         L.ordered ? h->kind : nullptr));
   return finish_step_out(h, out, st);
 }
 
@@ -926,8 +988,13 @@ int rs_step_rec_out(rs_handle* h, const int32_t* actions, int32_t flags, rs_step
   rs_obs_out o{};
   if (obs) o = *obs;
   const Launch L = step_launch(h, false);
+  if (L.ordered) {
+    const int rc = order_envs(h, st);
+    if (rc) return rc;
+  }
   CUDA_TRY(launch_tables(h, k_step, L.grid, L.block, L.smem, st, h->S, h->D, h->cfg, actions, flags, o,
-                         (int32_t*)nullptr, StepOut{}, L.epw, L.staged, L.glog2, h->check_steps, recs));
+                         (int32_t*)nullptr, StepOut{}, L.epw, L.staged, L.glog2, h->check_steps, recs,
+                         L.ordered ? (const int32_t*)h->order : nullptr, L.ordered ? h->kind : nullptr));
   return 0;
 }
 
@@ -979,10 +1046,14 @@ int rs_rollout_policy(rs_handle* h, int32_t steps, int32_t policy, const rs_obs_
   // persistent grid of the resident CTA count (tables staged once per CTA,
   // envs walked grid-stride)
   const Launch L = step_launch(h, true);
+  if (L.ordered) {
+    const int rc = order_envs(h, st);
+    if (rc) return rc;
+  }
   CUDA_TRY(launch_tables(h, k_rollout, L.grid, L.block, L.smem, st, h->S, h->D, h->cfg, steps, o,
                          obs ? obs_slots : 0, actions_log, actors_log, step_out(h, traj), stats_dev, digests_dev,
-                         step_out(h, out),
-                         L.epw, nullptr, L.staged, policy, L.glog2, h->check_steps));
+                         step_out(h, out), L.epw, nullptr, L.staged, policy, L.glog2, h->check_steps,
+                         L.ordered ? (const int32_t*)h->order : nullptr, L.ordered ? h->kind : nullptr));
   return finish_step_out(h, out, st);
 }
 
@@ -998,7 +1069,7 @@ int rs_debug_rollout_cycles(rs_handle* h, int32_t steps, const rs_obs_out* obs, 
   const Launch L = step_launch(h, true);
   CUDA_TRY(launch_tables(h, k_rollout, L.grid, L.block, L.smem, st, h->S, h->D, h->cfg, steps, o, obs ? 1 : 0,
                          nullptr, nullptr, StepOut{}, nullptr, nullptr, StepOut{}, L.epw, prof_dev, L.staged,
-                         (int)RS_POLICY_RANDOM, L.glog2, 0));
+                         (int)RS_POLICY_RANDOM, L.glog2, 0, (const int32_t*)nullptr, (uint8_t*)nullptr));
   CUDA_TRY(cudaGetLastError());
   return 0;
 }

@@ -60,3 +60,28 @@ def test_lane_group_sizes_match_oracle(n):
     ref = [d for _, ds in parts for d in ds]
     bad = [i for i in range(n) if got[i] != ref[i]]
     assert not bad, f"{len(bad)} of {n} envs diverge, first {bad[:8]}"
+
+
+@pytest.mark.parametrize("n,force", ((2048, True), (262144, False)))
+def test_env_ordering_matches_oracle(n, force, monkeypatch):
+    """envs processed in next-step-kind order (CUB sort between launches,
+    default at >= 262144 envs; forced below) keep every trajectory, one-step
+    launches and fused launches alike"""
+    if force:
+        monkeypatch.setenv("RINSHAN_ORDER", "2")
+    steps, seed, chunk = 120, 91, 1024
+    env = BatchEnv(n, EnvConfig(rule="red")).init(seed=seed, index_base=0)
+    digests = torch.zeros(n, dtype=torch.int64, device="cuda")
+    for _ in range(steps // 2):
+        env.rollout(1, digests=digests)
+    env.rollout(steps - steps // 2, digests=digests)
+    torch.cuda.synchronize()
+    got = [int(x) & ((1 << 64) - 1) for x in digests.cpu().tolist()]
+    env.close()
+    cfg = O.make_config(rule="red")
+    with ThreadPoolExecutor(max_workers=os.cpu_count() or 4) as ex:
+        parts = list(ex.map(lambda b: O.run_shard(cfg, seed, b, min(chunk, n - b), steps, digests=True),
+                            range(0, n, chunk)))
+    ref = [d for _, ds in parts for d in ds]
+    bad = [i for i in range(n) if got[i] != ref[i]]
+    assert not bad, f"{len(bad)} of {n} envs diverge, first {bad[:8]}"
