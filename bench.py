@@ -50,6 +50,8 @@ def parse():
     p.add_argument("--sweep", type=str, default="",
                    help="comma list of envs/GPU: one extra JSON line each (BASELINE configs[2])")
     p.add_argument("--fuse", type=int, default=1, help="env steps per k_rollout launch in --sweep")
+    p.add_argument("--sweep-warm", type=int, default=0,
+                   help="untimed env steps before a --sweep timing (0: fresh games, the reference's protocol)")
     return p.parse_args()
 
 
@@ -81,6 +83,8 @@ def sweep(args):
             if rc:
                 raise RuntimeError(env._L.rs_last_error().decode())
 
+        if args.sweep_warm:
+            env.rollout(args.sweep_warm, obs=obs, obs_slots=1)
         for _ in range(3):
             flush.fill_(1)
             launch()
@@ -97,7 +101,8 @@ def sweep(args):
         sps = n * k * reps / (ms / 1000)
         S = state_bytes_per_env(env)
         gbs = (2 * S + 272) * n * k / (ms / reps / 1000) / 1e9
-        print(json.dumps({"sweep": True, "rule": args.rule, "envs": n, "fuse": k, "launches": reps,
+        print(json.dumps({"sweep": True, "rule": args.rule, "envs": n, "fuse": k, "warm_steps": args.sweep_warm,
+                          "launches": reps,
                           "ms_per_launch": ms / reps, "env_steps_per_s": sps, "hbm_gbs_algorithmic": gbs}),
               flush=True)
         env.close()
