@@ -199,14 +199,15 @@ def test_step_tensors_match_records():
         assert bool(env.terminated[i]) == bool(r.env_terminated)
 
 
-@pytest.mark.parametrize("zero_copy", (True, False))
+@pytest.mark.parametrize("zero_copy,order", ((True, "1"), (False, "1"), (True, "2")))
 @pytest.mark.parametrize("rule", RULES)
-def test_host_stepper_equals_fused_rollout(rule, zero_copy):
+def test_host_stepper_equals_fused_rollout(rule, zero_copy, order, monkeypatch):
     """HostStepper (CUDA graph: actions in, fused step+autoreset+observe+
     policy, result block out -- through mapped pinned memory or explicit
     copies) follows the same trajectories as k_rollout."""
     from paper_2605_20577_b200.env import HostStepper
 
+    monkeypatch.setenv("RINSHAN_ORDER", order)  # "2": the env sort runs inside the captured graph
     n, steps = 300, 150
     cfg = EnvConfig(rule=rule)
     a = BatchEnv(n, cfg).init(seed=9)
