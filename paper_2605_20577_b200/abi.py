@@ -25,6 +25,10 @@ REWARD_RANK = 1
 
 STATUS_ILLEGAL = 1
 STATUS_CONTRACT = 2
+# river flags (include/rinshan.h RS_RIVER_*)
+RIVER_TSUMOGIRI = 1
+RIVER_RIICHI = 2
+RIVER_CALLED = 4
 STATUS_INVARIANT = 4
 # rs_check_invariants bits (include/rinshan.h RS_INV_*)
 INV_SCORE_SUM = 1

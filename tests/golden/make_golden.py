@@ -17,6 +17,7 @@ Writes small, deterministic JSON(.gz) files next to this script:
                     (engine/state.py:276-278) and observation digest
   logs.json.gz      mjlog-lite-v1 logs (engine/log.py) of the bench loop's
                     games, canonical JSON
+  renders.json.gz   render/svg.py documents (sha256) of reference states
 """
 
 from __future__ import annotations
@@ -418,6 +419,41 @@ def make_logs():
     dump("logs.json.gz", out)
 
 
+def make_renders():
+    """render/svg.py to_svg of reference states: a few steps of random and
+    heuristic games (mid-game and the final state with its result panel),
+    every viewer (None / seat) and both locales -> sha256 of the document"""
+    from mjsim.render.svg import to_svg
+
+    out = []
+    for rule, mode, seed, idx, policy in (("red", "single", 1, 0, "random"), ("no-red", "single", 2, 3, "heuristic"),
+                                         ("red", "east", 3, 1, "heuristic"), ("red", "single", 4, 5, "heuristic")):
+        cfg = EnvConfig(rule=rule, mode=mode)
+        st = init(env_game_seed(seed, idx), cfg)
+        pol = env_policy_state(seed, idx)
+        t = 0
+        picks = {7, 40, 90}
+        while True:
+            game = st.game
+            if t in picks or st.terminated or st.truncated:
+                for viewer in (None, 0, 2):
+                    for locale in ("en", "ja"):
+                        svg = to_svg(game, viewer=viewer, locale=locale)
+                        out.append({"rule": rule, "mode": mode, "seed": seed, "index": idx, "policy": policy,
+                                    "step": t, "viewer": viewer, "locale": locale,
+                                    "sha256": hashlib.sha256(svg.encode()).hexdigest(), "len": len(svg)})
+            if st.terminated or st.truncated:
+                break
+            if policy == "random":
+                a, pol = random_policy(st.legal, pol)
+            else:
+                a = heuristic_policy(observe(st, st.current_player), st.legal)
+            st = step(st, a)
+            t += 1
+    print(f"renders: {len(out)}")
+    dump("renders.json.gz", out)
+
+
 if __name__ == "__main__":
     if len(sys.argv) > 1:
         for name in sys.argv[1:]:
@@ -430,3 +466,4 @@ if __name__ == "__main__":
     make_traces()
     make_scenarios()
     make_logs()
+    make_renders()

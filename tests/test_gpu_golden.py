@@ -75,3 +75,29 @@ def test_contract_and_illegal_semantics():
     # the earlier state value is still usable (immutable semantics)
     ok = pgx.step(st, st.legal[0])
     assert not ok.terminated
+
+
+def test_device_states_render_like_the_reference():
+    """render.to_svg of pgx (device) states == the reference renderer's
+    documents for the same games and steps (tests/golden/renders.json.gz)"""
+    from paper_2605_20577_b200 import render
+
+    renders = json.loads(gzip.open(GOLD / "renders.json.gz").read())
+    games = {}
+    for g in renders:
+        games.setdefault((g["rule"], g["mode"], g["seed"], g["index"], g["policy"]), []).append(g)
+    for (rule, mode, seed, idx, policy), entries in games.items():
+        cfg = EnvConfig(rule=rule, mode=mode)
+        st = pgx.init(pgx.env_game_seed(seed, idx), cfg)
+        pol = pgx.env_policy_state(seed, idx)
+        t = 0
+        for g in sorted(entries, key=lambda x: x["step"]):
+            while t < g["step"]:
+                if policy == "random":
+                    a, pol = pgx.random_policy(st.legal, pol)
+                else:
+                    a = pgx.heuristic_policy(st)
+                st = pgx.step(st, a)
+                t += 1
+            svg = render.to_svg(st, viewer=g["viewer"], locale=g["locale"])
+            assert hashlib.sha256(svg.encode()).hexdigest() == g["sha256"], (rule, policy, g["step"], g["viewer"])

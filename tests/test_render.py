@@ -1,0 +1,57 @@
+"""SVG rendering of device / oracle states (paper_2605_20577_b200.render)
+against the reference renderer's documents (render/svg.py), byte for byte
+(sha256 of reference renders in tests/golden/renders.json.gz)."""
+
+from __future__ import annotations
+
+import gzip
+import hashlib
+import json
+from pathlib import Path
+
+import pytest
+
+from oracle import mjoracle as O
+from paper_2605_20577_b200 import records, render
+
+GOLD = Path(__file__).resolve().parent / "golden"
+
+
+def _renders():
+    return json.loads(gzip.open(GOLD / "renders.json.gz").read())
+
+
+def _states():
+    """(entry, record, last result) of every golden render, replayed on the oracle"""
+    games = {}
+    for g in _renders():
+        games.setdefault((g["rule"], g["mode"], g["seed"], g["index"], g["policy"]), []).append(g)
+    for (rule, mode, seed, idx, policy), entries in games.items():
+        env = O.OracleEnv(O.make_config(rule=rule, mode=mode)).init(O.env_game_seed(seed, idx))
+        kc = [O.env_policy_key(seed, idx), 0]
+        t = 0
+        for g in sorted(entries, key=lambda x: x["step"]):
+            while t < g["step"]:
+                a = env.random_policy(kc) if policy == "random" else env.heuristic_policy()
+                env.step(a)
+                t += 1
+            rec = env.record()
+            last = records.result_dict(rec.last_result) if rec.n_results else None
+            yield g, rec, last
+
+
+def test_render_matches_reference_documents():
+    n = 0
+    for g, rec, last in _states():
+        svg = render.to_svg(rec, viewer=g["viewer"], locale=g["locale"], last_result=last)
+        where = f"{g['rule']} {g['policy']} step {g['step']} viewer {g['viewer']} {g['locale']}"
+        assert len(svg) == g["len"], where
+        assert hashlib.sha256(svg.encode()).hexdigest() == g["sha256"], where
+        n += 1
+    assert n == len(_renders())
+
+
+def test_render_rejects_unknown_locale():
+    g, rec, last = next(_states())
+    with pytest.raises(ValueError):
+        render.to_svg(rec, locale="fr")
