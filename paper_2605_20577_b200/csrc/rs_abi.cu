@@ -121,6 +121,8 @@ int device_tables(int device, DevTables* out) {
     const uint8_t* hp = honor;
     CUDA_TRY(cudaMemcpyToSymbol(c_suit_cls, &sp, sizeof(sp)));
     CUDA_TRY(cudaMemcpyToSymbol(c_honor_cls, &hp, sizeof(hp)));
+    const uint8_t* tb = base;
+    CUDA_TRY(cudaMemcpyToSymbol(c_tblock, &tb, sizeof(tb)));
     dt.D.suit_cls = suit;
     dt.D.honor_cls = honor;
     dt.D.t3 = reinterpret_cast<const uint32_t*>(base);
@@ -169,6 +171,9 @@ struct StepOut {
 // warps spend no instructions on the copy and wait on the barrier phase.
 __shared__ __align__(8) uint64_t s_tables_bar;
 __device__ __forceinline__ void tables_wait() {
+#if defined(RS_TABLES_GLOBAL)
+  return;
+#endif
   const uint32_t bar_addr = (uint32_t)__cvta_generic_to_shared(&s_tables_bar);
   asm volatile(
       "{\n"
@@ -182,6 +187,11 @@ __device__ __forceinline__ void tables_wait() {
 // issue the copy; the caller waits (tables_wait) before the first table read
 __device__ __forceinline__ void tables_begin(const DevTables& D, int grp_log2) {
   const uint32_t bar_addr = (uint32_t)__cvta_generic_to_shared(&s_tables_bar);
+#if defined(RS_TABLES_GLOBAL)
+  if (threadIdx.x == 0) s_grp_log2 = grp_log2;
+  __syncthreads();
+  return;
+#endif
   if (threadIdx.x == 0) {
     s_grp_log2 = grp_log2;  // lanes per env (rs_common.cuh), published by the barrier below
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar_addr) : "memory");

@@ -167,6 +167,14 @@ RS_HD void deal_tile(Hand& h, int t) {
 // t3 | t1 | t2 block at the start of dynamic shared memory
 __constant__ const uint8_t* c_suit_cls;
 __constant__ const uint8_t* c_honor_cls;
+__constant__ const uint8_t* c_tblock;  // the t3 | t1 | t2 | pow block in global memory
+#endif
+// -DRS_TABLES_GLOBAL (experiment): read the factored tables through the
+// read-only cache instead of staging them into shared memory
+#if defined(RS_TABLES_GLOBAL) && defined(__CUDA_ARCH__)
+#define RS_TBL(off) (c_tblock + (off))
+#elif defined(__CUDA_ARCH__)
+#define RS_TBL(off) (g_smem + (off))
 #endif
 
 RS_HD uint32_t class_of(const Tabs& T, int suit, uint32_t code) {
@@ -178,21 +186,21 @@ RS_HD uint32_t class_of(const Tabs& T, int suit, uint32_t code) {
 }
 RS_HD int t1_at(const Tabs& T, int i) {
 #if defined(__CUDA_ARCH__)
-  return g_smem[T1_OFF + i];
+  return RS_TBL(T1_OFF)[i];
 #else
   return T.t1[i];
 #endif
 }
 RS_HD int t2_at(const Tabs& T, int i) {
 #if defined(__CUDA_ARCH__)
-  return g_smem[T2_OFF + i];
+  return RS_TBL(T2_OFF)[i];
 #else
   return T.t2[i];
 #endif
 }
 RS_HD uint32_t t3_at(const Tabs& T, int i) {
 #if defined(__CUDA_ARCH__)
-  return reinterpret_cast<const uint32_t*>(g_smem)[i];
+  return reinterpret_cast<const uint32_t*>(RS_TBL(0))[i];
 #else
   return T.t3[i];
 #endif
@@ -201,7 +209,7 @@ RS_HD int cls_byte(uint32_t cls, int s) { return (cls >> (8 * s)) & 255; }
 // base-5 code delta of one tile of kind k (staged table on the device)
 RS_HD uint32_t kind_pow(int k) {
 #if defined(__CUDA_ARCH__)
-  return reinterpret_cast<const uint32_t*>(g_smem + POW_OFF)[k];
+  return reinterpret_cast<const uint32_t*>(RS_TBL(POW_OFF))[k];
 #else
   return kind_pow_calc(k);
 #endif
