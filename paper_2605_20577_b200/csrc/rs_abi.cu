@@ -324,14 +324,11 @@ __global__ void __launch_bounds__(BLOCK) k_init(const __grid_constant__ Soa S, c
 // pass over the env's state.  With RS_STEP_AUTORESET the rewards / flags
 // describe the transition while the legal mask, current player and
 // observation already belong to the next game (Pgx auto_reset convention).
-// Env <-> thread mapping with `epw` envs per warp: lanes >= epw idle.  At
-// small batches a few envs per warp spread the batch over many more warps
-// (the step is a long dependent chain; the SMs' issue slots are idle), and
-// fewer envs per warp also means fewer divergent paths per warp.
-__device__ __forceinline__ int env_of_thread(int gtid, int epw) {
-  const int lane = gtid & 31;
-  return lane < epw ? (gtid >> 5) * epw + lane : -1;
-}
+// Env <-> thread mapping: `epw` envs per warp, each env run by a group of
+// 2^glog2 lanes (rs_common.cuh lane groups).  At small batches a few envs
+// per warp spread the batch over many more warps (the step is a long
+// dependent chain; the SMs' issue slots are idle), fewer envs per warp also
+// means fewer divergent paths per warp, and the idle lanes join their env.
 
 __global__ void __launch_bounds__(ROLL_BLOCK, ROLL_MINB) k_step(const __grid_constant__ Soa S, const __grid_constant__ DevTables D,
     const __grid_constant__ Cfg C, const int32_t* actions, int flags, rs_obs_out obs, int32_t* next_actions,
@@ -651,17 +648,6 @@ Cfg to_cfg(const rs_config* c) {
              c->kazoe, c->double_yakuman, c->agari_yame, c->renchan_cap};
 }
 int grid_of(int n) { return (n + BLOCK - 1) / BLOCK; }
-
-// one thread per env; below 148 x 128 envs the CTAs shrink (to a multiple
-// of 32) so the warps spread over every SM instead of filling a few
-void launch_dims(const rs_handle* h, int* grid, int* block) {
-  if (h->n < h->num_sms * BLOCK) {
-    *block = std::max(32, ((h->n + h->num_sms - 1) / h->num_sms + 31) & ~31);
-  } else {
-    *block = BLOCK;
-  }
-  *grid = (h->n + *block - 1) / *block;
-}
 
 // grid of `block`-thread CTAs covering n envs at `epw` envs per warp, capped
 // at `max_ctas` (the grid-stride kernels then loop)
