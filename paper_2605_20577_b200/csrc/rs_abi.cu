@@ -184,7 +184,24 @@ __device__ __forceinline__ void tables_wait() {
       "}\n" ::"r"(bar_addr)
       : "memory");
 }
-// issue the copy; the caller waits (tables_wait) before the first table read
+__device__ __forceinline__ uint32_t cluster_ncta() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_nctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+// issue the copy; the caller waits (tables_wait) before the first table read.
+// Launched as a thread-block cluster (RINSHAN_CLUSTER, stepping kernels), the
+// CTAs of the cluster split the block: CTA r fetches slice r once from L2 and
+// multicasts it into every CTA of the cluster, so the launch-start burst of
+// table reads (every CTA at once) shrinks by the cluster size.  Each CTA's
+// barrier expects the whole block; the cluster barrier orders the barrier
+// initialisations before any peer's slice can complete on them.  A CTA must
+// wait on its barrier before exiting (peers write into its shared memory).
 __device__ __forceinline__ void tables_begin(const DevTables& D, int grp_log2) {
   const uint32_t bar_addr = (uint32_t)__cvta_generic_to_shared(&s_tables_bar);
 #if defined(RS_TABLES_GLOBAL)
@@ -192,6 +209,8 @@ __device__ __forceinline__ void tables_begin(const DevTables& D, int grp_log2) {
   __syncthreads();
   return;
 #endif
+  const uint32_t nc = cluster_ncta();
+  const uint32_t dst = (uint32_t)__cvta_generic_to_shared(g_smem);
   if (threadIdx.x == 0) {
     s_grp_log2 = grp_log2;  // lanes per env (rs_common.cuh), published by the barrier below
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar_addr) : "memory");
@@ -199,13 +218,30 @@ __device__ __forceinline__ void tables_begin(const DevTables& D, int grp_log2) {
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar_addr), "r"(STAGE_BYTES)
                  : "memory");
-    asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-            (uint32_t)__cvta_generic_to_shared(g_smem)),
-        "l"(D.t3), "r"(STAGE_BYTES), "r"(bar_addr)
-        : "memory");
+    if (nc == 1)
+      asm volatile(
+          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+          "l"(D.t3), "r"(STAGE_BYTES), "r"(bar_addr)
+          : "memory");
   }
-  __syncthreads();
+  if (nc == 1) {
+    __syncthreads();
+    return;
+  }
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+  if (threadIdx.x == 0) {
+    const uint32_t chunk = ((STAGE_BYTES + nc - 1) / nc + 15u) & ~15u;
+    const uint32_t off = cluster_rank() * chunk;
+    if (off < STAGE_BYTES) {
+      const uint32_t bytes = min(chunk, STAGE_BYTES - off);
+      const uint16_t mask = (uint16_t)((1u << nc) - 1u);
+      asm volatile(
+          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster [%0], [%1], %2, "
+          "[%3], %4;" ::"r"(dst + off),
+          "l"(reinterpret_cast<const uint8_t*>(D.t3) + off), "r"(bytes), "r"(bar_addr), "h"(mask)
+          : "memory");
+    }
+  }
 }
 __device__ __forceinline__ Tabs stage_tables(const DevTables& D, int grp_log2 = 0) {
   tables_begin(D, grp_log2);
@@ -337,9 +373,11 @@ __global__ void __launch_bounds__(ROLL_BLOCK, ROLL_MINB) k_step(const __grid_con
   tables_begin(D, glog2);  // the action and header loads overlap the table copy
   const Tabs T{};
   const int lane = threadIdx.x & 31;
-  if ((lane >> glog2) >= epw) return;
   const int q = ((blockIdx.x * blockDim.x + threadIdx.x) >> 5) * epw + (lane >> glog2);
-  if (q >= S.n) return;
+  if ((lane >> glog2) >= epw || q >= S.n) {
+    tables_wait();  // (cluster launches: peers may still be writing this CTA's tables)
+    return;
+  }
   const int e = order ? order[q] : q;  // envs grouped by the kind of their step (large batches)
   // one stage slot per env, shared by the env's lane group
   const uint32_t sb = slot_off((threadIdx.x >> 5) * epw + (lane >> glog2));
@@ -535,6 +573,7 @@ __global__ void __launch_bounds__(ROLL_BLOCK, ROLL_MINB) k_rollout(const __grid_
     }
   }
   if (staged && sub == 0) stage_wait_all();
+  if (!tables_ready) tables_wait();  // a CTA without envs (cluster padding) still receives the tables
   if (stats) {
     unsigned long long g = games;
     for (int off = 16; off > 0; off >>= 1) g += __shfl_down_sync(0xffffffffu, g, off);
@@ -639,6 +678,10 @@ struct rs_handle {
   int epw_override;         // RINSHAN_EPW (tuning experiments), 0 = heuristic
   bool persist;             // launch with the tables' L2 persisting window
   cudaAccessPolicyWindow window;
+  // stepping kernels as thread-block clusters of this many CTAs, the table
+  // block multicast over the cluster (tables_begin); RINSHAN_CLUSTER
+  int cluster;
+  int occ_cl_key[8], occ_cl_val[8];  // co-resident clusters per (block, smem)
 };
 
 namespace {
@@ -662,7 +705,7 @@ int warp_grid(const rs_handle* h, int epw, int block, int max_ctas) {
 // (spread over every SM), else ROLL_BLOCK-thread CTAs; one stage slot per
 // env of the CTA.  `ctas` = resident CTAs per SM (occupancy, cached).
 struct Launch {
-  int grid, block, smem, epw, ctas, staged, glog2, ordered;
+  int grid, block, smem, epw, ctas, staged, glog2, ordered, cluster;
 };
 int resident_ctas(rs_handle* h, int block, int smem) {
   const int key = block * 1048576 + smem;
@@ -700,7 +743,40 @@ Launch launch_at(rs_handle* h, int epw) {
   L.smem = L.staged ? smem_staged(L.block, L.block / 32 * epw) : smem_for(L.block);
   L.ctas = resident_ctas(h, L.block, L.smem);
   L.grid = warp_grid(h, epw, L.block, 0);
+  L.cluster = h->cluster;
+  L.grid = (L.grid + L.cluster - 1) / L.cluster * L.cluster;
   return L;
+}
+// CTAs of the persistent grid: every resident CTA, or with clusters every
+// CTA of the clusters that fit at once (cudaOccupancyMaxActiveClusters)
+int persistent_ctas(rs_handle* h, const Launch& L) {
+  if (L.cluster <= 1) return h->num_sms * L.ctas;
+  const int key = L.block * 1048576 + L.smem;
+  for (int i = 0; i < 8; i++)
+    if (h->occ_cl_key[i] == key) return h->occ_cl_val[i];
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3((unsigned)L.grid);
+  cfg.blockDim = dim3((unsigned)L.block);
+  cfg.dynamicSmemBytes = (size_t)L.smem;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = (unsigned)L.cluster;
+  at[0].val.clusterDim.y = at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  int clusters = 0;
+  if (cudaOccupancyMaxActiveClusters(&clusters, k_rollout, &cfg) != cudaSuccess) {
+    cudaGetLastError();
+    clusters = h->num_sms * L.ctas / L.cluster;
+  }
+  const int ctas = std::max(clusters, 1) * L.cluster;
+  for (int i = 0; i < 8; i++)
+    if (h->occ_cl_key[i] == 0) {
+      h->occ_cl_key[i] = key;
+      h->occ_cl_val[i] = ctas;
+      break;
+    }
+  return ctas;
 }
 // envs per warp: the fewest (power of two) whose warps all fit in one wave
 // (7/8 of the resident warps).  A step is a long dependent chain per env and
@@ -722,7 +798,7 @@ int envs_per_warp(rs_handle* h) {
 // `persistent` caps the grid at the resident CTAs (k_rollout walks env tiles)
 Launch step_launch(rs_handle* h, bool persistent) {
   Launch L = launch_at(h, envs_per_warp(h));
-  if (persistent) L.grid = std::min(L.grid, h->num_sms * L.ctas);
+  if (persistent) L.grid = std::min(L.grid, persistent_ctas(h, L));
   return L;
 }
 
@@ -743,13 +819,20 @@ cudaError_t launch_tables(const rs_handle* h, void (*kernel)(KArgs...), int grid
   cfg.blockDim = dim3((unsigned)block);
   cfg.dynamicSmemBytes = (size_t)smem;
   cfg.stream = st;
-  cudaLaunchAttribute at[1];
+  cudaLaunchAttribute at[2];
+  int na = 0;
   if (h->persist) {
-    at[0].id = cudaLaunchAttributeAccessPolicyWindow;
-    at[0].val.accessPolicyWindow = h->window;
-    cfg.attrs = at;
-    cfg.numAttrs = 1;
+    at[na].id = cudaLaunchAttributeAccessPolicyWindow;
+    at[na++].val.accessPolicyWindow = h->window;
   }
+  if (h->cluster > 1) {  // the grid is a multiple of the cluster size (launch_at)
+    at[na].id = cudaLaunchAttributeClusterDimension;
+    at[na].val.clusterDim.x = (unsigned)h->cluster;
+    at[na].val.clusterDim.y = at[na].val.clusterDim.z = 1;
+    na++;
+  }
+  cfg.attrs = na ? at : nullptr;
+  cfg.numAttrs = (unsigned)na;
   return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
 }
 
@@ -909,6 +992,10 @@ int rs_create(rs_handle** out, int64_t n_envs, const rs_config* cfg, int32_t dev
   if ((err = cudaDeviceGetAttribute(&h->num_sms, cudaDevAttrMultiProcessorCount, device)))
     return cleanup(err, "device query");
   for (int i = 0; i < 16; i++) h->occ_key[i] = h->occ_val[i] = 0;
+  for (int i = 0; i < 8; i++) h->occ_cl_key[i] = h->occ_cl_val[i] = 0;
+  const char* cluster_env = getenv("RINSHAN_CLUSTER");
+  h->cluster = cluster_env ? std::max(1, std::min(8, atoi(cluster_env))) : 1;
+  if (h->cluster & (h->cluster - 1)) h->cluster = 1;
   const char* stage_env = getenv("RINSHAN_STAGE");
   h->stage_mode = stage_env ? std::max(0, std::min(2, atoi(stage_env))) : 0;
   const char* groups_env = getenv("RINSHAN_GROUPS");

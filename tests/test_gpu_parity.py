@@ -69,6 +69,32 @@ def test_shared_memory_stage_matches_oracle(rule, stage, monkeypatch):
     assert torch.equal(env.rewards, plain.rewards)
 
 
+@pytest.mark.parametrize("cluster", ("2", "4"))
+def test_cluster_multicast_tables_match_oracle(cluster, monkeypatch):
+    """the stepping kernels launched as thread-block clusters with the table
+    block multicast over the cluster (RINSHAN_CLUSTER, read at rs_create);
+    1000 envs leave padding CTAs without envs in the last cluster"""
+    monkeypatch.setenv("RINSHAN_CLUSTER", cluster)
+    n, steps = 1000, 200
+    cfg = EnvConfig(rule="red")
+    env = BatchEnv(n, cfg).init(seed=21, index_base=0)
+    digests = torch.zeros(n, dtype=torch.int64, device="cuda")
+    env.rollout(steps, digests=digests)
+    torch.cuda.synchronize()
+    _, ref = O.run_shard(_oracle_cfg(cfg), 21, 0, n, steps, digests=True)
+    assert [int(x) & ((1 << 64) - 1) for x in digests.cpu().tolist()] == ref
+    monkeypatch.setenv("RINSHAN_CLUSTER", "1")
+    plain = BatchEnv(n, cfg).init(seed=21, index_base=0)
+    plain.rollout(steps)
+    for _ in range(40):
+        acts = plain.random_actions()
+        plain.step(acts, autoreset=True)
+        env.step(acts, autoreset=True)
+    torch.cuda.synchronize()
+    assert torch.equal(env.legal_bits, plain.legal_bits)
+    assert torch.equal(env.rewards, plain.rewards)
+
+
 @pytest.mark.parametrize("rule", RULES)
 @pytest.mark.parametrize("mode", ("single", "half"))
 def test_heuristic_rollout_digests_match_oracle(rule, mode):
