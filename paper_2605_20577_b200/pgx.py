@@ -19,6 +19,7 @@ from __future__ import annotations
 import ctypes as C
 from dataclasses import dataclass, field
 
+import numpy as np
 import torch
 
 from . import abi, records
@@ -128,11 +129,29 @@ def _mask_int(words) -> int:
     return v
 
 
+def _reward(config: EnvConfig, x: float, illegal: bool) -> float:
+    """The reference's Python double for a device float32 reward
+    (core.py:74-78, 89-94).  Terminal rewards are (s - 25000) / 25000 with s a
+    multiple of 100, the rank values 1 / .333 / -.333 / -1, or the illegal
+    penalty: decimals of at most 6 significant digits, which the shortest
+    float32 representation recovers exactly; the penalty comes from the
+    config itself.  The device value must be that double rounded to float32."""
+    f32 = np.float32(x)
+    if illegal and f32 != 0 and f32 == np.float32(config.illegal_penalty):
+        d = float(config.illegal_penalty)
+    else:
+        d = float(str(f32))
+    if np.float32(d) != f32:
+        raise RuntimeError(f"device reward {x!r} is not a reference reward")
+    return d
+
+
 def _wrap(config: EnvConfig, rec: abi.rs_env_rec, events, results, game_legal) -> EnvState:
     m = _mask_int(rec.legal_mask)
+    illegal = bool(rec.status & abi.STATUS_ILLEGAL)
     return EnvState(config=config, current_player=int(rec.current_player),
                     legal=abi.mask_to_ids(rec.legal_mask), legal_mask_int=m,
-                    rewards=tuple(float(x) for x in rec.rewards),
+                    rewards=tuple(_reward(config, float(x), illegal) for x in rec.rewards),
                     terminated=bool(rec.env_terminated), truncated=bool(rec.env_truncated),
                     record=rec, events=tuple(events), results=tuple(results), game_legal=tuple(game_legal))
 

@@ -18,6 +18,9 @@ Writes small, deterministic JSON(.gz) files next to this script:
   logs.json.gz      mjlog-lite-v1 logs (engine/log.py) of the bench loop's
                     games, canonical JSON
   renders.json.gz   render/svg.py documents (sha256) of reference states
+  sessions.json.gz  service/sessions.py games (agents + a scripted human):
+                    action lists, persisted documents, final fingerprints
+                    and the service/app.py view documents (sha256)
 """
 
 from __future__ import annotations
@@ -454,6 +457,58 @@ def make_renders():
     dump("renders.json.gz", out)
 
 
+# (rule, mode, seed, human seats, agents): every agent kind, several humans,
+# no human at all (the whole game runs inside new_session)
+SESSION_CASES = (("red", "single", 11, [0], {1: "heuristic", 2: "random", 3: "heuristic"}),
+                 ("no-red", "east", 12, [1, 3], {0: "random", 2: "heuristic"}),
+                 ("red", "single", 13, [], {0: "heuristic", 1: "random", 2: "heuristic", 3: "random"}),
+                 ("no-red", "single", 14, [2], {0: "random", 1: "random", 3: "random"}))
+
+
+def session_human_action(legal, n_actions):
+    """the scripted human: a deterministic pick from the ascending legal ids"""
+    return legal[(7 * n_actions + 3) % len(legal)]
+
+
+def view_digest(view) -> str:
+    v = dict(view)
+    v.pop("game_id")
+    return hashlib.sha256(json.dumps(v, sort_keys=True, separators=(",", ":")).encode()).hexdigest()
+
+
+def make_sessions():
+    """service/sessions.py new_session / apply_session_action / advance_agents
+    with a scripted human, the service/app.py `_view` of the human seat after
+    creation, every 25 actions and at the end, and the SessionStore document"""
+    from mjsim.service.app import _view
+    from mjsim.service.sessions import SessionStore, advance_agents, apply_session_action
+
+    out = []
+    for rule, mode, seed, humans, agents in SESSION_CASES:
+        cfg = EnvConfig(rule=rule, mode=mode)
+        store = SessionStore(None)
+        sess = store.create(cfg, seed, humans, agents)
+        seat = humans[0] if humans else 0
+        views = [(len(sess.actions), "en", view_digest(_view(sess, seat, "en")))]
+        while sess.waiting_on() is not None:
+            apply_session_action(sess, session_human_action(sess.state.legal, len(sess.actions)))
+            advance_agents(sess)
+            if len(views) < 40 and len(sess.actions) % 25 < 4:
+                views.append((len(sess.actions), "en", view_digest(_view(sess, seat, "en"))))
+        views.append((len(sess.actions), "ja", view_digest(_view(sess, seat, "ja"))))
+        views.append((len(sess.actions), "en", view_digest(_view(sess, seat, "en"))))
+        doc = {"id": "0123456789abcdef", "seed": seed,
+               "config": {"rule": rule, "mode": mode, "reward_scheme": cfg.reward_scheme, "max_steps": cfg.max_steps},
+               "human_seats": humans, "agents": {str(k): v for k, v in agents.items()},
+               "actions": [list(a) for a in sess.actions], "created_at": 0.0, "updated_at": 0.0}
+        out.append({"rule": rule, "mode": mode, "seed": seed, "human_seats": humans,
+                    "agents": {str(k): v for k, v in agents.items()}, "actions": [list(a) for a in sess.actions],
+                    "fingerprint": state_fingerprint(sess.state.game), "views": views, "doc": doc,
+                    "rewards": list(sess.state.rewards)})
+        print(f"session {rule} {mode} {seed}: {len(sess.actions)} actions, {len(views)} views")
+    dump("sessions.json.gz", out)
+
+
 if __name__ == "__main__":
     if len(sys.argv) > 1:
         for name in sys.argv[1:]:
@@ -467,3 +522,4 @@ if __name__ == "__main__":
     make_scenarios()
     make_logs()
     make_renders()
+    make_sessions()

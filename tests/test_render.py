@@ -55,3 +55,17 @@ def test_render_rejects_unknown_locale():
     g, rec, last = next(_states())
     with pytest.raises(ValueError):
         render.to_svg(rec, locale="fr")
+
+
+def test_action_table_rows():
+    """actions.py:48-96 names and kinds"""
+    from paper_2605_20577_b200 import sessions as S
+
+    t = S.action_table()
+    assert len(t) == 115 and [r["id"] for r in t] == list(range(115))
+    assert t[0] == {"id": 0, "kind": "discard", "tile": "1m", "red": False, "name": "discard 1m"}
+    assert t[35] == {"id": 35, "kind": "discard", "tile": "5p", "red": True, "name": "discard red 5p"}
+    assert t[42] == {"id": 42, "kind": "chi", "name": "chi mid"}
+    assert t[45 + 33] == {"id": 78, "kind": "kan_closed", "tile": "C", "name": "closed kan C"}
+    assert t[79 + 27] == {"id": 106, "kind": "kan_added", "tile": "E", "name": "added kan E"}
+    assert t[113]["kind"] == "pass" and t[114] == {"id": 114, "kind": "abort", "name": "nine terminals"}
