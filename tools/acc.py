@@ -27,3 +27,17 @@ for i, nm in enumerate(names):
     print('  %-20s mean %8.0f  p99 %8.0f  max %8.0f  frac-nonzero %.3f  share %.3f' % (nm, mm[:, i].mean(), mm[:, i].quantile(0.99), mm[:, i].max(), (mm[:, i] > 0).double().mean(), mm[:, i].sum() / tot.sum()))
 # per-warp critical path: max over envs of (step+obs+reset+policy)
 print('  total per env-step   mean %8.0f  p99 %8.0f  max %8.0f' % (tot.mean(), tot.quantile(0.99), tot.max()))
+# the slow warps: rows are per thread (g_marks[thread][8]); at 4,096 envs a
+# warp holds envs 2w (lanes 0-15) and 2w+1 (lanes 16-31); a divergent warp
+# runs both envs' paths, and each timer also sees the other env's cycles
+if n == 4096:
+    per = [m.double().view(-1, 32, 8)[:, [0, 16], :] for m in rows if len(m) == n * 16]
+    W = torch.cat(per)                               # [warps][2 envs][8]
+    tot_env = W[:, :, 0] + W[:, :, 4] + W[:, :, 5] + W[:, :, 6]
+    wt = tot_env.max(1).values
+    cut = wt.quantile(0.98)
+    sel = W[wt >= cut]
+    print('slowest 2%% of warps (%d): max-env total mean %.0f cycles vs all warps %.0f' % (len(sel), wt[wt >= cut].mean(), wt.mean()))
+    for i, nm in enumerate(names):
+        print('  %-20s slow warps: env-sum mean %8.0f  frac-nonzero %.2f   (all warps %8.0f)' % (
+            nm, sel[:, :, i].sum(1).mean(), (sel[:, :, i].sum(1) > 0).double().mean(), W[:, :, i].sum(1).mean()))
