@@ -62,6 +62,15 @@ class Policy(nn.Module):
         return self.pi(h), self.v(h).squeeze(-1)
 
 
+def sample_masked(logits: torch.Tensor, mask: torch.Tensor) -> tuple[torch.Tensor, torch.Tensor]:
+    """masked categorical sample (Gumbel-max: no host sync, CUDA-graph safe)
+    -> (action, log-probability)"""
+    logits = logits.masked_fill(~mask, -1e9)
+    u = torch.rand_like(logits).clamp_(1e-20, 1.0)
+    a = (logits - torch.log(-torch.log(u))).argmax(-1)
+    return a, F.log_softmax(logits, -1).gather(1, a[:, None]).squeeze(1)
+
+
 def legal_mask(bits: torch.Tensor) -> torch.Tensor:
     """packed u32[n,4] env legal bits -> bool[n,115]"""
     shifts = torch.arange(32, device=bits.device, dtype=torch.int32)
@@ -78,6 +87,8 @@ def main():
     p.add_argument("--minibatch", type=int, default=8192)
     p.add_argument("--rule", default="no-red")
     p.add_argument("--seed", type=int, default=0)
+    p.add_argument("--no-graph", dest="graph", action="store_false",
+                   help="run the rollout eagerly instead of replaying it as one CUDA graph")
     args = p.parse_args()
     print(json.dumps(run(args)))
 
@@ -108,25 +119,43 @@ def run(args) -> dict:
     b_seat = torch.empty(T, n, dtype=torch.long, device=dev)
     b_rew = torch.empty(T, n, 4, device=dev)
     b_done = torch.empty(T, n, device=dev)
-    stats = {"env_steps": 0, "rollout_s": 0.0, "update_s": 0.0, "games": 0}
-    for it in range(args.iters):
-        t0 = time.perf_counter()
+    stats = {"env_steps": 0, "rollout_s": 0.0, "update_s": 0.0, "games": 0, "graph": bool(getattr(args, "graph", True))}
+
+    def collect():
+        """T steps: policy on the device observation and mask, masked sample,
+        env step with auto-reset + observation; everything stays on the GPU
+        (no host sync), so the whole horizon can be one CUDA graph"""
         with torch.no_grad():
             for t in range(T):
                 for k in keys:
                     buf[k][t].copy_(obs[k])
                 mask = legal_mask(env.legal_bits)
                 logits, v = net(obs)
-                logits = logits.masked_fill(~mask, -1e9)
-                a = torch.distributions.Categorical(logits=logits).sample()
-                b_mask[t], b_act[t], b_val[t] = mask, a, v
-                b_logp[t] = F.log_softmax(logits, -1).gather(1, a[:, None]).squeeze(1)
+                a, logp = sample_masked(logits, mask)
+                b_mask[t], b_act[t], b_val[t], b_logp[t] = mask, a, v, logp
                 b_seat[t] = env.current_player.long()
                 env.step(a.int(), autoreset=True, observe=True)  # obs / mask now the next state's
                 b_rew[t] = env.rewards
                 b_done[t] = (env.terminated | env.truncated).float()
+
+    graph = None
+    for it in range(args.iters):
+        t0 = time.perf_counter()
+        if graph is not None:
+            graph.replay()
+        else:
+            collect()
+            if stats["graph"]:
+                # the eager horizon above warmed up every kernel; capture the
+                # next one (the weights are read in place, so updates apply)
+                torch.cuda.synchronize(dev)
+                graph = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(graph):
+                    collect()
         torch.cuda.synchronize(dev)
-        stats["rollout_s"] += time.perf_counter() - t0
+        if it > 0 or not stats["graph"]:  # the capture iteration's time is not a rollout
+            stats["rollout_s"] += time.perf_counter() - t0
+            stats["timed_steps"] = stats.get("timed_steps", 0) + n * T
         stats["env_steps"] += n * T
         stats["games"] += int(b_done.sum().item())
         t1 = time.perf_counter()
@@ -174,7 +203,7 @@ def run(args) -> dict:
         torch.cuda.synchronize(dev)
         stats["update_s"] += time.perf_counter() - t1
         stats["last_loss"] = float(loss.item())
-    stats["env_steps_per_s_rollout"] = stats["env_steps"] / max(stats["rollout_s"], 1e-9)
+    stats["env_steps_per_s_rollout"] = stats.get("timed_steps", 0) / max(stats["rollout_s"], 1e-9)
     if world > 1:
         t = torch.tensor([stats["env_steps"], stats["games"]], dtype=torch.float64, device=dev)
         dist.all_reduce(t)

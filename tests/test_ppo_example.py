@@ -24,12 +24,57 @@ def _load():
     return m
 
 
-def test_ppo_selfplay_small():
+@pytest.mark.parametrize("graph", (False, True))
+def test_ppo_selfplay_small(graph):
+    """eager, and with the rollout horizon replayed as one CUDA graph"""
     m = _load()
-    args = argparse.Namespace(envs=256, horizon=24, iters=2, epochs=1, minibatch=2048, rule="no-red", seed=3)
+    args = argparse.Namespace(envs=256, horizon=24, iters=3, epochs=1, minibatch=2048, rule="no-red", seed=3,
+                              graph=graph)
     st = m.run(args)
-    assert st["env_steps"] == 2 * 256 * 24
+    assert st["env_steps"] == 3 * 256 * 24 and st["graph"] == graph
     assert math.isfinite(st["last_loss"])
+    assert st["env_steps_per_s_rollout"] > 0
+
+
+def test_graph_rollout_steps_the_envs_like_eager():
+    """the captured horizon replays real env steps: the same actions fed to
+    a second env eagerly give the same rewards, masks and flags"""
+    m = _load()
+    from paper_2605_20577_b200.env import BatchEnv, EnvConfig
+
+    n, T = 128, 16
+    a_env = BatchEnv(n, EnvConfig(rule="red")).init(seed=5)
+    b_env = BatchEnv(n, EnvConfig(rule="red")).init(seed=5)
+    obs = a_env.observe()
+    torch.manual_seed(0)
+    net = m.Policy().cuda()
+    acts = torch.empty(T, n, dtype=torch.int32, device="cuda")
+    rews = torch.empty(T, n, 4, device="cuda")
+
+    def body():
+        with torch.no_grad():
+            for t in range(T):
+                logits, _ = net(obs)
+                a, _ = m.sample_masked(logits, m.legal_mask(a_env.legal_bits))
+                acts[t] = a.int()
+                a_env.step(acts[t], autoreset=True, observe=True)
+                rews[t] = a_env.rewards
+
+    body()  # warm-up (eager)
+    for t in range(T):
+        b_env.step(acts[t], autoreset=True, observe=True)
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        body()
+    for _ in range(2):
+        g.replay()
+        torch.cuda.synchronize()
+        for t in range(T):
+            b_env.step(acts[t], autoreset=True, observe=True)
+            torch.cuda.synchronize()
+        assert torch.equal(rews[T - 1], b_env.rewards)
+        assert torch.equal(a_env.legal_bits, b_env.legal_bits)
+        assert int(b_env.status.sum().item()) == 0
 
 
 def test_masked_sampling_is_always_legal():
