@@ -18,6 +18,8 @@ Writes small, deterministic JSON(.gz) files next to this script:
   logs.json.gz      mjlog-lite-v1 logs (engine/log.py) of the bench loop's
                     games, canonical JSON
   renders.json.gz   render/svg.py documents (sha256) of reference states
+  cli.json.gz       cli.py selfplay logs and render SVGs (sha256), bench
+                    rows' games_completed (bench/runner.py rollout)
   sessions.json.gz  service/sessions.py games (agents + a scripted human):
                     action lists, persisted documents, final fingerprints
                     and the service/app.py view documents (sha256)
@@ -509,6 +511,45 @@ def make_sessions():
     dump("sessions.json.gz", out)
 
 
+def make_cli():
+    """cli.py _cmd_selfplay / _cmd_render outputs and bench/runner.py
+    rollout rows (games completed in the first pass)"""
+    import argparse
+    import tempfile
+
+    from mjsim import cli
+    from mjsim.bench import BenchConfig
+    from mjsim.bench.runner import rollout
+
+    out = {"selfplay": [], "render": [], "bench": []}
+    tmp = Path(tempfile.mkdtemp())
+    logs = []
+    for rule, mode, seed, policy in (("red", "single", 5, "random"), ("no-red", "single", 6, "heuristic"),
+                                     ("red", "east", 7, "random"), ("no-red", "single", 8, "random")):
+        path = tmp / f"log{seed}.json"
+        cli._cmd_selfplay(argparse.Namespace(rule=rule, mode=mode, seed=seed, policy=policy, out=str(path)))
+        text = path.read_text()
+        logs.append(path)
+        out["selfplay"].append({"rule": rule, "mode": mode, "seed": seed, "policy": policy,
+                                "sha256": hashlib.sha256(text.encode()).hexdigest(), "len": len(text)})
+    for li, step, viewer, locale in ((0, None, None, "en"), (0, 30, 1, "ja"), (1, 60, -1, "en"), (2, None, 3, "en"),
+                                     (2, 250, 0, "ja")):
+        path = tmp / "r.svg"
+        cli._cmd_render(argparse.Namespace(log=str(logs[li]), step=step, viewer=viewer, locale=locale,
+                                           out=str(path)))
+        svg = path.read_text()
+        out["render"].append({"log": li, "step": step, "viewer": viewer, "locale": locale,
+                              "sha256": hashlib.sha256(svg.encode()).hexdigest(), "len": len(svg)})
+    for rule, mode, seed, batch, steps in (("no-red", "single", 0, 64, 100), ("red", "single", 1, 48, 150),
+                                           ("red", "east", 2, 16, 300), ("no-red", "single", 3, 32, 400)):
+        row, _ = rollout(BenchConfig(rule=rule, mode=mode, batch=batch, steps=steps, seed=seed, threads=4),
+                         warmup=False)
+        out["bench"].append({"rule": rule, "mode": mode, "seed": seed, "batch": batch, "steps": steps,
+                             "games_completed": row.games_completed})
+    print(f"cli: {len(out['selfplay'])} logs, {len(out['render'])} renders, {len(out['bench'])} bench rows")
+    dump("cli.json.gz", out)
+
+
 if __name__ == "__main__":
     if len(sys.argv) > 1:
         for name in sys.argv[1:]:
@@ -523,3 +564,4 @@ if __name__ == "__main__":
     make_logs()
     make_renders()
     make_sessions()
+    make_cli()
