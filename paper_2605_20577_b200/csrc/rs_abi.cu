@@ -249,6 +249,24 @@ __device__ __forceinline__ Tabs stage_tables(const DevTables& D, int grp_log2 = 
   return Tabs{};
 }
 
+// ------------------------------------------------------------ prefetch
+// RINSHAN_PREFETCH (default 1): before an env's first step, the lanes of
+// its group issue L1 prefetches for the lines the step will touch first --
+// the 544-byte block (5-6 lines) and, with mode 2, the env's four observer
+// streams (8 lines) -- one line per lane, so the dependent first touches of
+// the step find them in L1 instead of waiting on HBM one after another
+__device__ __forceinline__ void prefetch_env(const Soa& S, int e, int sub, int G, int mode) {
+  const uintptr_t b0 = (uintptr_t)(S.blk + (size_t)e * BLK_BYTES) & ~(uintptr_t)127;
+  const uintptr_t b1 = ((uintptr_t)(S.blk + (size_t)e * BLK_BYTES) + BLK_BYTES - 1) & ~(uintptr_t)127;
+  const int nb = (int)((b1 - b0) >> 7) + 1;
+  const int total = nb + (mode >= 2 ? EVOBS_BYTES / 128 : 0);
+  for (int k = sub; k < total; k += G) {
+    const uintptr_t a = k < nb ? b0 + ((uintptr_t)k << 7)
+                               : (uintptr_t)(S.evobs + (size_t)e * (4 * EVOBS_SLOTS)) + ((uintptr_t)(k - nb) << 7);
+    asm volatile("prefetch.global.L1 [%0];" ::"l"(a));
+  }
+}
+
 // --------------------------------------------------------------- stage
 // Each env a CTA works on owns a SLOT_BYTES slot after the staged tables
 // (rs_state.cuh): its 544-byte block moves HBM -> slot with one TMA bulk
@@ -369,7 +387,7 @@ __global__ void __launch_bounds__(BLOCK) k_init(const __grid_constant__ Soa S, c
 __global__ void __launch_bounds__(ROLL_BLOCK, ROLL_MINB) k_step(const __grid_constant__ Soa S, const __grid_constant__ DevTables D,
     const __grid_constant__ Cfg C, const int32_t* actions, int flags, rs_obs_out obs, int32_t* next_actions,
     StepOut out, int epw, int staged, int glog2, int check, rs_step_rec* recs, const int32_t* order,
-    uint8_t* kind_out) {
+    uint8_t* kind_out, int prefetch) {
   tables_begin(D, glog2);  // the action and header loads overlap the table copy
   const Tabs T{};
   const int lane = threadIdx.x & 31;
@@ -391,6 +409,7 @@ __global__ void __launch_bounds__(ROLL_BLOCK, ROLL_MINB) k_step(const __grid_con
     __syncwarp(gm);  // the slot's barrier is initialised for the whole group
     stage_wait(sb, 0);
   }
+  if (prefetch && !staged) prefetch_env(S, e, sub, 1 << glog2, prefetch);
   const int action = actions[e];  // may live in mapped host memory (HostStepper)
   Engine E(S, T, C, e, staged ? g_smem + sb : S.blk + (size_t)e * BLK_BYTES);
   E.load();
@@ -483,7 +502,8 @@ __global__ void __launch_bounds__(ROLL_BLOCK, ROLL_MINB) k_rollout(const __grid_
                                                    StepOut traj, rs_rollout_stats* stats,
                                                    uint64_t* digests, StepOut out, int epw,
                                                    uint32_t* prof, int staged, int policy, int glog2,
-                                                   int check, const int32_t* order, uint8_t* kind_out) {
+                                                   int check, const int32_t* order, uint8_t* kind_out,
+                                                   int prefetch) {
   const uint32_t g_entry = prof ? globaltimer_lo() : 0u;
   tables_begin(D, glog2);  // the first env tile's header loads overlap the copy
   const Tabs T{};
@@ -511,6 +531,7 @@ __global__ void __launch_bounds__(ROLL_BLOCK, ROLL_MINB) k_rollout(const __grid_
       stage_wait(sb, phase);
       phase ^= 1u;
     }
+    if (prefetch && !staged) prefetch_env(S, e, sub, 1 << glog2, prefetch);
     Engine E(S, T, C, e, staged ? g_smem + sb : S.blk + (size_t)e * BLK_BYTES);
     E.load();
     uint64_t d = digests ? digests[e] : 0ull;
@@ -682,6 +703,7 @@ struct rs_handle {
   // block multicast over the cluster (tables_begin); RINSHAN_CLUSTER
   int cluster;
   int occ_cl_key[8], occ_cl_val[8];  // co-resident clusters per (block, smem)
+  int prefetch;  // RINSHAN_PREFETCH: L1 prefetch of an env's lines before its step (prefetch_env)
 };
 
 namespace {
@@ -996,6 +1018,10 @@ int rs_create(rs_handle** out, int64_t n_envs, const rs_config* cfg, int32_t dev
   const char* cluster_env = getenv("RINSHAN_CLUSTER");
   h->cluster = cluster_env ? std::max(1, std::min(8, atoi(cluster_env))) : 1;
   if (h->cluster & (h->cluster - 1)) h->cluster = 1;
+  const char* prefetch_env_s = getenv("RINSHAN_PREFETCH");
+  // measured on B200 (tools/prefetch_ab.sh): block lines +1-1.5 % at 4,096-16,384 envs, neutral at 1 M;
+  // the observer streams too (2) cost HBM traffic at large batches (1 M envs -7 %)
+  h->prefetch = prefetch_env_s ? std::max(0, std::min(2, atoi(prefetch_env_s))) : 1;
   const char* stage_env = getenv("RINSHAN_STAGE");
   h->stage_mode = stage_env ? std::max(0, std::min(2, atoi(stage_env))) : 0;
   const char* groups_env = getenv("RINSHAN_GROUPS");
@@ -1058,7 +1084,7 @@ int rs_step_ex(rs_handle* h, const int32_t* actions_dev, int32_t flags, const rs
   CUDA_TRY(launch_tables(h, k_step, L.grid, L.block, L.smem, st, h->S, h->D, h->cfg, actions_dev, flags, o,
                          next_actions_dev, step_out(h, out), L.epw, L.staged, L.glog2, h->check_steps,
                          (rs_step_rec*)nullptr, L.ordered ? (const int32_t*)h->order : nullptr,
-                         L.ordered ? h->kind : nullptr));
+                         L.ordered ? h->kind : nullptr, h->prefetch));
   return finish_step_out(h, out, st);
 }
 
@@ -1077,7 +1103,8 @@ int rs_step_rec_out(rs_handle* h, const int32_t* actions, int32_t flags, rs_step
   }
   CUDA_TRY(launch_tables(h, k_step, L.grid, L.block, L.smem, st, h->S, h->D, h->cfg, actions, flags, o,
                          (int32_t*)nullptr, StepOut{}, L.epw, L.staged, L.glog2, h->check_steps, recs,
-                         L.ordered ? (const int32_t*)h->order : nullptr, L.ordered ? h->kind : nullptr));
+                         L.ordered ? (const int32_t*)h->order : nullptr, L.ordered ? h->kind : nullptr,
+                         h->prefetch));
   return 0;
 }
 
@@ -1136,7 +1163,8 @@ int rs_rollout_policy(rs_handle* h, int32_t steps, int32_t policy, const rs_obs_
   CUDA_TRY(launch_tables(h, k_rollout, L.grid, L.block, L.smem, st, h->S, h->D, h->cfg, steps, o,
                          obs ? obs_slots : 0, actions_log, actors_log, step_out(h, traj), stats_dev, digests_dev,
                          step_out(h, out), L.epw, nullptr, L.staged, policy, L.glog2, h->check_steps,
-                         L.ordered ? (const int32_t*)h->order : nullptr, L.ordered ? h->kind : nullptr));
+                         L.ordered ? (const int32_t*)h->order : nullptr, L.ordered ? h->kind : nullptr,
+                         h->prefetch));
   return finish_step_out(h, out, st);
 }
 
@@ -1152,7 +1180,8 @@ int rs_debug_rollout_cycles(rs_handle* h, int32_t steps, const rs_obs_out* obs, 
   const Launch L = step_launch(h, true);
   CUDA_TRY(launch_tables(h, k_rollout, L.grid, L.block, L.smem, st, h->S, h->D, h->cfg, steps, o, obs ? 1 : 0,
                          nullptr, nullptr, StepOut{}, nullptr, nullptr, StepOut{}, L.epw, prof_dev, L.staged,
-                         (int)RS_POLICY_RANDOM, L.glog2, 0, (const int32_t*)nullptr, (uint8_t*)nullptr));
+                         (int)RS_POLICY_RANDOM, L.glog2, 0, (const int32_t*)nullptr, (uint8_t*)nullptr,
+                         h->prefetch));
   CUDA_TRY(cudaGetLastError());
   return 0;
 }
