@@ -279,6 +279,13 @@ int rs_init(rs_handle* h, const uint64_t* seeds_dev, const rs_step_out* out, voi
 int rs_init_indexed(rs_handle* h, uint64_t seed, int64_t index_base,
                     const rs_step_out* out, void* stream);
 int rs_step(rs_handle* h, const int32_t* actions_dev, const rs_step_out* out, void* stream);
+/* an action id for rs_step / rs_step_ex / rs_step_rec_out: the env is not
+ * stepped (state untouched: no transition, no auto-reset, no policy draw);
+ * its outputs describe its current state with zero rewards and status 0,
+ * and its next action is RS_ACTION_SKIP.  For actors that decide at
+ * different times (game sessions, asynchronous agents); the reference steps
+ * one env at a time and has no counterpart. */
+#define RS_ACTION_SKIP (-2147483647 - 1)
 
 /* rs_step fused with what an actor loop does next, in the same kernel:
  *   RS_STEP_AUTORESET  finished envs start their next game (auto-reset,

@@ -30,6 +30,7 @@ RIVER_TSUMOGIRI = 1
 RIVER_RIICHI = 2
 RIVER_CALLED = 4
 STATUS_INVARIANT = 4
+ACTION_SKIP = -(1 << 31)  # RS_ACTION_SKIP: the env is not stepped
 # rs_check_invariants bits (include/rinshan.h RS_INV_*)
 INV_SCORE_SUM = 1
 INV_TILES = 2

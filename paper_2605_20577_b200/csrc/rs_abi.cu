@@ -416,10 +416,20 @@ __global__ void __launch_bounds__(ROLL_BLOCK, ROLL_MINB) k_step(const __grid_con
   tables_wait();
   Mask115 m;
   float r[4];
-  const int st = E.step(action, m, r);
+  // RS_ACTION_SKIP: the env is not stepped (actors that have not decided
+  // yet); its outputs describe its current state with zero rewards
+  const bool skip = action == RS_ACTION_SKIP;
+  int st = 0;
+  if (skip) {
+    if (E.g.env_terminated || E.g.env_truncated) m.clear();
+    else m = E.load_legal();
+    r[0] = r[1] = r[2] = r[3] = 0.f;
+  } else {
+    st = E.step(action, m, r);
+  }
   const int term = E.g.env_terminated, trunc = E.g.env_truncated;
-  bool dirty = st != RS_STATUS_CONTRACT;
-  if ((flags & RS_STEP_AUTORESET) && (term || trunc)) {
+  bool dirty = !skip && st != RS_STATUS_CONTRACT;
+  if (!skip && (flags & RS_STEP_AUTORESET) && (term || trunc)) {
     float r2[4];
     E.g.resets++;
     E.init_game(derive_key(E.g.env_key, 2 + (uint64_t)E.g.resets), r2);
@@ -430,9 +440,10 @@ __global__ void __launch_bounds__(ROLL_BLOCK, ROLL_MINB) k_step(const __grid_con
   int next = -1;
   if (next_actions || recs) {
     const bool done = E.g.env_terminated || E.g.env_truncated;
-    next = done ? -1 : (flags & RS_STEP_HEURISTIC) ? E.heuristic_action(m) : E.random_action(m);
+    next = skip ? RS_ACTION_SKIP
+                : done ? -1 : (flags & RS_STEP_HEURISTIC) ? E.heuristic_action(m) : E.random_action(m);
     if (next_actions) next_actions[e] = next;
-    dirty |= !done;
+    dirty |= !done && !skip;
   }
   int st_out = st;
   if (check && check_invariants(E, true)) st_out |= (int)RS_STATUS_INVARIANT;  // debug: every step

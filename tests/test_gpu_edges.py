@@ -62,3 +62,46 @@ def test_max_batch_sampled_parity():
     with ThreadPoolExecutor(max_workers=os.cpu_count() or 4) as ex:
         ref = list(ex.map(lambda i: O.run_shard(cfg, seed, i, 1, 44, digests=True)[1][0], picks))
     assert [int(x) & ((1 << 64) - 1) for x in got] == ref
+
+
+@pytest.mark.parametrize("rule", ("no-red", "red"))
+def test_skip_action_leaves_envs_untouched(rule):
+    """RS_ACTION_SKIP: envs whose actor has not decided are not stepped.
+    Each env's trajectory depends only on its own action sequence, so env A
+    fed the same per-env action sequences as env B, with random SKIP ticks
+    interleaved, ends every env in B's state; skipped ticks report the
+    current mask / player, zero rewards and status 0"""
+    from paper_2605_20577_b200 import abi
+
+    n, T = 256, 120
+    cfg = EnvConfig(rule=rule)
+    b = BatchEnv(n, cfg).init(seed=31, index_base=0)
+    seq = []
+    for _ in range(T):
+        a = b.random_actions()
+        seq.append(a.clone())
+        b.step(a, autoreset=True)
+    seq = torch.stack(seq)  # [T][n]
+    a_env = BatchEnv(n, cfg).init(seed=31, index_base=0)
+    cnt = torch.zeros(n, dtype=torch.long, device="cuda")
+    gen = torch.Generator(device="cuda").manual_seed(3)
+    ar = torch.arange(n, device="cuda")
+    while int(cnt.min().item()) < T:
+        go = (torch.rand(n, device="cuda", generator=gen) < 0.6) & (cnt < T)
+        acts = torch.where(go, seq[cnt.clamp(max=T - 1), ar], torch.full_like(seq[0], abi.ACTION_SKIP))
+        before_bits, before_player = a_env.legal_bits.clone(), a_env.current_player.clone()
+        a_env.step(acts, autoreset=True)
+        skipped = ~go
+        assert torch.equal(a_env.legal_bits[skipped], before_bits[skipped])
+        assert torch.equal(a_env.current_player[skipped], before_player[skipped])
+        assert int(a_env.rewards[skipped].abs().sum().item()) == 0
+        assert int(a_env.status[skipped].sum().item()) == 0
+        cnt += go.long()
+    torch.cuda.synchronize()
+    for i in range(0, n, 17):
+        ra, rb = a_env.export(i), b.export(i)
+        # B's random_actions() drew from each env's policy stream; A's did not
+        assert ra.policy_counter == 0 and rb.policy_counter > 0
+        ra.policy_counter = rb.policy_counter
+        assert bytes(ra) == bytes(rb), i
+    assert torch.equal(a_env.legal_bits, b.legal_bits)
