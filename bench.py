@@ -347,15 +347,21 @@ def ours_arm(args, rank, world, local_rank):
     achieved = b_step * n / avg_launch_s / 1e9
     peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
     peak = peaks.get("hbm_gbs", 6650.0)
-    traffic = None
+    traffic = ncu_extra = None
     prof = ROOT / "profiles" / "ncu_rollout_summary.json"
     if prof.exists():
         try:
             pj = json.loads(prof.read_text())
             if pj.get("rule") == args.rule and pj.get("batch") == n:
                 traffic = pj.get("dram_bytes_per_launch")
+                ls = pj.get("launches") or []
+                if ls:  # instructions per step and warp execution efficiency beside the HBM fraction
+                    inst = sum(float(x["metrics"]["Executed Instructions"][0]) for x in ls) / len(ls)
+                    thr = sum(float(x["metrics"]["Avg. Active Threads Per Warp"][0]) for x in ls) / len(ls)
+                    ncu_extra = {"warp_inst_per_env_step": inst / n, "warp_exec_efficiency": thr / 32.0,
+                                 "source": "profiles/ncu_rollout_summary.json (" + str(pj.get("report")) + ")"}
         except Exception:
-            traffic = None
+            traffic = ncu_extra = None
 
     if rank == 0:
         line = {
@@ -375,7 +381,8 @@ def ours_arm(args, rank, world, local_rank):
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
                          "kernel": "k_rollout (K=1)", "bytes_per_env_step": b_step,
-                         "peak_source": "MEASURED_PEAKS.json hbm_gbs (burst copy)" if peaks else "fallback 6650"},
+                         "peak_source": "MEASURED_PEAKS.json hbm_gbs (burst copy)" if peaks else "fallback 6650",
+                         "ncu": ncu_extra},
             "cpu_baseline": cpu,
             "e2e": e2e,
             "fused_rollout": fused,
