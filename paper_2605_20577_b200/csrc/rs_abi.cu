@@ -44,9 +44,9 @@ constexpr int BLOCK = 128;
 // env of the CTA (staged stepping kernels) or a 144-byte shuffle scratch
 // per thread (kernels working on the blocks in HBM)
 constexpr int smem_staged(int block, int slots) {
-  return WALL_SLOT_OFF + block * WALL_STRIDE + slots * (int)SLOT_BYTES;
+  return WALL_SLOT_OFF + block * SCRATCH_STRIDE + slots * (int)SLOT_BYTES;
 }
-constexpr int smem_for(int block) { return WALL_SLOT_OFF + block * WALL_STRIDE; }
+constexpr int smem_for(int block) { return WALL_SLOT_OFF + block * SCRATCH_STRIDE; }
 // bytes of the staged t3 | t1 | t2 block (a TMA bulk copy is a multiple of 16 B)
 constexpr uint32_t STAGE_BYTES = (SMEM_TABLE_BYTES + 15u) & ~15u;
 
@@ -273,7 +273,7 @@ __device__ __forceinline__ void prefetch_env(const Soa& S, int e, int sub, int G
 // copy completing on the slot's mbarrier, the step runs on shared memory,
 // and the block moves back with one bulk copy (bulk_group).
 __device__ __forceinline__ uint32_t slot_off(int slot) {  // after the per-thread shuffle scratch
-  return (uint32_t)WALL_SLOT_OFF + blockDim.x * (uint32_t)WALL_STRIDE + (uint32_t)slot * SLOT_BYTES;
+  return (uint32_t)WALL_SLOT_OFF + blockDim.x * (uint32_t)SCRATCH_STRIDE + (uint32_t)slot * SLOT_BYTES;
 }
 __device__ __forceinline__ uint32_t smem_addr(uint32_t off) {
   return (uint32_t)__cvta_generic_to_shared(g_smem) + off;

@@ -142,12 +142,14 @@ struct Engine {
     // 144-byte scratch after the tables (copied to the block afterwards)
     uint8_t* const wall_dst = swall(bp);
 #if defined(__CUDA_ARCH__)
-    // (a staged wall is shared by the env's lane group: lanes shuffle privately)
-    const bool in_place = __isShared(wall_dst) && grp_size() == 1;
-    uint8_t* w = in_place ? wall_dst : g_smem + WALL_SLOT_OFF + threadIdx.x * WALL_STRIDE;
+    // always the thread's scratch (then copied to the block, staged or not):
+    // a pointer derived from the shared array alone keeps the swap chain on
+    // LDS / STS instead of generic loads and stores
+    constexpr bool in_place = false;
+    uint8_t* const w = g_smem + WALL_SLOT_OFF + threadIdx.x * SCRATCH_STRIDE;
 #else
-    const bool in_place = true;
-    uint8_t* w = wall_dst;
+    constexpr bool in_place = true;
+    uint8_t* const w = wall_dst;
 #endif
     {
       uint32_t* w32 = reinterpret_cast<uint32_t*>(w);
@@ -197,8 +199,10 @@ struct Engine {
     g.rng_counter = (uint32_t)c;
     if (!in_place) {
 #pragma unroll
-      for (int i = 0; i < WALL_STRIDE / 16; i++)
-        reinterpret_cast<uint4*>(wall_dst)[i] = reinterpret_cast<const uint4*>(w)[i];
+      for (int i = 0; i < WALL_STRIDE / 16; i++) {
+        const uint32_t* w32 = reinterpret_cast<const uint32_t*>(w) + 4 * i;  // (scratch: 4-byte aligned)
+        reinterpret_cast<uint4*>(wall_dst)[i] = make_uint4(w32[0], w32[1], w32[2], w32[3]);
+      }
     }
     RS_MARK(2);
     const int dealer = g.dealer();

@@ -23,6 +23,10 @@
 namespace rs {
 
 constexpr int WALL_STRIDE = 144;  // 136 tiles padded to 9 x 16 B
+// per-thread shuffle scratch in shared memory: 37 words, odd, so the 32 lanes
+// of a warp touching the same byte offset of their own copies hit 32
+// different banks (a 36-word stride put 4 lanes on every bank)
+constexpr int SCRATCH_STRIDE = 148;
 constexpr int EVOBS_SLOTS = RS_EVENT_WINDOW;                 // per observer
 constexpr int EVOBS_BYTES = 4 * EVOBS_SLOTS * 4;             // per env
 constexpr uint32_t EVOBS_PAD = 37u << 16;                    // (0, 0, 37)
