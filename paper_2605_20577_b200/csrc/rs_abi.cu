@@ -43,10 +43,10 @@ constexpr int BLOCK = 128;
 // dynamic shared memory: the staged tables, then either one stage slot per
 // env of the CTA (staged stepping kernels) or a 144-byte shuffle scratch
 // per thread (kernels working on the blocks in HBM)
-constexpr int smem_staged(int block, int slots) {
-  return WALL_SLOT_OFF + block * SCRATCH_STRIDE + slots * (int)SLOT_BYTES;
+constexpr int smem_staged(int block, int slots, int glog2 = 0) {
+  return WALL_SLOT_OFF + scratch_bytes(block, glog2) + slots * (int)SLOT_BYTES;
 }
-constexpr int smem_for(int block) { return WALL_SLOT_OFF + block * SCRATCH_STRIDE; }
+constexpr int smem_for(int block, int glog2 = 0) { return WALL_SLOT_OFF + scratch_bytes(block, glog2); }
 // bytes of the staged t3 | t1 | t2 block (a TMA bulk copy is a multiple of 16 B)
 constexpr uint32_t STAGE_BYTES = (SMEM_TABLE_BYTES + 15u) & ~15u;
 
@@ -272,8 +272,8 @@ __device__ __forceinline__ void prefetch_env(const Soa& S, int e, int sub, int G
 // (rs_state.cuh): its 544-byte block moves HBM -> slot with one TMA bulk
 // copy completing on the slot's mbarrier, the step runs on shared memory,
 // and the block moves back with one bulk copy (bulk_group).
-__device__ __forceinline__ uint32_t slot_off(int slot) {  // after the per-thread shuffle scratch
-  return (uint32_t)WALL_SLOT_OFF + blockDim.x * (uint32_t)SCRATCH_STRIDE + (uint32_t)slot * SLOT_BYTES;
+__device__ __forceinline__ uint32_t slot_off(int slot, int glog2) {  // after the shuffle scratch
+  return (uint32_t)WALL_SLOT_OFF + (uint32_t)scratch_bytes((int)blockDim.x, glog2) + (uint32_t)slot * SLOT_BYTES;
 }
 __device__ __forceinline__ uint32_t smem_addr(uint32_t off) {
   return (uint32_t)__cvta_generic_to_shared(g_smem) + off;
@@ -398,7 +398,7 @@ __global__ void __launch_bounds__(ROLL_BLOCK, ROLL_MINB) k_step(const __grid_con
   }
   const int e = order ? order[q] : q;  // envs grouped by the kind of their step (large batches)
   // one stage slot per env, shared by the env's lane group
-  const uint32_t sb = slot_off((threadIdx.x >> 5) * epw + (lane >> glog2));
+  const uint32_t sb = slot_off((threadIdx.x >> 5) * epw + (lane >> glog2), glog2);
   const int sub = lane & ((1 << glog2) - 1);
   const uint32_t gm = glog2 >= 5 ? 0xFFFFFFFFu : (((1u << (1 << glog2)) - 1u) << (lane - sub));
   if (staged) {
@@ -526,7 +526,7 @@ __global__ void __launch_bounds__(ROLL_BLOCK, ROLL_MINB) k_rollout(const __grid_
   const int sub = lane & ((1 << glog2) - 1);  // the lane's index in its env's group
   const uint32_t gm = glog2 >= 5 ? 0xFFFFFFFFu : (((1u << (1 << glog2)) - 1u) << (lane - sub));
   // one stage slot per env, shared by the env's lane group
-  const uint32_t sb = slot_off((threadIdx.x >> 5) * epw + (lane >> glog2));
+  const uint32_t sb = slot_off((threadIdx.x >> 5) * epw + (lane >> glog2), glog2);
   if (staged && (lane >> glog2) < epw && sub == 0) slot_bar_init(sb);
   uint32_t phase = 0;
   for (int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; w * epw < S.n; w += warps) {
@@ -773,7 +773,7 @@ Launch launch_at(rs_handle* h, int epw) {
   // +4 % / +75 %, 262 K -1.5 % / +50 %, 131 K -11 % / +25 %, below 64 K a
   // loss either way (the sort's launches cost more than the divergence saved)
   L.ordered = h->ordering == 2 || (h->ordering == 1 && h->n >= (1 << 18));
-  L.smem = L.staged ? smem_staged(L.block, L.block / 32 * epw) : smem_for(L.block);
+  L.smem = L.staged ? smem_staged(L.block, L.block / 32 * epw, L.glog2) : smem_for(L.block, L.glog2);
   L.ctas = resident_ctas(h, L.block, L.smem);
   L.grid = warp_grid(h, epw, L.block, 0);
   L.cluster = h->cluster;

@@ -141,14 +141,46 @@ struct Engine {
     // memory, in place when the block is staged, else in the thread's
     // 144-byte scratch after the tables (copied to the block afterwards)
     uint8_t* const wall_dst = swall(bp);
+    // Fisher-Yates (rng.py:59-65) on a shared-memory scratch (pointers derived
+    // from the shared array alone keep the swap chain on LDS / STS), copied
+    // to the block afterwards; the draws are counter-based: draw u of the
+    // deal (position 135 - u) uses counter rng_counter + 1 + u
+    uint64_t c = g.rng_counter;
 #if defined(__CUDA_ARCH__)
-    // always the thread's scratch (then copied to the block, staged or not):
-    // a pointer derived from the shared array alone keeps the swap chain on
-    // LDS / STS instead of generic loads and stores
-    constexpr bool in_place = false;
-    uint8_t* const w = g_smem + WALL_SLOT_OFF + threadIdx.x * SCRATCH_STRIDE;
+    const int G = grp_size();
+    uint8_t* const w = G > 1 ? g_smem + WALL_SLOT_OFF + (threadIdx.x >> s_grp_log2) * ENV_SCRATCH
+                             : g_smem + WALL_SLOT_OFF + threadIdx.x * SCRATCH_STRIDE;
+    if (G > 1) {
+      // lane group: one wall copy per env; the lanes draw the 135 targets in
+      // parallel, then lane 0 runs the swap chain alone (no redundant copies,
+      // a tenth of the shared memory per env)
+      const int sub = grp_sub();
+      const uint32_t gm = grp_mask();
+      uint32_t* w32 = reinterpret_cast<uint32_t*>(w);
+      for (int k = sub; k < 36; k += G) w32[k] = k < 34 ? 0x03020100u + 0x04040404u * (uint32_t)k : 0u;
+      uint8_t* const J = w + SCRATCH_STRIDE;
+      for (int i = 135 - sub; i > 0; i -= G)
+        J[i] = (uint8_t)randbelow_from(stream_value(g.rng_key, c + 1 + (uint64_t)(135 - i)), (uint32_t)(i + 1));
+      __syncwarp(gm);
+      if (sub == 0) {
+        for (int i = 135; i > 0; i -= 5) {  // 135 = 27 x 5
+          int j[5];
+#pragma unroll
+          for (int u = 0; u < 5; u++) j[u] = J[i - u];
+#pragma unroll
+          for (int u = 0; u < 5; u++) {
+            const uint8_t t = w[i - u];
+            w[i - u] = w[j[u]];
+            w[j[u]] = t;
+          }
+        }
+      }
+      __syncwarp(gm);
+      c += 135;
+      for (int k = sub; k < WALL_STRIDE / 16; k += G)
+        reinterpret_cast<uint4*>(wall_dst)[k] = make_uint4(w32[4 * k], w32[4 * k + 1], w32[4 * k + 2], w32[4 * k + 3]);
+    } else
 #else
-    constexpr bool in_place = true;
     uint8_t* const w = wall_dst;
 #endif
     {
@@ -156,32 +188,6 @@ struct Engine {
 #pragma unroll
       for (int i = 0; i < 34; i++) w32[i] = 0x03020100u + 0x04040404u * (uint32_t)i;
       w32[34] = w32[35] = 0;
-    }
-    // Fisher-Yates (rng.py:59-65): the draws are counter-based, so they are
-    // computed ahead (independent multiplies) and then swapped in order
-    uint64_t c = g.rng_counter;
-#if defined(__CUDA_ARCH__)
-    if (grp_size() > 1) {
-      // the env's lanes compute the draws of G swaps at once and every lane
-      // replays the swap chain on its own copy (shuffle broadcast)
-      const int G = grp_size(), sub = grp_sub();
-      const uint32_t gm = grp_mask();
-      const int base = (int)(threadIdx.x & 31) - sub;
-      for (int i0 = 135; i0 > 0; i0 -= G) {
-        const int i = i0 - sub;
-        const int mine = i > 0 ? (int)randbelow_from(stream_value(g.rng_key, c + 1 + (uint64_t)sub), (uint32_t)(i + 1)) : 0;
-        const int nu = i0 < G ? i0 : G;
-        for (int u = 0; u < nu; u++) {
-          const int j = __shfl_sync(gm, mine, base + u);
-          const uint8_t t = w[i0 - u];
-          w[i0 - u] = w[j];
-          w[j] = t;
-        }
-        c += (uint64_t)nu;
-      }
-    } else
-#endif
-    {
       for (int i = 135; i > 0; i -= 5) {
         int j[5];
 #pragma unroll
@@ -195,15 +201,12 @@ struct Engine {
           w[j[u]] = t;
         }
       }
+#if defined(__CUDA_ARCH__)
+      for (int k = 0; k < WALL_STRIDE / 16; k++)  // (scratch: 4-byte aligned)
+        reinterpret_cast<uint4*>(wall_dst)[k] = make_uint4(w32[4 * k], w32[4 * k + 1], w32[4 * k + 2], w32[4 * k + 3]);
+#endif
     }
     g.rng_counter = (uint32_t)c;
-    if (!in_place) {
-#pragma unroll
-      for (int i = 0; i < WALL_STRIDE / 16; i++) {
-        const uint32_t* w32 = reinterpret_cast<const uint32_t*>(w) + 4 * i;  // (scratch: 4-byte aligned)
-        reinterpret_cast<uint4*>(wall_dst)[i] = make_uint4(w32[0], w32[1], w32[2], w32[3]);
-      }
-    }
     RS_MARK(2);
     const int dealer = g.dealer();
     // deal 4-4-4 then 1 from the dealer (engine.py:142-151): seat s at

@@ -27,6 +27,13 @@ constexpr int WALL_STRIDE = 144;  // 136 tiles padded to 9 x 16 B
 // of a warp touching the same byte offset of their own copies hit 32
 // different banks (a 36-word stride put 4 lanes on every bank)
 constexpr int SCRATCH_STRIDE = 148;
+// with lane groups (G > 1) one shuffle scratch per env instead: the wall
+// copy, then the 135 swap targets the group's lanes draw in parallel
+constexpr int ENV_SCRATCH = 288;  // 148 + 136, 16-byte multiple
+// shuffle scratch bytes of a CTA of `block` threads at 2^glog2 lanes per env
+RS_HD constexpr int scratch_bytes(int block, int glog2) {
+  return glog2 == 0 ? block * SCRATCH_STRIDE : (block >> glog2) * ENV_SCRATCH;
+}
 constexpr int EVOBS_SLOTS = RS_EVENT_WINDOW;                 // per observer
 constexpr int EVOBS_BYTES = 4 * EVOBS_SLOTS * 4;             // per env
 constexpr uint32_t EVOBS_PAD = 37u << 16;                    // (0, 0, 37)
