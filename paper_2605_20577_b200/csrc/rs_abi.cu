@@ -1004,6 +1004,7 @@ int rs_create(rs_handle** out, int64_t n_envs, const rs_config* cfg, int32_t dev
   }
   auto cleanup = [&](cudaError_t e2, const char* what) {
     cudaFree(h->mem);
+    cudaFree(h->sort_tmp);  // (value-initialised: null until allocated)
     delete h;
     return set_err((int)e2, "%s: %s", what, cudaGetErrorString(e2));
   };
