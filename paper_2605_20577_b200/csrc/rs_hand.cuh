@@ -257,7 +257,7 @@ RS_HD void special_shanten(const Hand& h, int& seven, int& kokushi) {
   kokushi = 13 - okinds - (opair ? 1 : 0);
 }
 // shanten_codes (shanten.py:172-182)
-RS_HD int full_shanten(const Tabs& T, const Hand& h, int melds) {
+RS_HD int full_shanten_impl(const Tabs& T, const Hand& h, int melds) {
   int s = std_shanten_cls(T, h.cls, melds);
   if (melds == 0 && s > -1) {
     int sp, kk;
@@ -266,6 +266,21 @@ RS_HD int full_shanten(const Tabs& T, const Hand& h, int melds) {
     if (s > -1 && kk < s) s = kk;
   }
   return s;
+}
+// one out-of-line copy shared by every call site: the engine inlines its
+// hand updates in many places, and eight inlined copies of the shanten
+// evaluation made the executed code outgrow the instruction caches
+// (DESIGN §4 item 24: +3 % at 4,096 envs); the hand crosses the call as
+// scalars, so the caller's Hand stays in registers
+RS_COLD int full_shanten_s(const Tabs& T, uint32_t w0, uint32_t w1, uint32_t w2, uint32_t w3, uint32_t w4,
+                           uint32_t cls, int melds) {
+  Hand h;
+  h.w0 = w0; h.w1 = w1; h.w2 = w2; h.w3 = w3; h.w4 = w4;
+  h.cls = cls;
+  return full_shanten_impl(T, h, melds);
+}
+RS_HD int full_shanten(const Tabs& T, const Hand& h, int melds) {
+  return full_shanten_s(T, h.w0, h.w1, h.w2, h.w3, h.w4, h.cls, melds);
 }
 
 // waits_from_codes (shanten.py:198-244) for a 13-form hand

@@ -1,6 +1,6 @@
 #!/bin/bash
 # profiling tool: front-end optimisation level (-Xcicc -O2 vs default -O3) sweep A/B
-for rep in 1 2; do for v in b0 cc2; do
+for rep in 1 2; do for v in ${VARIANTS:-b0 cc2}; do
   echo "== $v"
   RINSHAN_LIB=build_variants/_rinshan_$v.so python bench.py --sweep 1024,4096,16384,65536,262144,1048576 --no-cpu-baseline --no-e2e --steps 100 --warmup 5 2>/dev/null | grep sweep | python -c "
 import json,sys
