@@ -78,6 +78,27 @@ struct Mask115 {
   }
 };
 
+// engine.py:100-102 event, written into the env's 64-slot ring and, as
+// observe() will encode it (observe.py:92-106), into the four observer
+// streams
+RS_HD void emit_event_impl(uint16_t* ring, uint32_t* ob, uint32_t p, int rule, int type, int actor, int tile) {
+  ring[p] = (uint16_t)(type | ((actor + 1) << 4) | ((tile + 1) << 7));
+  const uint32_t ty = (uint32_t)(type <= 8 ? type : type - 1);  // ron / tsumo share token 8
+  const uint32_t tok = tile < 0 ? 37u
+                       : (rule == RS_RULE_RED && is_red_tile(tile)) ? (uint32_t)(34 + red_index_of_kind(tile >> 2))
+                                                                    : (uint32_t)(tile >> 2);
+#pragma unroll
+  for (int o = 0; o < 4; o++) {
+    const uint32_t rel = actor >= 0 ? (uint32_t)((actor - o) & 3) : 0u;
+    const uint32_t t = (type == EV_DRAW && actor != o) ? 37u : tok;  // opponents' draws hidden
+    ob[o * EVOBS_SLOTS + p] = ty | (rel << 8) | (t << 16);
+  }
+}
+// out of line, called with scalars (19 emit sites; DESIGN §4 item 25)
+RS_COLD void emit_event(uint16_t* ring, uint32_t* ob, uint32_t p, int rule, int type, int actor, int tile) {
+  emit_event_impl(ring, ob, p, rule, type, actor, tile);
+}
+
 struct Engine {
   const Soa& S;
   const Tabs& T;
@@ -117,20 +138,8 @@ struct Engine {
   // engine.py:100-102 (64-slot ring; the full history is reconstructed by
   // the host while stepping)
   RS_HD void emit(int type, int actor, int tile) {
-    const uint32_t p = g.events_len & 63u;
-    S.events[(uint32_t)e * RS_EVENT_WINDOW + p] = (uint16_t)(type | ((actor + 1) << 4) | ((tile + 1) << 7));
-    // observe.py:92-106 per observer, done once here instead of per observe
-    const uint32_t ty = (uint32_t)(type <= 8 ? type : type - 1);  // ron / tsumo share token 8
-    const uint32_t tok = tile < 0 ? 37u
-                         : (C.rule == RS_RULE_RED && is_red_tile(tile)) ? (uint32_t)(34 + red_index_of_kind(tile >> 2))
-                                                                         : (uint32_t)(tile >> 2);
-    uint32_t* ob = S.evobs + (uint32_t)e * (4 * EVOBS_SLOTS);
-#pragma unroll
-    for (int o = 0; o < 4; o++) {
-      const uint32_t rel = actor >= 0 ? (uint32_t)((actor - o) & 3) : 0u;
-      const uint32_t t = (type == EV_DRAW && actor != o) ? 37u : tok;  // opponents' draws hidden
-      ob[o * EVOBS_SLOTS + p] = ty | (rel << 8) | (t << 16);
-    }
+    emit_event(S.events + (uint32_t)e * RS_EVENT_WINDOW, S.evobs + (uint32_t)e * (4 * EVOBS_SLOTS),
+               g.events_len & 63u, C.rule, type, actor, tile);
     g.events_len++;
   }
 
