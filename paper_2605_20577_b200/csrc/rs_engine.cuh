@@ -99,6 +99,25 @@ RS_COLD void emit_event(uint16_t* ring, uint32_t* ob, uint32_t p, int rule, int 
   emit_event_impl(ring, ob, p, rule, type, actor, tile);
 }
 
+// engine members that can go out of line for a smaller hot code footprint
+// (DESIGN §4 items 23-26): draw() is (gains at every batch size); these
+// switches keep the measured alternatives reproducible (mixed results, off)
+#if defined(RS_OL_LEGAL)
+#define RS_OL_LEGAL_Q RS_COLD
+#else
+#define RS_OL_LEGAL_Q RS_HD
+#endif
+#if defined(RS_OL_CALL)
+#define RS_OL_CALL_Q RS_COLD
+#else
+#define RS_OL_CALL_Q RS_HD
+#endif
+#if defined(RS_OL_STANDS)
+#define RS_OL_STANDS_Q RS_COLD
+#else
+#define RS_OL_STANDS_Q RS_HD
+#endif
+
 struct Engine {
   const Soa& S;
   const Tabs& T;
@@ -262,7 +281,7 @@ struct Engine {
   }
 
   // engine.py:167-178
-  RS_HD void draw(int seat) {
+  RS_COLD void draw(int seat) {  // out of line: DESIGN §4 item 26
     Hand h = load_hand(bp, seat);
     h.info = hi::set_temp(h.info, 0);
     const int tile = wall(g.cursor);
@@ -486,7 +505,7 @@ struct Engine {
   }
 
   // engine.py:105-122 + 253-262
-  RS_HD void compute_legal(Mask115& m) const {
+  RS_OL_LEGAL_Q void compute_legal(Mask115& m) const {
     m.clear();
     if (g.terminated || g.truncated) return;
     if (g.phase == PH_CALL) legal_call(m);
@@ -672,7 +691,7 @@ struct Engine {
     }
   }
   // engine.py:594-615
-  RS_HD void discard_stands() {
+  RS_OL_STANDS_Q void discard_stands() {
     const int discarder = g.phase == PH_CALL ? g.call_from : g.actor;
     g.phase = PH_ACT;
     const uint32_t inf = info(discarder);
@@ -713,7 +732,7 @@ struct Engine {
            (n >= 2 && count_of(s, kind - 2) && count_of(s, kind - 1));
   }
   // engine.py:498-531
-  RS_HD bool begin_call_phase(int tile, int discarder, bool chankan) {
+  RS_OL_CALL_Q bool begin_call_phase(int tile, int discarder, bool chankan) {
     const int kind = tile >> 2;
     // the queue is packed as it is built (Game::queue layout): no arrays,
     // so nothing goes through local memory
