@@ -25,6 +25,9 @@
  *   rs_autoreset      bench/runner.py:107-109  auto-reset of finished envs
  *   rs_check_invariants engine/state.py:105-180 check_invariants (+ runner.py soak gates)
  *   rs_export_env     engine/state.py:191-242  serialize_state (projection record)
+ *   rs_export_envs    engine/state.py:191-242  serialize_state of many envs (one
+ *                                              launch + one copy; service/sessions.py
+ *                                              state reads, batched sessions)
  *   rs_import_env     tests/engine_helpers.py:58-105 craft() (crafted states)
  *
  * Error convention: every function returns 0 on success, a negative RS_E*
@@ -356,6 +359,9 @@ int rs_autoreset(rs_handle* h, const rs_step_out* out, void* stream);
 int rs_check_invariants(rs_handle* h, int32_t fast, uint32_t* flags_dev, void* stream);
 
 int rs_export_env(rs_handle* h, int64_t env, rs_env_rec* out);
+/* records of envs[0..count) (host indices) into out[count] (host); waits
+ * for the device like rs_export_env */
+int rs_export_envs(rs_handle* h, const int64_t* envs, int64_t count, rs_env_rec* out);
 int rs_import_env(rs_handle* h, int64_t env, const rs_env_rec* in);
 /* sizeof of the records above, for binding checks: config, meld, hand,
  * win, result, env, step */

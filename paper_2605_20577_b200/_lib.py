@@ -27,7 +27,7 @@ SYMBOLS = (
     "rs_tables_crc", "rs_tables_info", "rs_tables_shanten_std", "rs_create", "rs_destroy",
     "rs_num_envs", "rs_state_bytes", "rs_init", "rs_init_indexed", "rs_step", "rs_step_ex", "rs_step_rec_out",
     "rs_observe",
-    "rs_policy_random", "rs_policy_heuristic", "rs_rollout", "rs_rollout_policy", "rs_autoreset", "rs_check_invariants", "rs_export_env", "rs_import_env", "rs_record_sizes", "rs_debug_rollout_cycles",
+    "rs_policy_random", "rs_policy_heuristic", "rs_rollout", "rs_rollout_policy", "rs_autoreset", "rs_check_invariants", "rs_export_env", "rs_export_envs", "rs_import_env", "rs_record_sizes", "rs_debug_rollout_cycles",
 )
 
 _lib = None
@@ -92,6 +92,7 @@ def lib():
         L.rs_autoreset.argtypes = [vp, vp, vp]
         L.rs_check_invariants.argtypes = [vp, i32, vp, vp]
         L.rs_export_env.argtypes = [vp, i64, vp]
+        L.rs_export_envs.argtypes = [vp, vp, i64, vp]
         L.rs_import_env.argtypes = [vp, i64, vp]
         L.rs_record_sizes.argtypes = [vp]
         L.rs_debug_rollout_cycles.argtypes = [vp, i32, vp, vp, vp]

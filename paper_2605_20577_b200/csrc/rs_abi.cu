@@ -664,6 +664,16 @@ __global__ void k_export(const __grid_constant__ Soa S, const __grid_constant__ 
   export_env(E, C, *out);
 }
 
+// one CTA per listed env: the records of many envs in one launch and one copy
+__global__ void k_export_many(const __grid_constant__ Soa S, const __grid_constant__ DevTables D,
+    const __grid_constant__ Cfg C, const int64_t* envs, rs_env_rec* out) {
+  const Tabs T = stage_tables(D);
+  if (threadIdx.x != 0) return;
+  const int e = (int)envs[blockIdx.x];
+  Engine E(S, T, C, e, S.blk + (size_t)e * BLK_BYTES);
+  export_env(E, C, out[blockIdx.x]);
+}
+
 __global__ void k_import(const __grid_constant__ Soa S, const __grid_constant__ DevTables D,
     const __grid_constant__ Cfg C, int e, const rs_env_rec* in) {
   const Tabs T = stage_tables(D);
@@ -1228,6 +1238,30 @@ int rs_export_env(rs_handle* h, int64_t env, rs_env_rec* out) {
   k_export<<<1, 32, smem_for(32)>>>(h->S, h->D, h->cfg, (int)env, h->rec_dev);
   CUDA_TRY(cudaGetLastError());
   CUDA_TRY(cudaMemcpy(out, h->rec_dev, sizeof(rs_env_rec), cudaMemcpyDeviceToHost));
+  return 0;
+}
+
+int rs_export_envs(rs_handle* h, const int64_t* envs, int64_t count, rs_env_rec* out) {
+  if (!h || count < 0 || (count > 0 && (!envs || !out)) || count > INT32_MAX)
+    return set_err(RS_E_ARG, "rs_export_envs: bad arguments");
+  for (int64_t i = 0; i < count; i++)
+    if (envs[i] < 0 || envs[i] >= h->n) return set_err(RS_E_ARG, "rs_export_envs: env %lld out of range", (long long)envs[i]);
+  if (count == 0) return 0;
+  CUDA_TRY(cudaSetDevice(h->device));
+  const size_t rec_bytes = (size_t)count * sizeof(rs_env_rec);
+  void* mem = nullptr;
+  CUDA_TRY(cudaMalloc(&mem, rec_bytes + (size_t)count * sizeof(int64_t)));
+  rs_env_rec* d_out = (rs_env_rec*)mem;
+  int64_t* d_envs = (int64_t*)((char*)mem + rec_bytes);
+  cudaError_t e = cudaMemcpy(d_envs, envs, (size_t)count * sizeof(int64_t), cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) {
+    k_export_many<<<(unsigned)count, 32, smem_for(32)>>>(h->S, h->D, h->cfg, d_envs, d_out);
+    e = cudaGetLastError();
+  }
+  if (e == cudaSuccess) e = cudaMemcpy(out, d_out, rec_bytes, cudaMemcpyDeviceToHost);
+  cudaError_t f = cudaFree(mem);
+  if (e == cudaSuccess) e = f;
+  if (e != cudaSuccess) return set_err((int)e, "rs_export_envs: %s", cudaGetErrorString(e));
   return 0;
 }
 

@@ -311,6 +311,15 @@ class BatchEnv:
         check(self._L.rs_export_env(self._h, int(i), C.byref(r)), "rs_export_env")
         return r
 
+    def export_many(self, envs) -> list:
+        """export() of every env in `envs` (host indices), one launch and one copy"""
+        envs = [int(i) for i in envs]
+        torch.cuda.current_stream(self.device).synchronize()
+        recs = (abi.rs_env_rec * len(envs))()
+        idx = (C.c_int64 * len(envs))(*envs)
+        check(self._L.rs_export_envs(self._h, idx, len(envs), recs), "rs_export_envs")
+        return list(recs)
+
     def load(self, i: int, rec: abi.rs_env_rec) -> None:
         torch.cuda.current_stream(self.device).synchronize()
         check(self._L.rs_import_env(self._h, int(i), C.byref(rec)), "rs_import_env")

@@ -159,12 +159,20 @@ def _wrap(config: EnvConfig, rec: abi.rs_env_rec, events, results, game_legal) -
 def init(seed: int, config: EnvConfig = EnvConfig(), device=None) -> EnvState:
     """env/core.py:81-82"""
     r = _Runner.get(config, device)
-    s = seed & _MASK64
-    r.env.init(torch.tensor([s - (1 << 64) if s >= (1 << 63) else s], dtype=torch.int64))
-    rec = r.env.export(0)
-    st = _wrap(config, rec, records.window_events(rec), (), abi.mask_to_ids(rec.legal_mask))
+    r.env.init(torch.tensor([_signed64(seed)], dtype=torch.int64))
+    st = _initial(config, r.env.export(0))
     r.current = st
     return st
+
+
+def _signed64(seed: int) -> int:
+    s = seed & _MASK64
+    return s - (1 << 64) if s >= (1 << 63) else s
+
+
+def _initial(config: EnvConfig, rec: abi.rs_env_rec) -> EnvState:
+    """the EnvState of a freshly dealt env's exported record"""
+    return _wrap(config, rec, records.window_events(rec), (), abi.mask_to_ids(rec.legal_mask))
 
 
 def step(state: EnvState, action: int) -> EnvState:
@@ -173,9 +181,24 @@ def step(state: EnvState, action: int) -> EnvState:
         raise ContractError("cannot step a finished episode")
     r = _Runner.get(state.config, None)
     r.load(state)
-    acts = torch.tensor([int(action) if -(1 << 31) <= int(action) < (1 << 31) else -1], dtype=torch.int32)
+    acts = torch.tensor([_action32(action)], dtype=torch.int32)
     r.env.step(acts)
-    rec = r.env.export(0)
+    st = _advance(state, r.env.export(0))
+    r.current = st
+    return st
+
+
+def _action32(action) -> int:
+    """an action id as the step kernel's int32; ids outside int32, and the
+    one int32 value the ABI reserves (RS_ACTION_SKIP, "not stepped"), become
+    -1 so they are illegal like any other unknown id (core.py:89-94)"""
+    a = int(action)
+    return a if -(1 << 31) < a < (1 << 31) else -1
+
+
+def _advance(state: EnvState, rec: abi.rs_env_rec) -> EnvState:
+    """the EnvState after one step of `state`, from the stepped env's
+    exported record (the event history and results extend `state`'s)"""
     old_len = int(state.record.events_len)
     new = records.window_events(rec)
     added = int(rec.events_len) - old_len
@@ -187,9 +210,7 @@ def step(state: EnvState, action: int) -> EnvState:
         results = results + (records.result_dict(rec.last_result),)
     illegal = bool(rec.status & abi.STATUS_ILLEGAL)
     game_legal = state.game_legal if illegal else abi.mask_to_ids(rec.legal_mask)
-    st = _wrap(state.config, rec, events, results, game_legal)
-    r.current = st
-    return st
+    return _wrap(state.config, rec, events, results, game_legal)
 
 
 def observe(state: EnvState, seat: int) -> Observation:

@@ -107,3 +107,91 @@ def test_session_persist_and_reload(tmp_path):
     assert again.actions == sess.actions and again.state.fingerprint() == sess.state.fingerprint()
     log = again.recorder.to_log(again.state)
     assert log["fingerprint"] == again.state.fingerprint()
+
+
+def _drive_batch(batch):
+    """every waiting human decides (the scripted human of the golden games),
+    all in one launch per tick"""
+    while True:
+        waiting = batch.waiting()
+        if not waiting:
+            return
+        batch.apply_actions({i: _human_action(batch.sessions[i].state.legal, len(batch.sessions[i].actions))
+                             for i in waiting})
+
+
+@pytest.mark.parametrize("key", [("red", "single"), ("no-red", "single"), ("no-red", "east")])
+def test_session_batch_matches_reference_and_single_sessions(key):
+    """SessionBatch: the reference's golden games of this config, multiplexed
+    with other sessions (different seeds, human seats and agent mixes) on one
+    device batch, reproduce the reference's action lists, fingerprints and
+    rewards; every other session equals the same game played alone through
+    new_session / apply_session_action / advance_agents"""
+    rule, mode = key
+    cfg = EnvConfig(rule=rule, mode=mode)
+    gold = [g for g in _cases() if (g["rule"], g["mode"]) == key]
+    extra = [(1000 + k, hs, ag) for k, (hs, ag) in enumerate([
+        ([0], {1: "random", 2: "heuristic", 3: "random"}),
+        ([], {0: "heuristic", 1: "heuristic", 2: "random", 3: "heuristic"}),
+        ([1, 2], {0: "heuristic", 3: "random"}),
+        ([0, 1, 2, 3], {}),
+        ([3], {0: "random", 1: "random", 2: "random"}),
+    ])]
+    if mode == "east":
+        extra = extra[:2]
+    spec = [(g["seed"], g["human_seats"], {int(k): v for k, v in g["agents"].items()}) for g in gold] + extra
+    batch = S.SessionBatch(cfg, [s for s, _, _ in spec], [h for _, h, _ in spec], [a for _, _, a in spec])
+    assert len(batch) == len(spec)
+    _drive_batch(batch)
+    for g, sess in zip(gold, batch.sessions):
+        assert [list(a) for a in sess.actions] == g["actions"]
+        assert sess.state.fingerprint() == g["fingerprint"]
+        assert list(sess.state.rewards) == g["rewards"]
+    for (seed, hs, ag), sess in list(zip(spec, batch.sessions))[len(gold):]:
+        alone = S.new_session(cfg, seed, hs, ag)
+        while alone.waiting_on() is not None:
+            S.apply_session_action(alone, _human_action(alone.state.legal, len(alone.actions)))
+            S.advance_agents(alone)
+        assert sess.waiting_on() is None
+        assert sess.actions == alone.actions
+        assert sess.state.fingerprint() == alone.state.fingerprint()
+        assert sess.state.rewards == alone.state.rewards and sess.state.results == alone.state.results
+        assert sess.recorder.to_log(sess.state) == alone.recorder.to_log(alone.state)
+        assert S.session_view(sess, 0)["final"] == S.session_view(alone, 0)["final"]
+
+
+def test_session_batch_contract():
+    """human decisions only for sessions waiting on a human; finished
+    sessions refuse actions; the reserved SKIP id is an illegal action on
+    the single-env facade, not a no-op"""
+    from paper_2605_20577_b200 import abi, pgx
+    cfg = EnvConfig()
+    batch = S.SessionBatch(cfg, [5, 6], [[0, 1, 2, 3], []], [{}, {0: "heuristic", 1: "random",
+                                                                  2: "heuristic", 3: "random"}])
+    assert batch.sessions[1].waiting_on() is None and batch.waiting() == {0: batch.sessions[0].waiting_on()}
+    with pytest.raises(pgx.ContractError):
+        batch.apply_actions({1: 0})
+    with pytest.raises(IndexError):
+        batch.apply_actions({2: 0})
+    st = pgx.init(5, cfg)
+    bad = pgx.step(st, abi.ACTION_SKIP)
+    assert bad.terminated and bad.record.status & abi.STATUS_ILLEGAL
+
+
+def test_export_many_matches_export():
+    """rs_export_envs: the records of a list of envs (any order, repeats)
+    equal one rs_export_env per env"""
+    import ctypes as C
+    import torch
+    from paper_2605_20577_b200.env import BatchEnv
+    env = BatchEnv(37, EnvConfig(rule="red"))
+    env.init(seed=3)
+    for _ in range(25):
+        env.step(env.random_actions(), autoreset=True)
+    order = [36, 0, 5, 5, 17, 2]
+    many = env.export_many(order)
+    for i, rec in zip(order, many):
+        assert bytes(rec) == bytes(env.export(i))
+    assert env.export_many([]) == []
+    with pytest.raises(Exception):
+        env.export_many([37])
