@@ -229,8 +229,13 @@ class rs_rollout_stats(C.Structure):
 
 
 def mask_to_ids(words) -> tuple[int, ...]:
+    m = 0
+    for i, w in enumerate(words):
+        m |= (int(w) & 0xFFFFFFFF) << (32 * i)
+    m &= (1 << NUM_ACTIONS) - 1
     out = []
-    for a in range(NUM_ACTIONS):
-        if (words[a >> 5] >> (a & 31)) & 1:
-            out.append(a)
+    while m:
+        low = m & -m
+        out.append(low.bit_length() - 1)
+        m ^= low
     return tuple(out)

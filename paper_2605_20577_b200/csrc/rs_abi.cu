@@ -1235,6 +1235,8 @@ int rs_autoreset(rs_handle* h, const rs_step_out* out, void* stream) {
 int rs_export_env(rs_handle* h, int64_t env, rs_env_rec* out) {
   if (!h || !out || env < 0 || env >= h->n) return set_err(RS_E_ARG, "rs_export_env: bad arguments");
   CUDA_TRY(cudaSetDevice(h->device));
+  // fields export_env leaves unwritten (padding, slots past the counts) read as zero
+  CUDA_TRY(cudaMemset(h->rec_dev, 0, sizeof(rs_env_rec)));
   k_export<<<1, 32, smem_for(32)>>>(h->S, h->D, h->cfg, (int)env, h->rec_dev);
   CUDA_TRY(cudaGetLastError());
   CUDA_TRY(cudaMemcpy(out, h->rec_dev, sizeof(rs_env_rec), cudaMemcpyDeviceToHost));
@@ -1254,6 +1256,7 @@ int rs_export_envs(rs_handle* h, const int64_t* envs, int64_t count, rs_env_rec*
   rs_env_rec* d_out = (rs_env_rec*)mem;
   int64_t* d_envs = (int64_t*)((char*)mem + rec_bytes);
   cudaError_t e = cudaMemcpy(d_envs, envs, (size_t)count * sizeof(int64_t), cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMemset(d_out, 0, rec_bytes);  // as rs_export_env
   if (e == cudaSuccess) {
     k_export_many<<<(unsigned)count, 32, smem_for(32)>>>(h->S, h->D, h->cfg, d_envs, d_out);
     e = cudaGetLastError();

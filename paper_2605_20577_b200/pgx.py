@@ -146,11 +146,15 @@ def _reward(config: EnvConfig, x: float, illegal: bool) -> float:
     return d
 
 
-def _wrap(config: EnvConfig, rec: abi.rs_env_rec, events, results, game_legal) -> EnvState:
+def _wrap(config: EnvConfig, rec: abi.rs_env_rec, events, results, game_legal=None) -> EnvState:
+    """game_legal None: the record's own legal ids"""
     m = _mask_int(rec.legal_mask)
     illegal = bool(rec.status & abi.STATUS_ILLEGAL)
+    legal = abi.mask_to_ids(rec.legal_mask)
+    if game_legal is None:
+        game_legal = legal
     return EnvState(config=config, current_player=int(rec.current_player),
-                    legal=abi.mask_to_ids(rec.legal_mask), legal_mask_int=m,
+                    legal=legal, legal_mask_int=m,
                     rewards=tuple(_reward(config, float(x), illegal) for x in rec.rewards),
                     terminated=bool(rec.env_terminated), truncated=bool(rec.env_truncated),
                     record=rec, events=tuple(events), results=tuple(results), game_legal=tuple(game_legal))
@@ -172,7 +176,7 @@ def _signed64(seed: int) -> int:
 
 def _initial(config: EnvConfig, rec: abi.rs_env_rec) -> EnvState:
     """the EnvState of a freshly dealt env's exported record"""
-    return _wrap(config, rec, records.window_events(rec), (), abi.mask_to_ids(rec.legal_mask))
+    return _wrap(config, rec, records.window_events(rec), ())
 
 
 def step(state: EnvState, action: int) -> EnvState:
@@ -200,16 +204,15 @@ def _advance(state: EnvState, rec: abi.rs_env_rec) -> EnvState:
     """the EnvState after one step of `state`, from the stepped env's
     exported record (the event history and results extend `state`'s)"""
     old_len = int(state.record.events_len)
-    new = records.window_events(rec)
     added = int(rec.events_len) - old_len
     if added > abi.EVENT_WINDOW:
         raise RuntimeError("more than 64 events in one step")
-    events = state.events + tuple(new[len(new) - added:]) if added > 0 else state.events
+    events = state.events + tuple(records.window_events(rec, added)) if added > 0 else state.events
     results = state.results
     if rec.n_results > state.record.n_results:
         results = results + (records.result_dict(rec.last_result),)
     illegal = bool(rec.status & abi.STATUS_ILLEGAL)
-    game_legal = state.game_legal if illegal else abi.mask_to_ids(rec.legal_mask)
+    game_legal = state.game_legal if illegal else None
     return _wrap(state.config, rec, events, results, game_legal)
 
 

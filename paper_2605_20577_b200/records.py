@@ -209,6 +209,9 @@ def internal_fields(rec) -> dict:
     }
 
 
-def window_events(rec) -> list[tuple[int, int, int]]:
+def window_events(rec, last: int | None = None) -> list[tuple[int, int, int]]:
+    """the events in the record's window (the `last` ones only, if given)"""
     n = min(int(rec.events_len), abi.EVENT_WINDOW)
-    return [(int(rec.events[i][0]), int(rec.events[i][1]), int(rec.events[i][2])) for i in range(n)]
+    ev = rec.events
+    return [(int(e[0]), int(e[1]), int(e[2])) for e in
+            (ev[i] for i in range(n - min(n, last) if last is not None else 0, n))]
