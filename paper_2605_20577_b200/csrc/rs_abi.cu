@@ -695,6 +695,8 @@ struct rs_handle {
   size_t mem_bytes;
   uint32_t* legal_bits_tmp;  // step output when the caller asks only for bools
   rs_env_rec* rec_dev;
+  void* export_buf = nullptr;  // rs_export_envs: records + env list, grown on demand
+  size_t export_cap = 0;
   int num_sms;
   int occ_key[16], occ_val[16];  // resident stepping-kernel CTAs per SM per (block, smem)
   // stepping kernels on a shared-memory stage (RINSHAN_STAGE): 0 = never
@@ -1066,6 +1068,7 @@ int rs_destroy(rs_handle* h) {
   cudaSetDevice(h->device);
   cudaFree(h->mem);
   cudaFree(h->sort_tmp);
+  cudaFree(h->export_buf);
   delete h;
   return 0;
 }
@@ -1251,10 +1254,16 @@ int rs_export_envs(rs_handle* h, const int64_t* envs, int64_t count, rs_env_rec*
   if (count == 0) return 0;
   CUDA_TRY(cudaSetDevice(h->device));
   const size_t rec_bytes = (size_t)count * sizeof(rs_env_rec);
-  void* mem = nullptr;
-  CUDA_TRY(cudaMalloc(&mem, rec_bytes + (size_t)count * sizeof(int64_t)));
-  rs_env_rec* d_out = (rs_env_rec*)mem;
-  int64_t* d_envs = (int64_t*)((char*)mem + rec_bytes);
+  const size_t need = rec_bytes + (size_t)count * sizeof(int64_t);
+  if (need > h->export_cap) {
+    CUDA_TRY(cudaFree(h->export_buf));
+    h->export_buf = nullptr;
+    h->export_cap = 0;
+    CUDA_TRY(cudaMalloc(&h->export_buf, need));
+    h->export_cap = need;
+  }
+  rs_env_rec* d_out = (rs_env_rec*)h->export_buf;
+  int64_t* d_envs = (int64_t*)((char*)h->export_buf + rec_bytes);
   cudaError_t e = cudaMemcpy(d_envs, envs, (size_t)count * sizeof(int64_t), cudaMemcpyHostToDevice);
   if (e == cudaSuccess) e = cudaMemset(d_out, 0, rec_bytes);  // as rs_export_env
   if (e == cudaSuccess) {
@@ -1262,8 +1271,6 @@ int rs_export_envs(rs_handle* h, const int64_t* envs, int64_t count, rs_env_rec*
     e = cudaGetLastError();
   }
   if (e == cudaSuccess) e = cudaMemcpy(out, d_out, rec_bytes, cudaMemcpyDeviceToHost);
-  cudaError_t f = cudaFree(mem);
-  if (e == cudaSuccess) e = f;
   if (e != cudaSuccess) return set_err((int)e, "rs_export_envs: %s", cudaGetErrorString(e));
   return 0;
 }
