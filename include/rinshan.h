@@ -29,6 +29,9 @@
  *                                              launch + one copy; service/sessions.py
  *                                              state reads, batched sessions)
  *   rs_import_env     tests/engine_helpers.py:58-105 craft() (crafted states)
+ *   rs_debug_score    scoring/score.py:45-82   score_win(ctx, kazoe, double_yakuman)
+ *                                              over WinContext (scoring/context.py:19-57),
+ *                                              the device scorer alone (parity harness)
  *
  * Error convention: every function returns 0 on success, a negative RS_E*
  * code on contract violations and a positive cudaError_t value when a CUDA
@@ -363,6 +366,35 @@ int rs_export_env(rs_handle* h, int64_t env, rs_env_rec* out);
  * for the device like rs_export_env */
 int rs_export_envs(rs_handle* h, const int64_t* envs, int64_t count, rs_env_rec* out);
 int rs_import_env(rs_handle* h, int64_t env, const rs_env_rec* in);
+/* WinContext (scoring/context.py:19-57) as plain data: the parity
+ * harness's input to the device scorer.  `concealed` counts include the
+ * winning tile; `ids` lists concealed plus meld tile ids (red fives and
+ * dora are counted over them, scoring/dora.py:9-22). */
+typedef struct rs_winctx {
+  uint8_t concealed[34];
+  int32_t n_melds;
+  rs_meld_rec melds[4];
+  int32_t win_tile;
+  int32_t tsumo; /* 1 tsumo, 0 ron */
+  int32_t seat_wind, round_wind; /* 27..30 */
+  int32_t n_ids;
+  uint8_t ids[18];
+  int32_t riichi, ippatsu, last_tile, rinshan, chankan, first_draw;
+  int32_t n_dora;
+  uint8_t dora[5];
+  int32_t n_ura;
+  uint8_t ura[5];
+  int32_t rule;
+  int32_t kazoe, double_yakuman;
+} rs_winctx;
+
+/* score_win (scoring/score.py:45-82) of count contexts (host arrays) on
+ * the device: the engine's own scorer (rs_score.cuh score_win, the result
+ * record's win entry as settlements write it) in one kernel, one thread
+ * per context.  ok[i] = 1 when scored, 0 on NoYakuError (out[i] zeroed).
+ * Test and parity entry point; synchronous. */
+int rs_debug_score(const rs_winctx* ctx, int64_t count, rs_win_rec* out, int32_t* ok, int32_t device);
+
 /* sizeof of the records above, for binding checks: config, meld, hand,
  * win, result, env, step */
 int rs_record_sizes(int32_t* out /*[7]*/);

@@ -98,31 +98,8 @@ class orc_obs(C.Structure):
     ]
 
 
-class orc_winctx(C.Structure):
-    _fields_ = [
-        ("concealed", C.c_uint8 * 34),
-        ("n_melds", C.c_int32),
-        ("melds", abi.rs_meld_rec * 4),
-        ("win_tile", C.c_int32),
-        ("tsumo", C.c_int32),
-        ("seat_wind", C.c_int32),
-        ("round_wind", C.c_int32),
-        ("n_ids", C.c_int32),
-        ("ids", C.c_uint8 * 18),
-        ("riichi", C.c_int32),
-        ("ippatsu", C.c_int32),
-        ("last_tile", C.c_int32),
-        ("rinshan", C.c_int32),
-        ("chankan", C.c_int32),
-        ("first_draw", C.c_int32),
-        ("n_dora", C.c_int32),
-        ("dora", C.c_uint8 * 5),
-        ("n_ura", C.c_int32),
-        ("ura", C.c_uint8 * 5),
-        ("rule", C.c_int32),
-        ("kazoe", C.c_int32),
-        ("double_yakuman", C.c_int32),
-    ]
+# the oracle's orc_winctx (mjoracle.h) has rs_winctx's layout (include/rinshan.h)
+orc_winctx = abi.rs_winctx
 
 
 def make_config(rule="red", mode="single", illegal_penalty=-1.0, reward_scheme="score_delta",

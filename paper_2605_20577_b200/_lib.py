@@ -28,6 +28,7 @@ SYMBOLS = (
     "rs_num_envs", "rs_state_bytes", "rs_init", "rs_init_indexed", "rs_step", "rs_step_ex", "rs_step_rec_out",
     "rs_observe",
     "rs_policy_random", "rs_policy_heuristic", "rs_rollout", "rs_rollout_policy", "rs_autoreset", "rs_check_invariants", "rs_export_env", "rs_export_envs", "rs_import_env", "rs_record_sizes", "rs_debug_rollout_cycles",
+    "rs_debug_score",
 )
 
 _lib = None
@@ -96,6 +97,7 @@ def lib():
         L.rs_import_env.argtypes = [vp, i64, vp]
         L.rs_record_sizes.argtypes = [vp]
         L.rs_debug_rollout_cycles.argtypes = [vp, i32, vp, vp, vp]
+        L.rs_debug_score.argtypes = [vp, i64, vp, vp, i32]
         if L.rs_abi_version() != 1:
             raise RinshanError("ABI version mismatch between _rinshan.so and the Python layer")
         _lib = L
@@ -117,3 +119,15 @@ def record_sizes() -> list[int]:
 def ctypes_record_sizes() -> list[int]:
     return [C.sizeof(t) for t in (abi.rs_config, abi.rs_meld_rec, abi.rs_hand_rec,
                                   abi.rs_win_rec, abi.rs_result_rec, abi.rs_env_rec, abi.rs_step_rec)]
+
+
+def debug_score(ctxs, device: int = 0) -> list:
+    """score_win (scoring/score.py:45-82) of abi.rs_winctx contexts on the
+    device (rs_debug_score): a list of abi.rs_win_rec, None where the
+    reference raises NoYakuError."""
+    n = len(ctxs)
+    arr = (abi.rs_winctx * max(n, 1))(*ctxs)
+    out = (abi.rs_win_rec * max(n, 1))()
+    ok = (C.c_int32 * max(n, 1))()
+    check(lib().rs_debug_score(arr, n, out, ok, device), "rs_debug_score")
+    return [out[i] if ok[i] else None for i in range(n)]

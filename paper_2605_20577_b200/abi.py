@@ -106,6 +106,34 @@ class rs_win_rec(C.Structure):
     ]
 
 
+class rs_winctx(C.Structure):
+    """include/rinshan.h rs_winctx: WinContext (scoring/context.py:19-57)"""
+    _fields_ = [
+        ("concealed", C.c_uint8 * 34),
+        ("n_melds", C.c_int32),
+        ("melds", rs_meld_rec * 4),
+        ("win_tile", C.c_int32),
+        ("tsumo", C.c_int32),
+        ("seat_wind", C.c_int32),
+        ("round_wind", C.c_int32),
+        ("n_ids", C.c_int32),
+        ("ids", C.c_uint8 * 18),
+        ("riichi", C.c_int32),
+        ("ippatsu", C.c_int32),
+        ("last_tile", C.c_int32),
+        ("rinshan", C.c_int32),
+        ("chankan", C.c_int32),
+        ("first_draw", C.c_int32),
+        ("n_dora", C.c_int32),
+        ("dora", C.c_uint8 * 5),
+        ("n_ura", C.c_int32),
+        ("ura", C.c_uint8 * 5),
+        ("rule", C.c_int32),
+        ("kazoe", C.c_int32),
+        ("double_yakuman", C.c_int32),
+    ]
+
+
 class rs_result_rec(C.Structure):
     _fields_ = [
         ("kyoku", C.c_int32),

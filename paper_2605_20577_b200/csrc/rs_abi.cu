@@ -683,6 +683,59 @@ __global__ void k_import(const __grid_constant__ Soa S, const __grid_constant__ 
   import_env(E, *in);
 }
 
+// score_win over WinContext records (rs_debug_score): the WinIn the
+// engine's win_input builds from a state, built here from the context
+// (scoring/context.py:19-57, dora parts as scoring/dora.py:9-22 counts them
+// over all_tile_ids), then the engine's scorer and result-record writer
+__global__ void k_debug_score(const rs_winctx* ctx, int64_t count, rs_win_rec* out, int32_t* ok) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= count) return;
+  const rs_winctx& c = ctx[i];
+  WinIn w;
+  for (int j = 0; j < 5; j++) w.conc.c[j] = 0;
+  for (int k = 0; k < 34; k++) w.conc.add(k, c.concealed[k]);
+  w.nmelds = c.n_melds;
+  w.closed = true;
+  for (int m = 0; m < 4; m++) {
+    w.mtype[m] = m < c.n_melds ? c.melds[m].type : 0;
+    w.mbase[m] = m < c.n_melds ? c.melds[m].tiles[0] >> 2 : 0;
+    if (m < c.n_melds && c.melds[m].type != M_KAN_CLOSED) w.closed = false;
+  }
+  w.win_kind = c.win_tile >> 2;
+  w.tsumo = c.tsumo != 0;
+  w.seat_wind = c.seat_wind;
+  w.round_wind = c.round_wind;
+  w.riichi = c.riichi;
+  w.ippatsu = c.ippatsu != 0;
+  w.last_tile = c.last_tile != 0;
+  w.rinshan = c.rinshan != 0;
+  w.chankan = c.chankan != 0;
+  w.first_draw = c.first_draw != 0;
+  Counts all;
+  for (int j = 0; j < 5; j++) all.c[j] = 0;
+  int reds = 0;
+  for (int j = 0; j < c.n_ids; j++) {
+    all.add(c.ids[j] >> 2, 1);
+    if (c.rule == RS_RULE_RED && is_red_tile(c.ids[j])) reds++;
+  }
+  int dora = 0, ura = 0;
+  for (int j = 0; j < c.n_dora; j++) dora += all.get(dora_kind(c.dora[j] >> 2));
+  if (c.riichi)
+    for (int j = 0; j < c.n_ura; j++) ura += all.get(dora_kind(c.ura[j] >> 2));
+  w.dora = dora;
+  w.ura = ura;
+  w.reds = reds;
+  w.kazoe = c.kazoe != 0;
+  w.double_yakuman = c.double_yakuman != 0;
+  Reading r;
+  rs_win_rec rec;
+  memset(&rec, 0, sizeof(rec));
+  const bool scored = score_win(w, r, false);
+  if (scored) fill_win_rec(rec, r, w);
+  out[i] = rec;
+  ok[i] = scored ? 1 : 0;
+}
+
 }  // namespace
 
 struct rs_handle {
@@ -1284,6 +1337,37 @@ int rs_import_env(rs_handle* h, int64_t env, const rs_env_rec* in) {
   CUDA_TRY(cudaGetLastError());
   CUDA_TRY(cudaDeviceSynchronize());
   return 0;
+}
+
+int rs_debug_score(const rs_winctx* ctx, int64_t count, rs_win_rec* out, int32_t* ok, int32_t device) {
+  if (count < 0 || (count && (!ctx || !out || !ok))) return set_err(RS_E_ARG, "bad rs_debug_score arguments");
+  if (!count) return 0;
+  for (int64_t i = 0; i < count; i++) {
+    const rs_winctx& c = ctx[i];
+    if (c.n_melds < 0 || c.n_melds > 4 || c.n_ids < 0 || c.n_ids > 18 || c.n_dora < 0 || c.n_dora > 5 ||
+        c.n_ura < 0 || c.n_ura > 5 || c.win_tile < 0 || c.win_tile >= RS_NUM_TILES)
+      return set_err(RS_E_ARG, "rs_winctx field out of range");
+  }
+  const DeviceScope device_scope(device);
+  rs_winctx* dctx = nullptr;
+  rs_win_rec* dout = nullptr;
+  int32_t* dok = nullptr;
+  int rc = 0;
+  cudaError_t e = cudaMalloc(&dctx, sizeof(rs_winctx) * count);
+  if (e == cudaSuccess) e = cudaMalloc(&dout, sizeof(rs_win_rec) * count);
+  if (e == cudaSuccess) e = cudaMalloc(&dok, sizeof(int32_t) * count);
+  if (e == cudaSuccess) e = cudaMemcpy(dctx, ctx, sizeof(rs_winctx) * count, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) {
+    k_debug_score<<<(unsigned)((count + 127) / 128), 128>>>(dctx, count, dout, dok);
+    e = cudaGetLastError();
+  }
+  if (e == cudaSuccess) e = cudaMemcpy(out, dout, sizeof(rs_win_rec) * count, cudaMemcpyDeviceToHost);
+  if (e == cudaSuccess) e = cudaMemcpy(ok, dok, sizeof(int32_t) * count, cudaMemcpyDeviceToHost);
+  if (e != cudaSuccess) rc = set_err((int)e, cudaGetErrorString(e));
+  cudaFree(dctx);
+  cudaFree(dout);
+  cudaFree(dok);
+  return rc;
 }
 
 int rs_record_sizes(int32_t* out /*[7]*/) {

@@ -528,25 +528,8 @@ struct Engine {
     rs_result_rec& r = result();
     for (int s = 0; s < 4; s++) r.scores_after[s] = g.scores[s];
   }
-  RS_COLD void write_win(int i, const Reading& rd, const WinIn& w) const {
-    rs_win_rec& x = result().wins[i];
-    for (int id = 0; id < 40; id++) {
-      int han = 0;
-      if ((rd.mask >> id) & 1) {
-        if (rd.yakuman) han = ((rd.x2 >> id) & 1) ? 2 : 1;
-        else han = yaku_han_of(id, rd.form == 1 ? true : w.closed);
-      }
-      x.yaku_han[id] = (int8_t)han;
-    }
-    x.yakuman = rd.yakuman;
-    x.han = rd.han;
-    x.fu = rd.fu;
-    x.base = rd.base;
-    x.dora = w.dora;
-    x.ura = w.ura;
-    x.reds = w.reds;
-    x.form = rd.form;
-  }
+  RS_COLD void write_win(int i, const Reading& rd, const WinIn& w) const { fill_win_rec(result().wins[i], rd, w); }
+
 
   RS_HD int final_kyoku() const { return C.mode == RS_MODE_SINGLE ? 0 : (C.mode == RS_MODE_EAST ? 3 : 7); }
   RS_HD void end_game() {

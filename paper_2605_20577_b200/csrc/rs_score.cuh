@@ -10,6 +10,7 @@
 // masks (+ a mask of ids counted twice), so a reading needs no arrays.
 #pragma once
 
+#include "../../include/rinshan.h"
 #include "rs_common.cuh"
 
 namespace rs {
@@ -425,6 +426,28 @@ RS_COLD bool score_win(const WinIn& w, Reading& best, bool first_only) {
     }
   }
   return found;
+}
+
+// WinScore (score.py:23-32) as the result record's per-win entry: han per
+// yaku id (yakuman multiplicity for yakuman hands), the reading's totals and
+// the dora parts of the win context
+RS_HD void fill_win_rec(rs_win_rec& x, const Reading& rd, const WinIn& w) {
+  for (int id = 0; id < 40; id++) {
+    int han = 0;
+    if ((rd.mask >> id) & 1) {
+      if (rd.yakuman) han = ((rd.x2 >> id) & 1) ? 2 : 1;
+      else han = yaku_han_of(id, rd.form == 1 ? true : w.closed);
+    }
+    x.yaku_han[id] = (int8_t)han;
+  }
+  x.yakuman = rd.yakuman;
+  x.han = rd.han;
+  x.fu = rd.fu;
+  x.base = rd.base;
+  x.dora = w.dora;
+  x.ura = w.ura;
+  x.reds = w.reds;
+  x.form = rd.form;
 }
 
 // settle (points.py:56-86)

@@ -11,10 +11,14 @@ Writes small, deterministic JSON(.gz) files next to this script:
   tables.json       suit-table blob CRC / sha256 and sampled value rows
   shanten.json.gz   random hands (with melds) -> shanten, waits
   scoring.json.gz   the reference's 38 GOLDEN_CASES + random wins -> score_win
+  scoring_rare.json.gz  yakuman / double-yakuman waits / kazoe hands under
+                    every (kazoe, double_yakuman) flag pair -> score_win
   traces.json.gz    full games (random / heuristic policies, both rules, all
                     modes): per step the action, legal ids, current player,
                     rewards and the sha256 state fingerprint prefix
                     (engine/state.py:276-278) and observation digest
+  wins.json.gz      tsumo / ron transitions of states crafted around the
+                    scoring fixtures' hands (settlement + result record)
   logs.json.gz      mjlog-lite-v1 logs (engine/log.py) of the bench loop's
                     games, canonical JSON
   renders.json.gz   render/svg.py documents (sha256) of reference states
@@ -222,6 +226,322 @@ def make_scoring():
         cases.append({"ctx": ctx_to_json(ctx), "kazoe": kz, "dy": dy, "want": score_json(ctx, kz, dy)})
         made += 1
     dump("scoring.json.gz", cases)
+
+
+# rare scoring branches the reference's fixtures above barely reach:
+# counted yakuman (kazoe) and the double-yakuman waits, each under every
+# (kazoe, double_yakuman) combination (engine/types.py:53-54)
+RARE_HANDS = [
+    # (concealed-13, win, type, melds, ctx kwargs)
+    ("19m19p19s1234567z", "9m", "tsumo", (), {}),                      # kokushi 13-sided
+    ("19m19p19s1234567z", "1z", "ron", (), {}),                        # kokushi 13-sided, ron
+    ("119m19p19s123456z", "7z", "ron", (), {}),                        # kokushi single wait
+    ("19m19p19s1234567z", "7z", "tsumo", (), {"seat_wind": 27, "is_first_uninterrupted_draw": True}),
+    ("19m19p19s1234567z", "1m", "tsumo", (), {"seat_wind": 28, "is_first_uninterrupted_draw": True}),
+    ("1112345678999m", "5m", "tsumo", (), {}),                          # chuuren 9-sided
+    ("1112345678999p", "9p", "ron", (), {}),                            # chuuren 9-sided on a terminal
+    ("1112345678999s", "1s", "tsumo", (), {"seat_wind": 27, "is_first_uninterrupted_draw": True}),
+    ("1112345678899m", "9m", "ron", (), {}),                            # chuuren, not 9-sided
+    ("111m999m111s999s1p", "1p", "tsumo", (), {}),                      # suuankou tanki
+    ("111m999m111s999s1p", "1p", "ron", (), {}),                        # suuankou tanki, ron
+    ("111m999m111s99s11p", "1p", "tsumo", (), {}),                      # suuankou shanpon
+    ("111m999m111s99s11p", "9s", "ron", (), {}),                        # sanankou only (ron)
+    ("111z222z333z444z5m", "5m", "ron", (), {}),                        # daisuushii + suuankou tanki
+    ("111z222z333z44z55m", "5m", "tsumo", (), {}),                      # shousuushi + suuankou
+    ("111z222z333z44z55m", "4z", "ron", (), {}),                        # daisuushii shanpon (ron)
+    ("222z333z44z55m", "4z", "ron", ("pon", 27), {}),                   # daisuushii with a pon
+    ("555z666z77z123m99p", "7z", "ron", (), {}),                        # daisangen
+    ("111z222z555z66z77z", "7z", "tsumo", (), {}),                      # tsuuiisou + suuankou
+    ("1122z3344z5566z7z", "7z", "ron", (), {}),                         # tsuuiisou seven pairs
+    ("111m999m111p99p11s", "1s", "ron", (), {}),                        # chinroutou
+    ("223344s666s888s6z", "6z", "tsumo", (), {}),                       # ryuuiisou
+    ("2m", "2m", "tsumo", ("kans",), {}),                               # suukantsu
+    ("123m456m789m11m23m", "4m", "tsumo", (),                           # kazoe: 13+ han
+     {"riichi": 1, "ippatsu": True, "dora_indicators": (32, 33), "ura_indicators": (34,)}),
+    ("123m456m789m11m23m", "4m", "ron", (),                             # 11-12 han
+     {"riichi": 1, "dora_indicators": (32,)}),
+    ("11223355577799p", "", "tsumo", (),                                # chinitsu seven pairs
+     {"riichi": 2, "ippatsu": True, "dora_indicators": (4 * 9 + 3,)}),
+    ("234m456p888s44m67p", "8p", "tsumo", (), {"seat_wind": 27, "is_first_uninterrupted_draw": True}),
+    ("234m456p888s44m67p", "5p", "tsumo", (), {"seat_wind": 29, "is_first_uninterrupted_draw": True}),
+    ("1122m4455p88s33z5z", "5z", "tsumo", (), {"seat_wind": 30, "is_first_uninterrupted_draw": True}),
+    ("234m456p888s44m67p", "8p", "tsumo", (), {"is_rinshan": True, "dora_indicators": (0, 4, 8, 12, 16)}),
+    ("234m456p888s44m67p", "8p", "ron", (), {"is_chankan": True, "is_last_tile": False}),
+    ("234m456p888s44m67p", "8p", "ron", (), {"is_last_tile": True, "riichi": 2, "ippatsu": True}),
+    ("123456789m1234p", "1p", "ron", (), {"rule": 1}),                # no-red rule
+    ("234m406p888s44m67p", "8p", "tsumo", (), {"reds": (13,)}),       # red five held
+    ("234m456p44m67p", "8p", "tsumo", ("ckan", 26), {"is_rinshan": True}),  # rinshan after a kan
+    ("234m456p44m67p", "5p", "tsumo", ("ckan", 31), {"is_rinshan": True, "riichi": 1}),
+]
+
+
+def rare_ctx(hand, win, wtype, melds, kw):
+    import test_scoring as TS
+    from mjsim.melds import KAN_CLOSED as KC
+
+    kw = dict(kw)
+    reds = kw.pop("reds", ())
+    ml = ()
+    if melds and melds[0] == "pon":
+        ml = (TS.pon(melds[1]),)
+    elif melds and melds[0] == "ckan":
+        ml = (TS.kan(melds[1], KC),)
+    elif melds and melds[0] == "kans":
+        ml = (TS.kan(4, KC), TS.kan(13, KC), TS.kan(22), TS.kan(31))
+    if not win:  # 14-tile text: the last tile wins
+        counts, _ = __import__("oracle").parse_hand(hand)
+        win_kind = max(k for k in range(34) if counts[k])
+        hand = hand  # keep the text; make_ctx adds the win kind, so drop it here
+        digits = {"m": 0, "p": 9, "s": 18, "z": 27}
+        suit = next(s for s, b in digits.items() if b <= win_kind < b + 9)
+        win = f"{win_kind - digits[suit] + 1}{suit}"
+        body, sfx = hand[:-1], hand[-1]
+        i = body.rindex(win[0])
+        hand = body[:i] + body[i + 1:] + sfx
+    return TS.make_ctx(hand, win, wtype, melds=ml, reds=reds, **kw)
+
+
+def make_scoring_rare():
+    cases = []
+    for hand, win, wtype, melds, kw in RARE_HANDS:
+        ctx = rare_ctx(hand, win, wtype, melds, kw)
+        for kz in (False, True):
+            for dy in (False, True):
+                cases.append({"ctx": ctx_to_json(ctx), "kazoe": kz, "dy": dy, "want": score_json(ctx, kz, dy)})
+    dump("scoring_rare.json.gz", cases)
+
+
+# wins through the engine: states crafted around the scoring fixtures'
+# hands (winner, seat / round wind, melds, riichi / ippatsu, dora and ura
+# indicators in the dead wall, haitei / houtei, rinshan, chankan, first
+# draw, honba, deposits, kazoe / double-yakuman configs), then TSUMO on the
+# winner's draw or RON on an opponent's discard / added kan, recorded like
+# the scenarios above: (pre-state record, action, post-state projection |
+# exception).  The post state carries the settled scores and the result
+# record with the win details; in half mode the next kyoku is dealt.
+
+def craft_win(c, kazoe, dy, rnd):
+    """GameState for a fixture context (ctx_to_json form) or None"""
+    from mjsim.engine.engine import _B, _finish
+    from mjsim.engine.state import make_hand
+    from mjsim.engine.types import MODE_HALF, PH_ACT, GameConfig, GameState, RiverTile
+    from mjsim.melds import KAN_CLOSED as KC
+    from mjsim.melds import PON as PN
+    from mjsim.rng import seed_state
+    from mjsim.tiles import Wall
+
+    melds = [Meld(t, tuple(ts), cal, frm) for t, ts, cal, frm in c["melds"]]
+    meld_ids = [t for m in melds for t in m.tiles]
+    conc = [t for t in c["ids"] if t not in meld_ids]
+    win = c["win_tile"]
+    if win not in conc:
+        same = [t for t in conc if t >> 2 == win >> 2]
+        if not same or win in meld_ids:
+            return None
+        conc[conc.index(same[0])] = win
+    tsumo = c["tsumo"]
+    chankan, rinshan, last, first = c["chankan"], c["rinshan"], c["last_tile"], c["first_draw"]
+    riichi = c["riichi"]
+    kans = sum(1 for m in melds if m.type in (2, 3, 4))
+    if rinshan and not kans:
+        return None
+    if first and (riichi or melds or not tsumo):
+        return None
+    if len(set(conc + meld_ids)) != len(conc) + len(meld_ids):
+        return None
+    kyoku = (c["round_wind"] - 27) * 4 + rnd.randrange(4)
+    dealer = kyoku % 4
+    winner = (dealer + c["seat_wind"] - 27) % 4
+    # open melds were called from someone: chi from the left, others anyone
+    melds = [m if m.type == KC else Meld(m.type, m.tiles, m.tiles[0] if m.called_tile < 0 else m.called_tile,
+                                         (winner + 3) % 4 if m.type == 0 else (winner + 1 + rnd.randrange(3)) % 4)
+             for m in melds]
+    used = set(conc) | set(meld_ids)
+    hands = [None] * 4
+    discarder = None
+    disc_pon = None
+    if not tsumo:
+        discarder = (winner + 1 + rnd.randrange(3)) % 4
+        conc.remove(win)
+        if chankan:
+            others = [4 * (win >> 2) + j for j in range(4) if 4 * (win >> 2) + j != win]
+            if any(t in used for t in others):
+                return None
+            used |= set(others)
+            disc_pon = Meld(PN, tuple(sorted(others)), others[0], (discarder + 2) % 4)
+    free = [t for t in range(136) if t not in used]
+    rnd.shuffle(free)
+
+    def take(pred=lambda t: True):
+        for i, t in enumerate(free):
+            if pred(t):
+                return free.pop(i)
+        return None
+
+    # dead wall: dora indicators (slot 122 + 2i) and ura (123 + 2i)
+    n_dora = min(5, max(len(c["dora"]), 1 + kans))
+    dora, ura = [], []
+    for i in range(n_dora):
+        d = take(lambda t: t >> 2 == c["dora"][i] >> 2) if i < len(c["dora"]) else take()
+        u = take(lambda t: t >> 2 == c["ura"][i] >> 2) if i < len(c["ura"]) else None
+        u = u if u is not None else take()
+        if d is None or u is None:
+            return None
+        dora.append(d)
+        ura.append(u)
+    # hands: winner's from the context, opponents' random
+    wh = make_hand(conc, melds=tuple(melds))
+    wait_kinds = set(wh.waits) | {win >> 2}
+    for s in range(4):
+        if s == winner:
+            continue
+        n = 13
+        if s == discarder and disc_pon is not None:
+            n = 10
+        hs = [take(lambda t: t >> 2 not in wait_kinds or s != discarder) for _ in range(n)]
+        if None in hs:
+            return None
+        hands[s] = hs
+    drawn = win if tsumo else -1
+    actor = winner if tsumo else discarder
+    if not tsumo:
+        hands[discarder] = hands[discarder] + [win]
+        drawn = win
+    # rivers: the winner's avoids its waits (furiten); riichi needs a
+    # declaration discard; haitei / houtei fill the rivers up to the last tile
+    rivers = [[] for _ in range(4)]
+    wr = 0 if first else (rnd.randint(1, 3) if (riichi or not melds or rnd.random() < 0.5) else 0)
+    if riichi and wr == 0:
+        wr = 1
+    for _ in range(wr):
+        t = take(lambda t: t >> 2 not in wait_kinds)
+        if t is None:
+            return None
+        rivers[winner].append(t)
+    in_play = sum(len(h) for h in hands if h) + len(conc) + len(meld_ids) + \
+        (len(disc_pon.tiles) if disc_pon else 0) + wr
+    target = (122 - kans if last else in_play + rnd.randint(0, 30)) + kans
+    if first:
+        target = in_play
+    seat_cycle = [s for s in range(4) if s != winner]
+    k = 0
+    while in_play < target:
+        s = seat_cycle[k % 3]
+        k += 1
+        if len(rivers[s]) >= 30:
+            if all(len(rivers[x]) >= 30 for x in seat_cycle):
+                return None
+            continue
+        t = take()
+        if t is None:
+            return None
+        rivers[s].append(t)
+        in_play += 1
+    cursor = in_play - kans
+    if cursor > 122 - kans:
+        return None
+    front = [t for h in hands if h for t in h] + conc + meld_ids + (list(disc_pon.tiles) if disc_pon else []) + \
+        [t for r in rivers for t in r]
+    assert len(front) == in_play
+    rnd.shuffle(front)
+    tail = front[cursor:]
+    front = front[:cursor]
+    live = free[:]  # whatever is left goes to the live wall and dead wall rest
+    wall = front + live[: 122 - cursor]  # [122 - kans, 122) are never drawn
+    live = live[122 - cursor:]
+    dead = [None] * 14
+    for i in range(n_dora):
+        dead[2 * i], dead[2 * i + 1] = dora[i], ura[i]
+    rest = [x for x in live]
+    for i in range(14 - kans):
+        if dead[i] is None:
+            dead[i] = rest.pop()
+    for i in range(kans):
+        dead[13 - i] = tail[i]
+    wall += dead
+    assert sorted(wall) == list(range(136)), (len(wall), len(set(wall)))
+    hs = []
+    for s in range(4):
+        riv = tuple(RiverTile(t, False, riichi and s == winner and i == 0, False) for i, t in enumerate(rivers[s]))
+        if s == winner:
+            hs.append(make_hand(conc + ([] if tsumo else []), melds=tuple(melds), river=riv, riichi=riichi,
+                                riichi_index=0 if riichi else -1, ippatsu=bool(c["ippatsu"] and riichi)))
+        else:
+            hs.append(make_hand(hands[s], melds=(disc_pon,) if (s == discarder and disc_pon) else (), river=riv))
+    deposits = rnd.randint(0, 2) + (1 if riichi else 0)
+    scores = [25000] * 4
+    if riichi:
+        scores[winner] -= 1000
+    for _ in range(deposits - (1 if riichi else 0)):
+        scores[rnd.randrange(4)] -= 1000
+    cfg = GameConfig(rule=c["rule"], mode=MODE_HALF, kazoe=kazoe, double_yakuman=dy)
+    template = GameState(
+        config=cfg, wall=Wall(tiles=tuple(wall), cursor=cursor, kan_draws=kans, dora_count=n_dora),
+        hands=tuple(hs), scores=tuple(scores), kyoku=kyoku, honba=rnd.randint(0, 3), deposits=deposits,
+        phase=PH_ACT, actor=actor, drawn=drawn, rinshan_pending=bool(rinshan), rng=seed_state(rnd.randrange(1 << 30)),
+        any_call_made=bool(melds and any(m.type != KC for m in melds)) or disc_pon is not None)
+    return _finish(_B(template)), winner, discarder, disc_pon
+
+
+def make_wins():
+    import test_scoring as TS
+    from mjsim import actions as A
+    from mjsim.engine.engine import apply_action
+
+    srcs = []
+    for hand, win, wtype, melds, kw, _ in TS.GOLDEN_CASES:
+        srcs.append(("golden", ctx_to_json(TS.make_ctx(hand, win, wtype, melds=melds, **kw)), False, False))
+    for hand, win, wtype, melds, kw in RARE_HANDS:
+        cj = ctx_to_json(rare_ctx(hand, win, wtype, melds, kw))
+        for kz in (False, True):
+            for dy in (False, True):
+                srcs.append(("rare", cj, kz, dy))
+    for case in json.loads(gzip.open(HERE / "scoring.json.gz").read())[38::2]:
+        srcs.append(("random", case["ctx"], case["kazoe"], case["dy"]))
+    rnd = random.Random(0x5EED)
+    out = []
+    stats = {}
+
+    def record(tag, pre, action):
+        try:
+            post, err = state_projection(apply_action(pre, action)), None
+        except Exception as e:  # IllegalActionError
+            post, err = None, type(e).__name__
+        out.append({"test": tag, "pre": state_record(pre), "action": int(action), "post": post, "error": err})
+        stats[(tag, err)] = stats.get((tag, err), 0) + 1
+
+    for tag, cj, kz, dy in srcs:
+        made = None
+        for _ in range(4):
+            made = craft_win(cj, kz, dy, rnd)
+            if made is not None:
+                break
+        if made is None:
+            stats[(tag, "skipped")] = stats.get((tag, "skipped"), 0) + 1
+            continue
+        st, winner, discarder, disc_pon = made
+        if cj["tsumo"]:
+            record(tag, st, A.TSUMO)
+            continue
+        kind = cj["win_tile"] >> 2
+        if disc_pon is not None:
+            act = A.KAN_ADDED_BASE + kind
+        elif cj["rule"] == 0 and cj["win_tile"] in (16, 52, 88):
+            act = A.RED_ACTION_BY_KIND[kind]
+        else:
+            act = kind
+        if not (st.legal_mask >> act) & 1:
+            stats[(tag, "no-discard")] = stats.get((tag, "no-discard"), 0) + 1
+            continue
+        st = apply_action(st, act)
+        while st.phase == 1 and st.actor != winner and (st.legal_mask >> A.PASS) & 1:
+            st = apply_action(st, A.PASS)
+        if st.phase == 1 and st.actor == winner:
+            record(tag, st, A.RON)  # legal or not: a NoYaku / furiten ron is an IllegalActionError
+        else:
+            stats[(tag, "no-call")] = stats.get((tag, "no-call"), 0) + 1
+    print("wins:", sorted(stats.items(), key=str))
+    dump("wins.json.gz", out)
 
 
 def obs_digest(o) -> str:
@@ -559,8 +879,10 @@ if __name__ == "__main__":
     make_tables()
     make_shanten()
     make_scoring()
+    make_scoring_rare()
     make_traces()
     make_scenarios()
+    make_wins()
     make_logs()
     make_renders()
     make_sessions()

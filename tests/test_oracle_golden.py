@@ -12,6 +12,7 @@ import pytest
 
 from oracle import mjoracle as O
 from paper_2605_20577_b200 import abi
+from paritylib import ctx_from_json
 
 GOLD = Path(__file__).resolve().parent / "golden"
 
@@ -65,39 +66,10 @@ def test_shanten_and_waits():
             assert list(O.waits(counts, melds)) == waits, (counts, melds)
 
 
-def ctx_from_json(c, kazoe, dy) -> O.orc_winctx:
-    x = O.orc_winctx()
-    for k in range(34):
-        x.concealed[k] = c["concealed"][k]
-    x.n_melds = len(c["melds"])
-    for i, (typ, tiles, called, frm) in enumerate(c["melds"]):
-        m = x.melds[i]
-        m.type, m.n_tiles, m.from_seat = typ, len(tiles), frm
-        for j, t in enumerate(tiles):
-            m.tiles[j] = t
-        m.called_tile = called
-    x.win_tile = c["win_tile"]
-    x.tsumo = int(c["tsumo"])
-    x.seat_wind, x.round_wind = c["seat_wind"], c["round_wind"]
-    x.n_ids = len(c["ids"])
-    for i, t in enumerate(c["ids"]):
-        x.ids[i] = t
-    x.riichi, x.ippatsu = c["riichi"], int(c["ippatsu"])
-    x.last_tile, x.rinshan, x.chankan, x.first_draw = (int(c[k]) for k in ("last_tile", "rinshan", "chankan", "first_draw"))
-    x.n_dora = len(c["dora"])
-    for i, t in enumerate(c["dora"]):
-        x.dora[i] = t
-    x.n_ura = len(c["ura"])
-    for i, t in enumerate(c["ura"]):
-        x.ura[i] = t
-    x.rule = c["rule"]
-    x.kazoe, x.double_yakuman = int(kazoe), int(dy)
-    return x
-
-
 def test_scoring_golden_and_randomized():
     cases = load("scoring.json.gz")
     assert len(cases) >= 900
+    cases += load("scoring_rare.json.gz")
     scored = 0
     for case in cases:
         got = O.score(ctx_from_json(case["ctx"], case["kazoe"], case["dy"]))
