@@ -2145,9 +2145,147 @@ void orc_env_result(const orc_env* e, int i, rs_result_rec* out, int8_t* orders,
 /* ------------------------------------------------------------- digests */
 
 static uint64_t o_fold(uint64_t d, uint64_t w) { return orc_mix((d ^ w) + GOLDEN); }
+static uint64_t o_digest_summary(uint64_t d, int action, const orc_env* e);
 
-/* identical on the device */
+static uint64_t o_pack4(uint32_t a, uint32_t b, uint32_t c, uint32_t x) {
+  return (uint64_t)(a & 0xFFFFu) | ((uint64_t)(b & 0xFFFFu) << 16) | ((uint64_t)(c & 0xFFFFu) << 32) |
+         ((uint64_t)(x & 0xFFFFu) << 48);
+}
+
+/* The wide part of the digest (device: rs_io.cuh digest_state): every
+ * field of the state in a canonical form -- hands (concealed tile-id set,
+ * HandState flags and waits, melds, river), call state, both RNGs, the
+ * wall, the newest 8 events and the last kyoku result
+ * (engine/types.py:72-179, engine/state.py:191-242). */
+static uint64_t o_digest_state(uint64_t d, const orc_env* e) {
+  for (int s = 0; s < 4; s++) {
+    const OHand* h = &e->hands[s];
+    uint64_t set[3] = {0, 0, 0};
+    for (int i = 0; i < h->nconc; i++) set[h->conc[i] >> 6] |= 1ull << (h->conc[i] & 63);
+    d = o_fold(d, set[0]);
+    d = o_fold(d, set[1]);
+    d = o_fold(d, set[2]);
+    d = o_fold(d, (uint64_t)h->riichi | ((uint64_t)(h->riichi_index + 1) << 2) | ((uint64_t)h->ippatsu << 8) |
+                      ((uint64_t)h->temp_furiten << 9) | ((uint64_t)h->perm_furiten << 10) |
+                      ((uint64_t)h->nmelds << 12) | ((uint64_t)h->nriver << 16) | ((uint64_t)h->nconc << 24) |
+                      (h->waits << 30));
+    for (int i = 0; i < h->nmelds; i++) {
+      const rs_meld_rec* m = &h->melds[i];
+      uint32_t tiles = 0;
+      for (int j = 0; j < m->n_tiles; j++) tiles |= (uint32_t)m->tiles[j] << (8 * j);
+      d = o_fold(d, (uint64_t)tiles | ((uint64_t)m->type << 32) | ((uint64_t)m->n_tiles << 36) |
+                        ((uint64_t)(m->from_seat + 1) << 40) | ((uint64_t)(m->called_tile + 1) << 48));
+    }
+    for (int i = 0; i < h->nriver; i += 4) {
+      uint32_t v[4];
+      for (int j = 0; j < 4; j++)
+        v[j] = i + j < h->nriver ? (uint32_t)h->river_tile[i + j] | ((uint32_t)h->river_flags[i + j] << 8) : 0u;
+      d = o_fold(d, o_pack4(v[0], v[1], v[2], v[3]));
+    }
+  }
+  d = o_fold(d, (uint64_t)(uint32_t)(e->drawn + 1) | ((uint64_t)(uint32_t)(e->call_tile + 1) << 8) |
+                    ((uint64_t)(uint32_t)(e->kakan_kind + 1) << 16) | ((uint64_t)(uint32_t)(e->call_from + 1) << 24) |
+                    ((uint64_t)e->actor << 28) | ((uint64_t)e->riichi_pending << 32) |
+                    ((uint64_t)e->rinshan_pending << 33) | ((uint64_t)e->call_chankan << 34) |
+                    ((uint64_t)e->four_kan_pending << 35) | ((uint64_t)e->any_call_made << 36) |
+                    ((uint64_t)e->terminated << 37) | ((uint64_t)e->truncated << 38) |
+                    ((uint64_t)e->pending_dora << 40) | ((uint64_t)e->repeats << 48) |
+                    ((uint64_t)e->nresults << 56));
+  uint64_t q = (uint64_t)e->nq;
+  for (int i = 0; i < e->nq; i++) q |= (uint64_t)(e->qseat[i] | (e->qstage[i] << 2)) << (4 + 4 * i);
+  q |= (uint64_t)e->nrons << 40;
+  for (int i = 0; i < e->nrons; i++) q |= (uint64_t)e->rons[i] << (44 + 2 * i);
+  d = o_fold(d, q);
+  d = o_fold(d, e->rng.key);
+  d = o_fold(d, e->rng.counter);
+  d = o_fold(d, e->policy_key);
+  d = o_fold(d, e->policy_counter);
+  for (int i = 0; i < 136; i += 8) {
+    uint64_t w = 0;
+    for (int j = 0; j < 8; j++) w |= (uint64_t)e->wall[i + j] << (8 * j);
+    d = o_fold(d, w);
+  }
+  for (int j = 0; j < 8; j += 4) {
+    uint32_t v[4];
+    for (int k = 0; k < 4; k++) {
+      int idx = e->nevents - 1 - (j + k);
+      v[k] = 0;
+      if (idx >= 0) {
+        const int16_t* ev = e->events + 3 * idx;
+        v[k] = (uint32_t)ev[0] | ((uint32_t)(ev[1] + 1) << 4) | ((uint32_t)(ev[2] + 1) << 7);
+      }
+    }
+    d = o_fold(d, o_pack4(v[0], v[1], v[2], v[3]));
+  }
+  if (e->nresults > 0) {
+    const rs_result_rec* r = &e->results[e->nresults - 1].rec;
+    uint64_t wn = 0;
+    for (int i = 0; i < r->n_winners; i++) wn |= (uint64_t)(uint8_t)r->winners[i] << (2 * i);
+    d = o_fold(d, (uint64_t)(uint32_t)r->kyoku | ((uint64_t)(uint32_t)r->honba << 8) |
+                      ((uint64_t)(uint32_t)r->kind << 16) | ((uint64_t)(uint32_t)r->n_winners << 24) |
+                      ((uint64_t)(uint32_t)r->n_settlements << 28) | ((uint64_t)(uint32_t)(r->loser + 1) << 32) |
+                      ((uint64_t)(uint32_t)r->tenpai_mask << 40) | (wn << 48));
+    for (int i = 0; i < r->n_settlements; i++) {
+      d = o_fold(d, (uint64_t)(uint32_t)r->deltas[i][0] | ((uint64_t)(uint32_t)r->deltas[i][1] << 32));
+      d = o_fold(d, (uint64_t)(uint32_t)r->deltas[i][2] | ((uint64_t)(uint32_t)r->deltas[i][3] << 32));
+      d = o_fold(d, (uint64_t)(uint32_t)r->honba_component[i] | ((uint64_t)(uint32_t)r->deposits_claimed[i] << 32));
+    }
+    for (int i = 0; i < r->n_winners; i++) {
+      const rs_win_rec* w = &r->wins[i];
+      for (int k = 0; k < 40; k += 8) {
+        uint64_t y = 0;
+        for (int j = 0; j < 8; j++) y |= (uint64_t)(uint8_t)w->yaku_han[k + j] << (8 * j);
+        d = o_fold(d, y);
+      }
+      d = o_fold(d, (uint64_t)(uint32_t)w->yakuman | ((uint64_t)(uint32_t)w->han << 8) |
+                        ((uint64_t)(uint32_t)w->fu << 16) | ((uint64_t)(uint32_t)w->base << 32));
+      d = o_fold(d, (uint64_t)(uint32_t)w->dora | ((uint64_t)(uint32_t)w->ura << 8) |
+                        ((uint64_t)(uint32_t)w->reds << 16) | ((uint64_t)(uint32_t)w->form << 24));
+    }
+    d = o_fold(d, (uint64_t)(uint32_t)r->scores_after[0] | ((uint64_t)(uint32_t)r->scores_after[1] << 32));
+    d = o_fold(d, (uint64_t)(uint32_t)r->scores_after[2] | ((uint64_t)(uint32_t)r->scores_after[3] << 32));
+  }
+  return d;
+}
+
+/* observe(current player) folded (device: rs_io.cuh digest_obs) */
+static uint64_t o_digest_obs(uint64_t d, const orc_obs* o) {
+  uint64_t lo = 0, hi = 0;
+  for (int j = 0; j < 8; j++) lo |= (uint64_t)o->hand_tokens[j] << (8 * j);
+  for (int j = 0; j < 6; j++) hi |= (uint64_t)o->hand_tokens[8 + j] << (8 * j);
+  d = o_fold(d, lo);
+  d = o_fold(d, hi);
+  const uint8_t* ev = &o->event_tokens[0][0];
+  for (int k = 0; k < 192; k += 8) {
+    uint64_t w = 0;
+    for (int j = 0; j < 8; j++) w |= (uint64_t)ev[k + j] << (8 * j);
+    d = o_fold(d, w);
+  }
+  d = o_fold(d, o_pack4((uint16_t)(int16_t)o->scores[0], (uint16_t)(int16_t)o->scores[1],
+                        (uint16_t)(int16_t)o->scores[2], (uint16_t)(int16_t)o->scores[3]));
+  d = o_fold(d, (uint64_t)(uint8_t)(int8_t)o->shanten | ((uint64_t)(uint8_t)o->round_wind << 8) |
+                    ((uint64_t)(uint8_t)o->seat_wind << 16) | ((uint64_t)(uint8_t)o->kyoku << 24) |
+                    ((uint64_t)(uint16_t)(int16_t)o->honba << 32) | ((uint64_t)(uint16_t)(int16_t)o->deposits << 48));
+  uint64_t w = 0;
+  for (int j = 0; j < 5; j++) w |= (uint64_t)o->dora_tokens[j] << (8 * j);
+  w |= (uint64_t)(uint8_t)o->live_wall << 40;
+  for (int j = 0; j < 4; j++) w |= (uint64_t)(o->riichi_flags[j] & 1u) << (48 + j);
+  return o_fold(d, w);
+}
+
+/* identical on the device (rs_io.cuh
+ * digest_step + digest_state + digest_obs) */
 uint64_t orc_digest_step(uint64_t d, int action, const orc_env* e) {
+  d = o_digest_summary(d, action, e);
+  d = o_digest_state(d, e);
+  orc_obs o;
+  orc_env_observe(e, e->current_player, &o);
+  return o_digest_obs(d, &o);
+}
+
+/* the summary part: action, player, flags, round counters, legal mask,
+ * scores, rewards, shanten, event count, wall counters */
+static uint64_t o_digest_summary(uint64_t d, int action, const orc_env* e) {
   d = o_fold(d, (uint64_t)(uint32_t)action);
   d = o_fold(d, (uint64_t)(uint32_t)e->current_player | ((uint64_t)e->env_terminated << 8) |
                     ((uint64_t)e->env_truncated << 9) | ((uint64_t)e->phase << 12) |

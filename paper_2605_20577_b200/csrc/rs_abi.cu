@@ -504,6 +504,20 @@ __global__ void __launch_bounds__(BLOCK) k_observe(const __grid_constant__ Soa S
   write_obs(E, seats ? (int)seats[e] : E.g.current_player, obs, e);
 }
 
+// the wide trajectory digest of one step (tests, rs_rollout digests): the
+// summary, every state field, then the current player's observation as
+// write_obs encodes it into the env's scratch record (the lane group's
+// lanes write quarters of the window, so the group syncs around it)
+__device__ __noinline__ uint64_t digest_wide(uint64_t d, int a, const Engine& E, const Mask115& m, const float* r,
+                                             const rs_obs_out& dobs, uint32_t gm) {
+  d = digest_state(digest_step(d, a, E, m, r), E);
+  write_obs(E, E.g.current_player, dobs, E.e);
+  __syncwarp(gm);
+  d = digest_obs(d, dobs, E.e);
+  __syncwarp(gm);
+  return d;
+}
+
 // the fused rollout: the packed header stays in registers for all K steps.
 // Persistent grid (at most the resident CTA count): each CTA stages the
 // tables once and walks env tiles grid-stride.
@@ -511,7 +525,7 @@ __global__ void __launch_bounds__(ROLL_BLOCK, ROLL_MINB) k_rollout(const __grid_
     const __grid_constant__ Cfg C, int steps, rs_obs_out obs,
                                                    int obs_slots, int16_t* actions_log, int8_t* actors_log,
                                                    StepOut traj, rs_rollout_stats* stats,
-                                                   uint64_t* digests, StepOut out, int epw,
+                                                   uint64_t* digests, rs_obs_out dobs, StepOut out, int epw,
                                                    uint32_t* prof, int staged, int policy, int glog2,
                                                    int check, const int32_t* order, uint8_t* kind_out,
                                                    int prefetch) {
@@ -575,7 +589,7 @@ __global__ void __launch_bounds__(ROLL_BLOCK, ROLL_MINB) k_rollout(const __grid_
       if (traj.legal_bits || traj.rewards || traj.current_player || traj.terminated || traj.status)
         write_step_out(traj, (int64_t)t * S.n + e, E, m, r, st);
       if ((E.g.env_terminated || E.g.env_truncated) && sub == 0) games++;
-      if (digests) d = digest_step(d, a, E, m, r);
+      if (digests) d = digest_wide(d, a, E, m, r, dobs, gm);
       if (obs_slots > 0 && (obs_slots > 1 || t == steps - 1)) {
         const int slot = obs_slots > 1 ? t % obs_slots : 0;
         write_obs(E, E.g.current_player, obs, (int64_t)slot * S.n + e);
@@ -780,6 +794,10 @@ struct rs_handle {
   int cluster;
   int occ_cl_key[8], occ_cl_val[8];  // co-resident clusters per (block, smem)
   int prefetch;  // RINSHAN_PREFETCH: L1 prefetch of an env's lines before its step (prefetch_env)
+  // per-env observation scratch of the wide trajectory digest (digest_obs),
+  // allocated by the first rollout that asks for digests
+  void* dig_obs_mem = nullptr;
+  rs_obs_out dig_obs{};
 };
 
 namespace {
@@ -1122,6 +1140,7 @@ int rs_destroy(rs_handle* h) {
   cudaFree(h->mem);
   cudaFree(h->sort_tmp);
   cudaFree(h->export_buf);
+  cudaFree(h->dig_obs_mem);
   delete h;
   return 0;
 }
@@ -1234,6 +1253,17 @@ int rs_rollout_policy(rs_handle* h, int32_t steps, int32_t policy, const rs_obs_
   if (obs) o = *obs;
   // persistent grid of the resident CTA count (tables staged once per CTA,
   // envs walked grid-stride)
+  if (digests_dev && !h->dig_obs_mem) {
+    const size_t n = (size_t)h->n;
+    uint8_t* p = nullptr;
+    CUDA_TRY(cudaMalloc(&p, n * 256));
+    h->dig_obs_mem = p;
+    rs_obs_out& d = h->dig_obs;
+    d.event_tokens = p; d.hand_tokens = p + 192 * n; d.shanten = (int8_t*)(p + 206 * n);  // window: uint4 stores
+    d.scores = (int16_t*)(p + 208 * n); d.honba = (int16_t*)(p + 216 * n); d.deposits = (int16_t*)(p + 218 * n);
+    d.round_wind = p + 220 * n; d.seat_wind = p + 221 * n; d.kyoku = p + 222 * n; d.live_wall = p + 223 * n;
+    d.dora_tokens = p + 224 * n; d.riichi_flags = p + 229 * n;
+  }
   const Launch L = step_launch(h, true);
   if (L.ordered) {
     const int rc = order_envs(h, st);
@@ -1241,7 +1271,7 @@ int rs_rollout_policy(rs_handle* h, int32_t steps, int32_t policy, const rs_obs_
   }
   CUDA_TRY(launch_tables(h, k_rollout, L.grid, L.block, L.smem, st, h->S, h->D, h->cfg, steps, o,
                          obs ? obs_slots : 0, actions_log, actors_log, step_out(h, traj), stats_dev, digests_dev,
-                         step_out(h, out), L.epw, nullptr, L.staged, policy, L.glog2, h->check_steps,
+                         h->dig_obs, step_out(h, out), L.epw, nullptr, L.staged, policy, L.glog2, h->check_steps,
                          L.ordered ? (const int32_t*)h->order : nullptr, L.ordered ? h->kind : nullptr,
                          h->prefetch));
   return finish_step_out(h, out, st);
@@ -1258,7 +1288,7 @@ int rs_debug_rollout_cycles(rs_handle* h, int32_t steps, const rs_obs_out* obs, 
   if (obs) o = *obs;
   const Launch L = step_launch(h, true);
   CUDA_TRY(launch_tables(h, k_rollout, L.grid, L.block, L.smem, st, h->S, h->D, h->cfg, steps, o, obs ? 1 : 0,
-                         nullptr, nullptr, StepOut{}, nullptr, nullptr, StepOut{}, L.epw, prof_dev, L.staged,
+                         nullptr, nullptr, StepOut{}, nullptr, nullptr, rs_obs_out{}, StepOut{}, L.epw, prof_dev, L.staged,
                          (int)RS_POLICY_RANDOM, L.glog2, 0, (const int32_t*)nullptr, (uint8_t*)nullptr,
                          h->prefetch));
   CUDA_TRY(cudaGetLastError());

@@ -131,6 +131,132 @@ RS_HD uint64_t digest_step(uint64_t d, int action, const Engine& E, const Mask11
   return d;
 }
 
+// The wide part of the trajectory digest (identical to oracle/mjoracle.c
+// o_digest_state / o_digest_obs): every state field of the env, folded in
+// a canonical form after every step -- the four hands (136-bit concealed
+// sets, HandState flags and waits, melds, river entries with their flags),
+// the call state, the game and policy RNGs, the whole wall, the newest
+// events and the last kyoku result with its win details
+// (engine/types.py:72-179, engine/state.py:191-242) -- and the observation
+// of the current player exactly as write_obs encodes it (observe.py:81-124).
+RS_HD uint64_t dpack4(uint32_t a, uint32_t b, uint32_t c, uint32_t e) {
+  return (uint64_t)(a & 0xFFFFu) | ((uint64_t)(b & 0xFFFFu) << 16) | ((uint64_t)(c & 0xFFFFu) << 32) |
+         ((uint64_t)(e & 0xFFFFu) << 48);
+}
+RS_COLD uint64_t digest_state(uint64_t d, const Engine& E) {
+  const Soa& S = E.S;
+  const Game& g = E.g;
+  for (int s = 0; s < 4; s++) {
+    const Hand h = load_hand(E.bp, s);
+    d = dfold(d, (uint64_t)h.w0 | ((uint64_t)h.w1 << 32));
+    d = dfold(d, (uint64_t)h.w2 | ((uint64_t)h.w3 << 32));
+    d = dfold(d, (uint64_t)(h.w4 & 0xFFu));
+    const uint32_t inf = h.info;
+    const int nm = hi::nmelds(inf), nr = hi::nriver(inf);
+    d = dfold(d, (uint64_t)hi::riichi(inf) | ((uint64_t)(hi::riichi_index(inf) + 1) << 2) |
+                     ((uint64_t)hi::ippatsu(inf) << 8) | ((uint64_t)hi::temp(inf) << 9) |
+                     ((uint64_t)hi::perm(inf) << 10) | ((uint64_t)nm << 12) | ((uint64_t)nr << 16) |
+                     ((uint64_t)hi::nconc(inf) << 24) | (E.waits(s) << 30));
+    for (int i = 0; i < nm; i++) {
+      const uint32_t mf = E.meld_info(s, i), mt = E.meld_tiles(s, i);
+      const int nt = mi::ntiles(mf);
+      const uint32_t tiles = nt >= 4 ? mt : (mt & ((1u << (8 * nt)) - 1u));
+      d = dfold(d, (uint64_t)tiles | ((uint64_t)mi::type(mf) << 32) | ((uint64_t)nt << 36) |
+                       ((uint64_t)(mi::from(mf) + 1) << 40) | ((uint64_t)(mi::called(mf) + 1) << 48));
+    }
+    for (int i = 0; i < nr; i += 4) {
+      uint32_t v[4];
+      for (int j = 0; j < 4; j++) v[j] = i + j < nr ? S.river[E.at(s * RS_MAX_RIVER + i + j)] : 0u;
+      d = dfold(d, dpack4(v[0], v[1], v[2], v[3]));
+    }
+  }
+  d = dfold(d, (uint64_t)(uint32_t)(g.drawn + 1) | ((uint64_t)(uint32_t)(g.call_tile + 1) << 8) |
+                   ((uint64_t)(uint32_t)(g.kakan_kind + 1) << 16) | ((uint64_t)(uint32_t)(g.call_from + 1) << 24) |
+                   ((uint64_t)g.actor << 28) | ((uint64_t)g.riichi_pending << 32) |
+                   ((uint64_t)g.rinshan_pending << 33) | ((uint64_t)g.call_chankan << 34) |
+                   ((uint64_t)g.four_kan_pending << 35) | ((uint64_t)g.any_call_made << 36) |
+                   ((uint64_t)g.terminated << 37) | ((uint64_t)g.truncated << 38) |
+                   ((uint64_t)g.pending_dora << 40) | ((uint64_t)g.repeats << 48) | ((uint64_t)g.n_results << 56));
+  uint64_t q = (uint64_t)g.qn();
+  for (int i = 0; i < g.qn(); i++) q |= (uint64_t)(g.qseat(i) | (g.qstage(i) << 2)) << (4 + 4 * i);
+  q |= (uint64_t)g.rn() << 40;
+  for (int i = 0; i < g.rn(); i++) q |= (uint64_t)g.rseat(i) << (44 + 2 * i);
+  d = dfold(d, q);
+  d = dfold(d, g.rng_key);
+  d = dfold(d, (uint64_t)g.rng_counter);
+  d = dfold(d, g.policy_key);
+  d = dfold(d, g.policy_counter);
+  const uint8_t* wl = swall(E.bp);
+  for (int i = 0; i < 136; i += 8) {
+    uint64_t w = 0;
+    for (int j = 0; j < 8; j++) w |= (uint64_t)wl[i + j] << (8 * j);
+    d = dfold(d, w);
+  }
+  // the newest 8 events (type | (actor + 1) << 4 | (tile + 1) << 7)
+  for (int j = 0; j < 8; j += 4) {
+    uint32_t v[4];
+    for (int k = 0; k < 4; k++) {
+      const int idx = (int)g.events_len - 1 - (j + k);
+      v[k] = idx >= 0 ? S.events[(size_t)E.e * RS_EVENT_WINDOW + (idx & 63)] : 0u;
+    }
+    d = dfold(d, dpack4(v[0], v[1], v[2], v[3]));
+  }
+  if (g.n_results > 0) {
+    const rs_result_rec& r = S.results[E.e];
+    uint64_t wn = 0;
+    for (int i = 0; i < r.n_winners; i++) wn |= (uint64_t)(uint8_t)r.winners[i] << (2 * i);
+    d = dfold(d, (uint64_t)(uint32_t)r.kyoku | ((uint64_t)(uint32_t)r.honba << 8) | ((uint64_t)(uint32_t)r.kind << 16) |
+                     ((uint64_t)(uint32_t)r.n_winners << 24) | ((uint64_t)(uint32_t)r.n_settlements << 28) |
+                     ((uint64_t)(uint32_t)(r.loser + 1) << 32) | ((uint64_t)(uint32_t)r.tenpai_mask << 40) |
+                     (wn << 48));
+    for (int i = 0; i < r.n_settlements; i++) {
+      d = dfold(d, (uint64_t)(uint32_t)r.deltas[i][0] | ((uint64_t)(uint32_t)r.deltas[i][1] << 32));
+      d = dfold(d, (uint64_t)(uint32_t)r.deltas[i][2] | ((uint64_t)(uint32_t)r.deltas[i][3] << 32));
+      d = dfold(d, (uint64_t)(uint32_t)r.honba_component[i] | ((uint64_t)(uint32_t)r.deposits_claimed[i] << 32));
+    }
+    for (int i = 0; i < r.n_winners; i++) {
+      const rs_win_rec& w = r.wins[i];
+      for (int k = 0; k < 40; k += 8) {
+        uint64_t y = 0;
+        for (int j = 0; j < 8; j++) y |= (uint64_t)(uint8_t)w.yaku_han[k + j] << (8 * j);
+        d = dfold(d, y);
+      }
+      d = dfold(d, (uint64_t)(uint32_t)w.yakuman | ((uint64_t)(uint32_t)w.han << 8) | ((uint64_t)(uint32_t)w.fu << 16) |
+                       ((uint64_t)(uint32_t)w.base << 32));
+      d = dfold(d, (uint64_t)(uint32_t)w.dora | ((uint64_t)(uint32_t)w.ura << 8) | ((uint64_t)(uint32_t)w.reds << 16) |
+                       ((uint64_t)(uint32_t)w.form << 24));
+    }
+    d = dfold(d, (uint64_t)(uint32_t)r.scores_after[0] | ((uint64_t)(uint32_t)r.scores_after[1] << 32));
+    d = dfold(d, (uint64_t)(uint32_t)r.scores_after[2] | ((uint64_t)(uint32_t)r.scores_after[3] << 32));
+  }
+  return d;
+}
+// the observation record i of `o` (as write_obs wrote it)
+RS_COLD uint64_t digest_obs(uint64_t d, const rs_obs_out& o, int64_t i) {
+  const uint8_t* ht = o.hand_tokens + i * 14;
+  uint64_t lo = 0, hi8 = 0;
+  for (int j = 0; j < 8; j++) lo |= (uint64_t)ht[j] << (8 * j);
+  for (int j = 0; j < 6; j++) hi8 |= (uint64_t)ht[8 + j] << (8 * j);
+  d = dfold(d, lo);
+  d = dfold(d, hi8);
+  const uint8_t* ev = o.event_tokens + i * 192;
+  for (int k = 0; k < 192; k += 8) {
+    uint64_t w = 0;
+    for (int j = 0; j < 8; j++) w |= (uint64_t)ev[k + j] << (8 * j);
+    d = dfold(d, w);
+  }
+  const int16_t* sc = o.scores + i * 4;
+  d = dfold(d, dpack4((uint16_t)sc[0], (uint16_t)sc[1], (uint16_t)sc[2], (uint16_t)sc[3]));
+  d = dfold(d, (uint64_t)(uint8_t)o.shanten[i] | ((uint64_t)o.round_wind[i] << 8) | ((uint64_t)o.seat_wind[i] << 16) |
+                   ((uint64_t)o.kyoku[i] << 24) | ((uint64_t)(uint16_t)o.honba[i] << 32) |
+                   ((uint64_t)(uint16_t)o.deposits[i] << 48));
+  uint64_t w = 0;
+  for (int j = 0; j < 5; j++) w |= (uint64_t)o.dora_tokens[i * 5 + j] << (8 * j);
+  w |= (uint64_t)o.live_wall[i] << 40;
+  for (int j = 0; j < 4; j++) w |= (uint64_t)(o.riichi_flags[i * 4 + j] & 1u) << (48 + j);
+  return dfold(d, w);
+}
+
 // projection record (include/rinshan.h rs_env_rec) of env e
 RS_COLD void export_env(Engine& E, const Cfg& C, rs_env_rec& r) {
   const Soa& S = E.S;

@@ -148,7 +148,18 @@ int64_t hc_rollout(void* p, int steps, uint64_t* digests, int16_t* actions_log, 
       E.step(a, m, r);
       if (actions_log) actions_log[(size_t)t * h->S.n + e] = (int16_t)a;
       if (E.g.env_terminated || E.g.env_truncated) games++;
-      if (digests) d = digest_step(d, a, E, m, r);
+      if (digests) {  // the wide digest, as k_rollout folds it
+        uint8_t ht[14], ev[192], misc[4], dora[5], riichi[4];
+        int8_t sh;
+        int16_t sc[4], hd[2];
+        rs_obs_out o;
+        o.hand_tokens = ht; o.event_tokens = ev; o.shanten = &sh; o.scores = sc;
+        o.round_wind = misc; o.seat_wind = misc + 1; o.kyoku = misc + 2; o.live_wall = misc + 3;
+        o.honba = hd; o.deposits = hd + 1; o.dora_tokens = dora; o.riichi_flags = riichi;
+        d = digest_state(digest_step(d, a, E, m, r), E);
+        write_obs(E, E.g.current_player, o, 0);
+        d = digest_obs(d, o, 0);
+      }
     }
     if (digests) digests[e] = d;
     E.store();

@@ -18,7 +18,9 @@ RULES = ("no-red", "red")
 
 def _oracle_cfg(cfg: EnvConfig):
     return O.make_config(rule=cfg.rule, mode=cfg.mode, illegal_penalty=cfg.illegal_penalty,
-                         reward_scheme=cfg.reward_scheme, max_steps=cfg.max_steps)
+                         reward_scheme=cfg.reward_scheme, max_steps=cfg.max_steps, kazoe=cfg.kazoe,
+                         double_yakuman=cfg.double_yakuman, agari_yame=cfg.agari_yame,
+                         renchan_cap=cfg.renchan_cap)
 
 
 @pytest.mark.parametrize("rule", RULES)
@@ -39,6 +41,28 @@ def test_fused_rollout_digests_match_oracle(rule, mode):
     assert not bad, f"{len(bad)} envs diverge, first {bad[:8]}"
     st = stats.cpu().tolist()
     assert st[0] == n * steps and st[1] == games
+
+
+@pytest.mark.parametrize("rule", RULES)
+@pytest.mark.parametrize("policy", ("random", "heuristic"))
+def test_config_flags_rollouts_match_oracle(rule, policy):
+    """GameConfig flags off their defaults (engine/types.py:49-57): kazoe and
+    double yakuman on (the settlement values of 13+ han and of the
+    double-yakuman waits), agari-yame off, a short renchan cap and the rank
+    reward scheme, over hanchan games, fused rollouts vs the oracle"""
+    n, steps = (1024, 900) if policy == "random" else (2048, 600)
+    cfg = EnvConfig(rule=rule, mode="half", kazoe=True, double_yakuman=True, agari_yame=False,
+                    renchan_cap=2, reward_scheme="rank")
+    env = BatchEnv(n, cfg).init(seed=29, index_base=0)
+    digests = torch.zeros(n, dtype=torch.int64, device="cuda")
+    stats = torch.zeros(3, dtype=torch.int64, device="cuda")
+    env.rollout(steps, digests=digests, stats=stats, policy=policy)
+    torch.cuda.synchronize()
+    games, ref = O.run_shard(_oracle_cfg(cfg), 29, 0, n, steps, policy=policy, digests=True)
+    got = [int(x) & ((1 << 64) - 1) for x in digests.cpu().tolist()]
+    bad = [i for i in range(n) if got[i] != ref[i]]
+    assert not bad, f"{len(bad)} envs diverge, first {bad[:8]}"
+    assert stats.cpu().tolist()[1] == games
 
 
 @pytest.mark.parametrize("stage", ("1", "2"))

@@ -1,9 +1,19 @@
 """North-star parity bar (BASELINE.json): bit-exact with the CPU oracle on
 >= 10^5 randomly played hands per rule.  32,768 bench-seeded envs x 400
 fused steps on the device; the oracle replays the same envs on all host
-threads; every env's 64-bit trajectory digest (action, player, flags,
-phase, round counters, legal mask, scores, rewards, shanten of all seats,
-events length, wall counters at every step) must match.  Needs a B200."""
+threads; every env's 64-bit trajectory digest must match.  The digest
+folds, after every step: the action, player, flags, phase, round
+counters, legal mask, scores, rewards, shanten of all seats, events
+length and wall counters (digest_step); every state field in canonical
+form -- the four concealed tile-id sets, HandState flags (riichi, riichi
+index, ippatsu, temp / permanent furiten), waits, melds, river entries
+with their flags, the call queue and ron list, both RNGs, the whole wall
+with its dora / ura indicators, the newest events and the last kyoku
+result with its win details (digest_state); and the current player's
+observation exactly as encoded (digest_obs, env/observe.py:81-124).  The
+random-policy soak also runs the fast invariant checker
+(engine/state.py:105-178, the soak gate of bench/runner.py:226-284) after
+every step of the whole run (RINSHAN_CHECK=1).  Needs a B200."""
 
 from __future__ import annotations
 
@@ -20,13 +30,18 @@ pytestmark = pytest.mark.gpu
 
 
 @pytest.mark.parametrize("rule", ("no-red", "red"))
-def test_bit_exact_on_1e5_hands(rule):
+def test_bit_exact_on_1e5_hands(rule, monkeypatch):
+    from paper_2605_20577_b200 import abi
+
+    monkeypatch.setenv("RINSHAN_CHECK", "1")  # invariants after every step (read at rs_create)
     n, steps, seed, chunk = 32768, 400, 2026, 1024
     env = BatchEnv(n, EnvConfig(rule=rule)).init(seed=seed, index_base=0)
     digests = torch.zeros(n, dtype=torch.int64, device="cuda")
     stats = torch.zeros(3, dtype=torch.int64, device="cuda")
     env.rollout(steps, digests=digests, stats=stats)
     torch.cuda.synchronize()
+    # RS_STATUS_INVARIANT is sticky over the fused steps of a launch
+    assert int((env.status.int() & abi.STATUS_INVARIANT).count_nonzero().item()) == 0
     got = [int(x) & ((1 << 64) - 1) for x in digests.cpu().tolist()]
     games = int(stats[1].item())
     env.close()
