@@ -97,7 +97,8 @@ def lib():
         L.rs_import_env.argtypes = [vp, i64, vp]
         L.rs_record_sizes.argtypes = [vp]
         L.rs_debug_rollout_cycles.argtypes = [vp, i32, vp, vp, vp]
-        L.rs_debug_score.argtypes = [vp, i64, vp, vp, i32]
+        if hasattr(L, "rs_debug_score"):  # (A/B builds of older sources lack it)
+            L.rs_debug_score.argtypes = [vp, i64, vp, vp, i32]
         if L.rs_abi_version() != 1:
             raise RinshanError("ABI version mismatch between _rinshan.so and the Python layer")
         _lib = L

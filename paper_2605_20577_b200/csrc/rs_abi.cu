@@ -521,6 +521,10 @@ __device__ __noinline__ uint64_t digest_wide(uint64_t d, int a, const Engine& E,
 // the fused rollout: the packed header stays in registers for all K steps.
 // Persistent grid (at most the resident CTA count): each CTA stages the
 // tables once and walks env tiles grid-stride.
+// WIDE: the test / parity instantiation that folds the wide digest
+// (digest_wide) when `digests` is given; the production instantiation has
+// none of that code (-2.5 % launch time at 4,096 envs when it shared it)
+template <bool WIDE>
 __global__ void __launch_bounds__(ROLL_BLOCK, ROLL_MINB) k_rollout(const __grid_constant__ Soa S, const __grid_constant__ DevTables D,
     const __grid_constant__ Cfg C, int steps, rs_obs_out obs,
                                                    int obs_slots, int16_t* actions_log, int8_t* actors_log,
@@ -589,7 +593,7 @@ __global__ void __launch_bounds__(ROLL_BLOCK, ROLL_MINB) k_rollout(const __grid_
       if (traj.legal_bits || traj.rewards || traj.current_player || traj.terminated || traj.status)
         write_step_out(traj, (int64_t)t * S.n + e, E, m, r, st);
       if ((E.g.env_terminated || E.g.env_truncated) && sub == 0) games++;
-      if (digests) d = digest_wide(d, a, E, m, r, dobs, gm);
+      if (WIDE && digests) d = digest_wide(d, a, E, m, r, dobs, gm);
       if (obs_slots > 0 && (obs_slots > 1 || t == steps - 1)) {
         const int slot = obs_slots > 1 ? t % obs_slots : 0;
         write_obs(E, E.g.current_player, obs, (int64_t)slot * S.n + e);
@@ -828,7 +832,7 @@ int resident_ctas(rs_handle* h, int block, int smem) {
   for (int i = 0; i < 16; i++)
     if (h->occ_key[i] == key) return h->occ_val[i];
   int ctas = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ctas, k_rollout, block, smem) != cudaSuccess) {
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ctas, k_rollout<false>, block, smem) != cudaSuccess) {
     cudaGetLastError();
     ctas = 1;
   }
@@ -882,7 +886,7 @@ int persistent_ctas(rs_handle* h, const Launch& L) {
   cfg.attrs = at;
   cfg.numAttrs = 1;
   int clusters = 0;
-  if (cudaOccupancyMaxActiveClusters(&clusters, k_rollout, &cfg) != cudaSuccess) {
+  if (cudaOccupancyMaxActiveClusters(&clusters, k_rollout<false>, &cfg) != cudaSuccess) {
     cudaGetLastError();
     clusters = h->num_sms * L.ctas / L.cluster;
   }
@@ -1102,7 +1106,8 @@ int rs_create(rs_handle** out, int64_t n_envs, const rs_config* cfg, int32_t dev
     return cleanup(err, "sort size query");
   if ((err = cudaMalloc(&h->sort_tmp, std::max<size_t>(h->sort_tmp_bytes, 16)))) return cleanup(err, "sort scratch");
   const void* kernels[] = {(const void*)k_init, (const void*)k_step, (const void*)k_policy,
-                           (const void*)k_observe, (const void*)k_rollout, (const void*)k_export,
+                           (const void*)k_observe, (const void*)k_rollout<false>, (const void*)k_rollout<true>,
+                           (const void*)k_export,
                            (const void*)k_import, (const void*)k_autoreset, (const void*)k_check};
   for (const void* k : kernels)
     if ((err = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_staged(ROLL_BLOCK, ROLL_BLOCK))))
@@ -1269,8 +1274,8 @@ int rs_rollout_policy(rs_handle* h, int32_t steps, int32_t policy, const rs_obs_
     const int rc = order_envs(h, st);
     if (rc) return rc;
   }
-  CUDA_TRY(launch_tables(h, k_rollout, L.grid, L.block, L.smem, st, h->S, h->D, h->cfg, steps, o,
-                         obs ? obs_slots : 0, actions_log, actors_log, step_out(h, traj), stats_dev, digests_dev,
+  CUDA_TRY(launch_tables(h, digests_dev ? k_rollout<true> : k_rollout<false>, L.grid, L.block, L.smem, st, h->S,
+                         h->D, h->cfg, steps, o, obs ? obs_slots : 0, actions_log, actors_log, step_out(h, traj), stats_dev, digests_dev,
                          h->dig_obs, step_out(h, out), L.epw, nullptr, L.staged, policy, L.glog2, h->check_steps,
                          L.ordered ? (const int32_t*)h->order : nullptr, L.ordered ? h->kind : nullptr,
                          h->prefetch));
@@ -1287,7 +1292,7 @@ int rs_debug_rollout_cycles(rs_handle* h, int32_t steps, const rs_obs_out* obs, 
   rs_obs_out o{};
   if (obs) o = *obs;
   const Launch L = step_launch(h, true);
-  CUDA_TRY(launch_tables(h, k_rollout, L.grid, L.block, L.smem, st, h->S, h->D, h->cfg, steps, o, obs ? 1 : 0,
+  CUDA_TRY(launch_tables(h, k_rollout<false>, L.grid, L.block, L.smem, st, h->S, h->D, h->cfg, steps, o, obs ? 1 : 0,
                          nullptr, nullptr, StepOut{}, nullptr, nullptr, rs_obs_out{}, StepOut{}, L.epw, prof_dev, L.staged,
                          (int)RS_POLICY_RANDOM, L.glog2, 0, (const int32_t*)nullptr, (uint8_t*)nullptr,
                          h->prefetch));
