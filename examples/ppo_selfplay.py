@@ -19,17 +19,16 @@ from __future__ import annotations
 
 import argparse
 import json
-import os
 import sys
 import time
 from pathlib import Path
 
 import torch
-import torch.distributed as dist
 import torch.nn as nn
 import torch.nn.functional as F
 
 sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
+from paper_2605_20577_b200 import dist as D  # noqa: E402
 from paper_2605_20577_b200.env import BatchEnv, EnvConfig  # noqa: E402
 
 NUM_ACTIONS = 115
@@ -87,6 +86,7 @@ def main():
     p.add_argument("--minibatch", type=int, default=8192)
     p.add_argument("--rule", default="no-red")
     p.add_argument("--seed", type=int, default=0)
+    p.add_argument("--dist-backend", choices=("nccl", "gloo"), default="nccl")
     p.add_argument("--no-graph", dest="graph", action="store_false",
                    help="run the rollout eagerly instead of replaying it as one CUDA graph")
     args = p.parse_args()
@@ -94,21 +94,19 @@ def main():
 
 
 def run(args) -> dict:
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
+    rank, world, local = D.world()
     if world > 1:
-        dist.init_process_group("nccl")
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
+        D.init(args.dist_backend, local)  # DDP gradient all-reduce + the stats reduction
+    dev = D.device(local)
+    torch.cuda.set_device(dev)
     torch.manual_seed(args.seed + rank)
-    n, T = args.envs, args.horizon
+    T = args.horizon
     # env shard of this rank: global indices [rank * n, (rank + 1) * n)
-    env = BatchEnv(n, EnvConfig(rule=args.rule, mode="single"), device=dev).init(seed=args.seed,
-                                                                                  index_base=rank * n)
+    base, n = D.shard(rank, world, args.envs)
+    env = BatchEnv(n, EnvConfig(rule=args.rule, mode="single"), device=dev).init(seed=args.seed, index_base=base)
     obs = env.observe()
     net = Policy().to(dev)
-    model = nn.parallel.DistributedDataParallel(net, device_ids=[local]) if world > 1 else net
+    model = nn.parallel.DistributedDataParallel(net, device_ids=[dev.index]) if world > 1 else net
     opt = torch.optim.Adam(model.parameters(), lr=3e-4)
     keys = list(obs.keys())
     buf = {k: torch.empty((T,) + tuple(obs[k].shape), dtype=obs[k].dtype, device=dev) for k in keys}
@@ -205,10 +203,9 @@ def run(args) -> dict:
         stats["last_loss"] = float(loss.item())
     stats["env_steps_per_s_rollout"] = stats.get("timed_steps", 0) / max(stats["rollout_s"], 1e-9)
     if world > 1:
-        t = torch.tensor([stats["env_steps"], stats["games"]], dtype=torch.float64, device=dev)
-        dist.all_reduce(t)
+        t = D.reduce_stats(torch.tensor([stats["env_steps"], stats["games"]], dtype=torch.int64, device=dev))
         stats["env_steps_all_ranks"], stats["games_all_ranks"] = int(t[0]), int(t[1])
-        dist.destroy_process_group()
+        D.finish()
     env.close()
     stats["rank"], stats["world"] = rank, world
     return stats

@@ -67,6 +67,9 @@ def _ptr(t: torch.Tensor | None) -> int | None:
     return None if t is None else t.data_ptr()
 
 
+OBS_BYTES = 232  # one observation record (rs_obs_out fields) per env
+
+
 class Observations(dict):
     """Observation tensors keyed like Observation.to_dict() (docs/formats.md:32-52)."""
 
@@ -88,6 +91,29 @@ def alloc_observations(n: int, device, slots: int | None = None) -> Observations
         live_wall=torch.empty(*lead, dtype=torch.uint8, **kw),
         riichi_flags=torch.empty(*lead, 4, dtype=torch.uint8, **kw),
     )
+
+
+def alloc_observations_block(n: int, pinned: bool = True, device=None) -> tuple[torch.Tensor, Observations]:
+    """one contiguous 232-byte-per-env block (field-major) and the
+    observation views into it: pinned host memory by default (the kernels
+    write it directly over the host link), else device memory.  The event
+    window comes first: write_obs stores it as 16-byte vectors."""
+    kw = dict(pin_memory=True) if pinned else dict(device=device)
+    buf = torch.zeros(OBS_BYTES * n, dtype=torch.uint8, **kw)
+    o, off = {}, 0
+    for name, shape, dt in (("event_tokens", (64, 3), torch.uint8), ("hand_tokens", (14,), torch.uint8),
+                            ("scores", (4,), torch.int16), ("honba", (), torch.int16),
+                            ("deposits", (), torch.int16), ("shanten", (), torch.int8),
+                            ("round_wind", (), torch.uint8), ("seat_wind", (), torch.uint8),
+                            ("kyoku", (), torch.uint8), ("dora_indicator_tokens", (5,), torch.uint8),
+                            ("live_wall", (), torch.uint8), ("riichi_flags", (4,), torch.uint8)):
+        size = torch.tensor([], dtype=dt).element_size()
+        for d in shape:
+            size *= d
+        o[name] = buf[off:off + size * n].view(dt).view(n, *shape)
+        off += size * n
+    assert off == OBS_BYTES * n
+    return buf, Observations(o)
 
 
 def alloc_trajectory(steps: int, n: int, device) -> dict:
@@ -340,14 +366,23 @@ class HostStepper:
 
     Host result views (valid after `step()` returns): rewards f32[n,4],
     legal_bits i32[n,4], next_actions i32[n], current_player i8[n],
-    terminated / truncated / status u8[n].
+    terminated / truncated / status u8[n]; with `obs_to_host` (and
+    `observe`) also `observations`, the current player's observation of
+    every env (observe.py:81-124) in pinned host memory, written by the
+    same kernel over the host link.
     """
 
     BYTES_PER_ENV = 40
 
     def __init__(self, env: BatchEnv, *, autoreset: bool = True, observe: bool = True, policy: bool = True,
-                 graph: bool = True, zero_copy: bool | str = True):
+                 graph: bool = True, zero_copy: bool | str = True, obs_to_host: bool = False):
         n, dev = env.n, env.device
+        self.observations = None
+        self._obs_host = None
+        if obs_to_host:
+            if not observe:
+                raise ValueError("obs_to_host needs observe=True")
+            self._obs_host, self.observations = alloc_observations_block(n, pinned=True)
         self.env = env
         self.n = n
         self.autoreset, self.observe, self.policy = autoreset, observe, policy
@@ -377,7 +412,7 @@ class HostStepper:
             rewards=d["rewards"].data_ptr(), terminated=d["terminated"].data_ptr(),
             truncated=d["truncated"].data_ptr(), status=d["status"].data_ptr())
         self.bytes_h2d = 4 * n
-        self.bytes_d2h = self.BYTES_PER_ENV * n
+        self.bytes_d2h = self.BYTES_PER_ENV * n + (OBS_BYTES * n if obs_to_host else 0)
         self._graph = None
         if graph:
             # no eager warm-up: a step mutates the envs, and nothing in the
@@ -418,12 +453,18 @@ class HostStepper:
             "status": buf[39 * n:40 * n],
         }
 
+    def _obs_target(self) -> Observations:
+        if self.observations is not None:
+            return self.observations
+        env = self.env
+        if env._obs is None:
+            env._obs = alloc_observations(env.n, env.device)
+        return env._obs
+
     def _body(self):
         if self._packed:
             env = self.env
-            if env._obs is None:
-                env._obs = alloc_observations(env.n, env.device)
-            ost = obs_struct(env._obs) if self.observe else None
+            ost = obs_struct(self._obs_target()) if self.observe else None
             flags = (1 if self.autoreset else 0) | (2 if self.observe else 0)
             check(env._L.rs_step_rec_out(env._h, self.actions.data_ptr(), flags, self._res_host.data_ptr(),
                                          C.byref(ost) if ost is not None else None, env._stream()),
@@ -431,9 +472,7 @@ class HostStepper:
             return
         if self.zero_copy != "none":
             env = self.env
-            if env._obs is None:
-                env._obs = alloc_observations(env.n, env.device)
-            ost = obs_struct(env._obs) if self.observe else None
+            ost = obs_struct(self._obs_target()) if self.observe else None
             flags = (1 if self.autoreset else 0) | (2 if self.observe else 0)
             check(env._L.rs_step_ex(env._h, self.actions.data_ptr(), flags, C.byref(self._out),
                                     C.byref(ost) if ost is not None else None,
@@ -443,6 +482,8 @@ class HostStepper:
                 self._res_host.copy_(self._res_dev, non_blocking=True)
             return
         self._act_dev.copy_(self.actions, non_blocking=True)
+        if self.observations is not None:
+            self.env._obs = self.observations  # written over the host link
         self.env.step(self._act_dev, autoreset=self.autoreset, observe=self.observe,
                       next_actions=self._dev_views["next_actions"] if self.policy else None, out=self._out)
         self._res_host.copy_(self._res_dev, non_blocking=True)
@@ -460,3 +501,7 @@ class HostStepper:
         self.launch()
         torch.cuda.current_stream(self.env.device).synchronize()
         return self
+
+    def close(self):
+        """drop the captured graph (the pinned buffers go with the object)"""
+        self._graph = None

@@ -92,3 +92,29 @@ def test_masked_sampling_is_always_legal():
         env.step(a.int(), autoreset=True, observe=True)
         torch.cuda.synchronize()
         assert int(env.status.sum().item()) == 0  # no illegal / contract status
+
+
+def test_ppo_two_ranks_on_one_gpu_gloo():
+    """the DDP path (configs[4] across GPUs): two ranks sharing one B200
+    over gloo, env shards by global index, gradients all-reduced by DDP,
+    env steps and games summed over ranks by paper_2605_20577_b200.dist"""
+    import json
+    import os
+    import socket
+    import subprocess
+    import sys
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2", "--master-addr",
+           "127.0.0.1", "--master-port", str(port), str(ROOT / "examples" / "ppo_selfplay.py"), "--envs", "128",
+           "--horizon", "16", "--iters", "2", "--epochs", "1", "--minibatch", "1024", "--dist-backend", "gloo"]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT, env=dict(os.environ, OMP_NUM_THREADS="1"))
+    assert r.returncode == 0, r.stderr[-3000:]
+    outs = [json.loads(ln) for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(outs) == 2 and {o["rank"] for o in outs} == {0, 1}
+    for o in outs:
+        assert o["world"] == 2 and o["env_steps_all_ranks"] == 2 * 2 * 128 * 16
+        assert math.isfinite(o["last_loss"])
