@@ -260,7 +260,10 @@ typedef struct rs_handle rs_handle;
 const char* rs_last_error(void);
 int rs_abi_version(void);
 
-/* tables (host-built once per process, uploaded per handle) */
+/* tables (host-built once per process, uploaded per handle).  A blob is
+ * loaded before the tables are first used (built, queried or uploaded by
+ * rs_create); afterwards an identical blob is a no-op and a different one
+ * is rejected with RS_E_TABLES (live tables are never replaced). */
 int rs_tables_build(void);
 int rs_tables_load(const uint8_t* blob, int64_t size);
 int rs_tables_blob(uint8_t* out, int64_t cap, int64_t* size);
@@ -361,9 +364,15 @@ int rs_autoreset(rs_handle* h, const rs_step_out* out, void* stream);
  * OR-ed into flags_dev[n] (u32, device), so calls accumulate. */
 int rs_check_invariants(rs_handle* h, int32_t fast, uint32_t* flags_dev, void* stream);
 
+/* Synchronous projection-record I/O (parity harness, sessions, crafted
+ * states).  Each call first waits for all work on the handle's device
+ * (cudaDeviceSynchronize, so steps launched on any stream, blocking or
+ * not, are complete), then copies; the caller's current device is kept.
+ * rs_export_envs: records of envs[0..count) (host indices) into
+ * out[count] (host).  rs_import_env rejects a record whose fields do not
+ * fit the device layout (counts, tile ids, packed-header widths) with
+ * RS_E_ARG. */
 int rs_export_env(rs_handle* h, int64_t env, rs_env_rec* out);
-/* records of envs[0..count) (host indices) into out[count] (host); waits
- * for the device like rs_export_env */
 int rs_export_envs(rs_handle* h, const int64_t* envs, int64_t count, rs_env_rec* out);
 int rs_import_env(rs_handle* h, int64_t env, const rs_env_rec* in);
 /* WinContext (scoring/context.py:19-57) as plain data: the parity

@@ -273,7 +273,8 @@ __device__ __forceinline__ void prefetch_env(const Soa& S, int e, int sub, int G
 // copy completing on the slot's mbarrier, the step runs on shared memory,
 // and the block moves back with one bulk copy (bulk_group).
 __device__ __forceinline__ uint32_t slot_off(int slot, int glog2) {  // after the shuffle scratch
-  return (uint32_t)WALL_SLOT_OFF + (uint32_t)scratch_bytes((int)blockDim.x, glog2) + (uint32_t)slot * SLOT_BYTES;
+  const uint32_t o = (uint32_t)WALL_SLOT_OFF + (uint32_t)scratch_bytes((int)blockDim.x, glog2) + (uint32_t)slot * SLOT_BYTES;
+  return o;
 }
 __device__ __forceinline__ uint32_t smem_addr(uint32_t off) {
   return (uint32_t)__cvta_generic_to_shared(g_smem) + off;
@@ -285,6 +286,7 @@ __device__ __forceinline__ void slot_bar_init(uint32_t sb) {
 }
 // one thread of the env's lane group issues the copy ...
 __device__ __forceinline__ void stage_issue(const Soa& S, int e, uint32_t sb) {
+  RS_CHECK((unsigned)e < (unsigned)S.n && sb % 16u == 0 && sb + SLOT_BYTES <= rs::dyn_smem_bytes());
   const uint32_t dst = smem_addr(sb), bar = smem_addr(sb + SLOT_BAR);
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(BLK_BYTES) : "memory");
   asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
@@ -662,6 +664,9 @@ __global__ void __launch_bounds__(BLOCK) k_check(const __grid_constant__ Soa S, 
   if (e >= S.n) return;
   Engine E(S, T, C, e, S.blk + (size_t)e * BLK_BYTES);
   E.load();
+#if defined(RS_BOUNDS)
+  if (fast == 2) (void)E.wall(RS_NUM_TILES);  // bounds-build canary: must trap (tools/bounds_check.sh)
+#endif
   const uint32_t bad = check_invariants(E, fast != 0);
   if (bad) flags[e] |= bad;
 }
@@ -674,22 +679,15 @@ __global__ void k_expand(const uint32_t* bits, uint8_t* bools, int n) {
   bools[i] = (uint8_t)((bits[e * 4 + (a >> 5)] >> (a & 31)) & 1u);
 }
 
-__global__ void k_export(const __grid_constant__ Soa S, const __grid_constant__ DevTables D,
-    const __grid_constant__ Cfg C, int e, rs_env_rec* out) {
-  const Tabs T = stage_tables(D);
-  if (threadIdx.x != 0) return;
-  Engine E(S, T, C, e, S.blk + (size_t)e * BLK_BYTES);
-  export_env(E, C, *out);
-}
-
-// one CTA per listed env: the records of many envs in one launch and one copy
-__global__ void k_export_many(const __grid_constant__ Soa S, const __grid_constant__ DevTables D,
-    const __grid_constant__ Cfg C, const int64_t* envs, rs_env_rec* out) {
-  const Tabs T = stage_tables(D);
-  if (threadIdx.x != 0) return;
-  const int e = (int)envs[blockIdx.x];
-  Engine E(S, T, C, e, S.blk + (size_t)e * BLK_BYTES);
-  export_env(E, C, out[blockIdx.x]);
+// the projection records of envs[0..count) (export_env reads no tables):
+// one thread per listed env, so many envs cost one launch and one copy
+__global__ void k_export_many(const __grid_constant__ Soa S, const __grid_constant__ Cfg C, const int64_t* envs,
+                              int64_t count, rs_env_rec* out) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= count) return;
+  const int e = (int)envs[i];
+  Engine E(S, Tabs{}, C, e, S.blk + (size_t)e * BLK_BYTES);
+  export_env(E, C, out[i]);
 }
 
 __global__ void k_import(const __grid_constant__ Soa S, const __grid_constant__ DevTables D,
@@ -767,6 +765,7 @@ struct rs_handle {
   uint32_t* legal_bits_tmp;  // step output when the caller asks only for bools
   rs_env_rec* rec_dev;
   void* export_buf = nullptr;  // rs_export_envs: records + env list, grown on demand
+  std::mutex export_mu;        // export_buf / rec_dev: export and import calls from several threads
   size_t export_cap = 0;
   int num_sms;
   int occ_key[16], occ_val[16];  // resident stepping-kernel CTAs per SM per (block, smem)
@@ -994,6 +993,61 @@ int finish_step_out(rs_handle* h, const rs_step_out* o, cudaStream_t st) {
 
 }  // namespace
 
+// the fields of an imported record must fit the device layout (bit widths
+// of the packed header, array slots): the name of the first that does not
+namespace {
+const char* record_out_of_range(const rs_env_rec& r) {
+  auto tile_or_none = [](int t) { return t >= -1 && t < RS_NUM_TILES; };
+  for (int i = 0; i < RS_NUM_TILES; i++)
+    if (r.wall[i] >= RS_NUM_TILES) return "wall";
+  if (r.kan_draws < 0 || r.kan_draws > 4) return "kan_draws";
+  if (r.cursor < 0 || r.cursor > 122 - r.kan_draws) return "cursor";
+  if (r.dora_count < 1 || r.dora_count > 5) return "dora_count";
+  for (int s = 0; s < 4; s++) {
+    const rs_hand_rec& hr = r.hands[s];
+    if (hr.n_concealed > 14) return "hands.n_concealed";
+    for (int i = 0; i < hr.n_concealed; i++)
+      if (hr.concealed[i] >= RS_NUM_TILES) return "hands.concealed";
+    if (hr.n_melds > 4) return "hands.n_melds";
+    for (int i = 0; i < hr.n_melds; i++) {
+      const rs_meld_rec& m = hr.melds[i];
+      if (m.type < 0 || m.type > 4 || m.n_tiles < 3 || m.n_tiles > 4 || m.from_seat < -1 || m.from_seat > 3 ||
+          !tile_or_none(m.called_tile))
+        return "hands.melds";
+      for (int j = 0; j < m.n_tiles; j++)
+        if (m.tiles[j] >= RS_NUM_TILES) return "hands.melds.tiles";
+    }
+    // a discard appends one entry: keep a free slot
+    if (hr.n_river < 0 || hr.n_river >= RS_MAX_RIVER) return "hands.n_river";
+    for (int i = 0; i < hr.n_river; i++)
+      if (hr.river_tile[i] >= RS_NUM_TILES || hr.river_flags[i] > 7) return "hands.river";
+    if (hr.riichi < 0 || hr.riichi > 2 || hr.riichi_index < -1 || hr.riichi_index >= RS_MAX_RIVER) return "hands.riichi";
+  }
+  if (r.kyoku < 0 || r.kyoku > 7) return "kyoku";
+  if (r.honba < 0 || r.honba > 255 || r.deposits < 0 || r.deposits > 255 || r.repeats < 0 || r.repeats > 255)
+    return "honba / deposits / repeats";
+  if (r.phase < 0 || r.phase > 2 || r.actor < 0 || r.actor > 3 || r.current_player < 0 || r.current_player > 3)
+    return "phase / actor";
+  if (!tile_or_none(r.drawn) || !tile_or_none(r.call_tile) || r.call_from < -1 || r.call_from > 3 ||
+      r.kakan_kind < -1 || r.kakan_kind >= RS_NUM_KINDS)
+    return "drawn / call state";
+  if (r.n_queue < 0 || r.n_queue > 5) return "n_queue";
+  for (int i = 0; i < r.n_queue; i++)
+    if (r.queue_seat[i] < 0 || r.queue_seat[i] > 3 || r.queue_stage[i] < 0 || r.queue_stage[i] > 2) return "queue";
+  if (r.n_rons < 0 || r.n_rons > 3) return "n_rons";
+  for (int i = 0; i < r.n_rons; i++)
+    if (r.rons[i] < 0 || r.rons[i] > 3) return "rons";
+  if (r.pending_dora < 0 || r.pending_dora > 4) return "pending_dora";
+  if (r.n_results < 0 || r.n_results > 255 || r.events_len < 0 || r.step_count < 0) return "counters";
+  const int cnt = r.events_len < RS_EVENT_WINDOW ? r.events_len : RS_EVENT_WINDOW;
+  for (int i = 0; i < cnt; i++)
+    if (r.events[i][0] < 0 || r.events[i][0] > 11 || r.events[i][1] < -1 || r.events[i][1] > 3 ||
+        !tile_or_none(r.events[i][2]))
+      return "events";
+  return nullptr;
+}
+}  // namespace
+
 extern "C" {
 
 const char* rs_last_error(void) { return g_err.c_str(); }
@@ -1005,6 +1059,8 @@ int rs_tables_build(void) {
 }
 int rs_tables_load(const uint8_t* blob, int64_t size) {
   const int rc = host_tables_load(blob, size);
+  if (rc == -5) return set_err(RS_E_TABLES, "suit tables already in use (built or loaded); a different blob must be "
+                                         "loaded before the first handle or table query");
   return rc ? set_err(rc, "suit-table blob rejected (magic, cardinality or crc)") : 0;
 }
 int rs_tables_blob(uint8_t* out, int64_t cap, int64_t* size) {
@@ -1046,7 +1102,7 @@ int rs_create(rs_handle** out, int64_t n_envs, const rs_config* cfg, int32_t dev
   if (cfg->illegal_penalty > 0.f) return set_err(RS_E_ARG, "illegal penalty must be <= 0");
   if (cfg->max_steps <= 0 || cfg->max_steps > 65535) return set_err(RS_E_ARG, "max_steps out of range");
   const HostTables& H = host_tables();
-  CUDA_TRY(cudaSetDevice(device));
+  const DeviceScope device_scope(device);
   rs_handle* h = new rs_handle();
   h->device = device;
   h->n = (int)n_envs;
@@ -1107,7 +1163,6 @@ int rs_create(rs_handle** out, int64_t n_envs, const rs_config* cfg, int32_t dev
   if ((err = cudaMalloc(&h->sort_tmp, std::max<size_t>(h->sort_tmp_bytes, 16)))) return cleanup(err, "sort scratch");
   const void* kernels[] = {(const void*)k_init, (const void*)k_step, (const void*)k_policy,
                            (const void*)k_observe, (const void*)k_rollout<false>, (const void*)k_rollout<true>,
-                           (const void*)k_export,
                            (const void*)k_import, (const void*)k_autoreset, (const void*)k_check};
   for (const void* k : kernels)
     if ((err = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_staged(ROLL_BLOCK, ROLL_BLOCK))))
@@ -1141,7 +1196,7 @@ int rs_create(rs_handle** out, int64_t n_envs, const rs_config* cfg, int32_t dev
 
 int rs_destroy(rs_handle* h) {
   if (!h) return 0;
-  cudaSetDevice(h->device);
+  const DeviceScope device_scope(h->device);
   cudaFree(h->mem);
   cudaFree(h->sort_tmp);
   cudaFree(h->export_buf);
@@ -1325,13 +1380,7 @@ int rs_autoreset(rs_handle* h, const rs_step_out* out, void* stream) {
 
 int rs_export_env(rs_handle* h, int64_t env, rs_env_rec* out) {
   if (!h || !out || env < 0 || env >= h->n) return set_err(RS_E_ARG, "rs_export_env: bad arguments");
-  CUDA_TRY(cudaSetDevice(h->device));
-  // fields export_env leaves unwritten (padding, slots past the counts) read as zero
-  CUDA_TRY(cudaMemset(h->rec_dev, 0, sizeof(rs_env_rec)));
-  k_export<<<1, 32, smem_for(32)>>>(h->S, h->D, h->cfg, (int)env, h->rec_dev);
-  CUDA_TRY(cudaGetLastError());
-  CUDA_TRY(cudaMemcpy(out, h->rec_dev, sizeof(rs_env_rec), cudaMemcpyDeviceToHost));
-  return 0;
+  return rs_export_envs(h, &env, 1, out);
 }
 
 int rs_export_envs(rs_handle* h, const int64_t* envs, int64_t count, rs_env_rec* out) {
@@ -1340,7 +1389,10 @@ int rs_export_envs(rs_handle* h, const int64_t* envs, int64_t count, rs_env_rec*
   for (int64_t i = 0; i < count; i++)
     if (envs[i] < 0 || envs[i] >= h->n) return set_err(RS_E_ARG, "rs_export_envs: env %lld out of range", (long long)envs[i]);
   if (count == 0) return 0;
-  CUDA_TRY(cudaSetDevice(h->device));
+  const DeviceScope device_scope(h->device);
+  std::lock_guard<std::mutex> lk(h->export_mu);  // the export buffer is shared by the handle's callers
+  // steps may have been launched on any stream, blocking or not
+  CUDA_TRY(cudaDeviceSynchronize());
   const size_t rec_bytes = (size_t)count * sizeof(rs_env_rec);
   const size_t need = rec_bytes + (size_t)count * sizeof(int64_t);
   if (need > h->export_cap) {
@@ -1353,9 +1405,10 @@ int rs_export_envs(rs_handle* h, const int64_t* envs, int64_t count, rs_env_rec*
   rs_env_rec* d_out = (rs_env_rec*)h->export_buf;
   int64_t* d_envs = (int64_t*)((char*)h->export_buf + rec_bytes);
   cudaError_t e = cudaMemcpy(d_envs, envs, (size_t)count * sizeof(int64_t), cudaMemcpyHostToDevice);
-  if (e == cudaSuccess) e = cudaMemset(d_out, 0, rec_bytes);  // as rs_export_env
+  // fields export_env leaves unwritten (padding, slots past the counts) read as zero
+  if (e == cudaSuccess) e = cudaMemset(d_out, 0, rec_bytes);
   if (e == cudaSuccess) {
-    k_export_many<<<(unsigned)count, 32, smem_for(32)>>>(h->S, h->D, h->cfg, d_envs, d_out);
+    k_export_many<<<(unsigned)((count + 127) / 128), 128>>>(h->S, h->cfg, d_envs, count, d_out);
     e = cudaGetLastError();
   }
   if (e == cudaSuccess) e = cudaMemcpy(out, d_out, rec_bytes, cudaMemcpyDeviceToHost);
@@ -1366,7 +1419,10 @@ int rs_export_envs(rs_handle* h, const int64_t* envs, int64_t count, rs_env_rec*
 int rs_import_env(rs_handle* h, int64_t env, const rs_env_rec* in) {
   if (!h || !in || env < 0 || env >= h->n) return set_err(RS_E_ARG, "rs_import_env: bad arguments");
   if (in->abi_version != RS_ABI_VERSION) return set_err(RS_E_ARG, "record abi version mismatch");
-  CUDA_TRY(cudaSetDevice(h->device));
+  if (const char* bad = record_out_of_range(*in)) return set_err(RS_E_ARG, "rs_import_env: %s out of range", bad);
+  const DeviceScope device_scope(h->device);
+  std::lock_guard<std::mutex> lk(h->export_mu);  // rec_dev
+  CUDA_TRY(cudaDeviceSynchronize());
   CUDA_TRY(cudaMemcpy(h->rec_dev, in, sizeof(rs_env_rec), cudaMemcpyHostToDevice));
   k_import<<<1, 32, smem_for(32)>>>(h->S, h->D, h->cfg, (int)env, h->rec_dev);
   CUDA_TRY(cudaGetLastError());

@@ -25,7 +25,44 @@ struct alignas(16) int4 { int x, y, z, w; };
 inline uint4 make_uint4(uint32_t x, uint32_t y, uint32_t z, uint32_t w) { return uint4{x, y, z, w}; }
 #endif
 
+// -DRS_BOUNDS: bounds checks on every state-array index, wall position,
+// meld / river slot and shared-memory scratch / stage offset; a violation
+// traps the kernel (abort() in the host build).  compute-sanitizer is not
+// available on the measurement pool, so the parity suite runs against this
+// build (tools/bounds_check.sh) and the host build runs under ASan / UBSan
+// (tests/test_hostcheck_sanitized.py).  Off in the shipped library.
+#if defined(RS_BOUNDS)
+#if defined(__CUDA_ARCH__)
+#define RS_CHECK(c) \
+  do {              \
+    if (!(c)) __trap(); \
+  } while (0)
+#else
+#include <stdlib.h>
+#define RS_CHECK(c) \
+  do {              \
+    if (!(c)) abort(); \
+  } while (0)
+#endif
+#else
+#define RS_CHECK(c) ((void)0)
+#endif
+
 namespace rs {
+
+#if defined(__CUDACC__)
+// dynamic shared memory of the running CTA (RS_BOUNDS checks of scratch /
+// stage offsets)
+__device__ __forceinline__ uint32_t dyn_smem_bytes() {
+#if defined(__CUDA_ARCH__)
+  uint32_t v;
+  asm("mov.u32 %0, %%dynamic_smem_size;" : "=r"(v));
+  return v;
+#else
+  return 0u;
+#endif
+}
+#endif
 
 // -DRS_PROFILE_MARKS=3: per-thread cycle accumulators of selected functions
 // (profiling builds only; g_marks[thread][8])

@@ -131,7 +131,10 @@ struct Engine {
 
   // ------------------------------------------------------------- memory
   // 32-bit index math: rs_create bounds n so that 160 * n < 2^31
-  RS_HD uint32_t at(int f) const { return (uint32_t)f * (uint32_t)S.n + (uint32_t)e; }
+  RS_HD uint32_t at(int f) const {
+    RS_CHECK((unsigned)f < 4u * RS_MAX_RIVER && (unsigned)e < (unsigned)S.n);
+    return (uint32_t)f * (uint32_t)S.n + (uint32_t)e;
+  }
   RS_HD void load() {
     const int4 sc = *reinterpret_cast<const int4*>(&squad(bp, W_SCORES));
     g.unpack(squad(bp, W_HDR), squad(bp, W_HDR + 4), squad(bp, W_HDR + 8), squad(bp, W_HDR + 12), sc);
@@ -143,7 +146,10 @@ struct Engine {
     squad(bp, W_HDR) = a; squad(bp, W_HDR + 4) = b; squad(bp, W_HDR + 8) = c; squad(bp, W_HDR + 12) = d;
     *reinterpret_cast<int4*>(&squad(bp, W_SCORES)) = sc;
   }
-  RS_HD int wall(int pos) const { return swall(bp)[pos]; }
+  RS_HD int wall(int pos) const {
+    RS_CHECK((unsigned)pos < (unsigned)RS_NUM_TILES);
+    return swall(bp)[pos];
+  }
   RS_HD int tok() const { return C.rule == RS_RULE_RED ? 1 : 0; }  // hand_put / hand_take token mode
   RS_HD uint32_t info(int s) const { return sword(bp, W_HINFO + s); }
   RS_HD void set_info(int s, uint32_t v) const { sword(bp, W_HINFO + s) = v; }
@@ -151,8 +157,14 @@ struct Engine {
   RS_HD int count_of(int s, int k) const {
     return popc32((sword(bp, W_HMASK + 5 * s + (k >> 3)) >> ((k & 7) * 4)) & 0xFu);
   }
-  RS_HD uint32_t meld_info(int s, int i) const { return S.minfo[at(s * 4 + i)]; }
-  RS_HD uint32_t meld_tiles(int s, int i) const { return S.mtiles[at(s * 4 + i)]; }
+  RS_HD uint32_t meld_info(int s, int i) const {
+    RS_CHECK((unsigned)s < 4u && (unsigned)i < 4u);
+    return S.minfo[at(s * 4 + i)];
+  }
+  RS_HD uint32_t meld_tiles(int s, int i) const {
+    RS_CHECK((unsigned)s < 4u && (unsigned)i < 4u);
+    return S.mtiles[at(s * 4 + i)];
+  }
 
   // engine.py:100-102 (64-slot ring; the full history is reconstructed by
   // the host while stepping)
@@ -178,6 +190,7 @@ struct Engine {
     const int G = grp_size();
     uint8_t* const w = G > 1 ? g_smem + WALL_SLOT_OFF + (threadIdx.x >> s_grp_log2) * ENV_SCRATCH
                              : g_smem + WALL_SLOT_OFF + threadIdx.x * SCRATCH_STRIDE;
+    RS_CHECK((uint32_t)(w - g_smem) + (uint32_t)(G > 1 ? ENV_SCRATCH : SCRATCH_STRIDE) <= dyn_smem_bytes());
     if (G > 1) {
       // lane group: one wall copy per env; the lanes draw the 135 targets in
       // parallel, then lane 0 runs the swap chain alone (no redundant copies,
@@ -774,6 +787,7 @@ struct Engine {
     }
     int ipp = hi::ippatsu(h.info);
     if (hi::riichi(h.info) && !declaring && ipp) ipp = 0;
+    RS_CHECK((unsigned)seat < 4u && (unsigned)nriver < (unsigned)RS_MAX_RIVER);
     S.river[at(seat * RS_MAX_RIVER + nriver)] =
         (uint16_t)(tile | ((tsumogiri ? RS_RIVER_TSUMOGIRI : 0) | (declaring ? RS_RIVER_RIICHI : 0)) << 8);
     sdword(bp, W_HRKIND + 2 * seat) |= 1ull << (tile >> 2);
@@ -807,6 +821,7 @@ struct Engine {
   RS_HD void mark_called_tile() {
     const int d = g.call_from;
     const int idx = hi::nriver(info(d)) - 1;
+    RS_CHECK((unsigned)d < 4u && (unsigned)idx < (unsigned)RS_MAX_RIVER);
     uint16_t& rt = S.river[at(d * RS_MAX_RIVER + idx)];
     rt = (uint16_t)(rt | (RS_RIVER_CALLED << 8));
   }
@@ -833,6 +848,7 @@ struct Engine {
     uint32_t packed = 0;
     for (int i = 0; i < nids; i++) packed |= (uint32_t)t[i] << (8 * i);
     const int nm = hi::nmelds(h.info);
+    RS_CHECK((unsigned)seat < 4u && (unsigned)nm < 4u && nids >= 3 && nids <= 4);
     S.mtiles[at(seat * 4 + nm)] = packed;
     S.minfo[at(seat * 4 + nm)] = mi::make(type, nids, from, called);
     h.info = hi::set_nmelds(h.info, nm + 1);

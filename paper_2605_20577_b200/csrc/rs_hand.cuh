@@ -369,6 +369,7 @@ RS_HD void finish_hand(const Tabs& T, Hand& h) {
 // add / remove one tile without the rebuild (hand_add / hand_remove parts)
 // tok: 0 no-red tokens, 1 red-rule tokens, -1 scratch copy (tokens unused)
 RS_HD void hand_put(const Tabs& T, Hand& h, int t, int tok) {
+  RS_CHECK((unsigned)t < (unsigned)RS_NUM_TILES && !h.has(t) && hi::nconc(h.info) < 14);
   const int k = t >> 2, s = kind_suit(k);
   h.set_word(t >> 5, h.word(t >> 5) | (1u << (t & 31)));
   const uint32_t nc = h.code(s) + kind_pow(k);
@@ -378,6 +379,7 @@ RS_HD void hand_put(const Tabs& T, Hand& h, int t, int tok) {
   if (tok >= 0) tok_insert(h.tlo, h.thi, token_of(t, tok == 1));
 }
 RS_HD void hand_take(const Tabs& T, Hand& h, int t, int tok) {
+  RS_CHECK((unsigned)t < (unsigned)RS_NUM_TILES && h.has(t) && hi::nconc(h.info) > 0);
   const int k = t >> 2, s = kind_suit(k);
   h.set_word(t >> 5, h.word(t >> 5) & ~(1u << (t & 31)));
   const uint32_t nc = h.code(s) - kind_pow(k);

@@ -201,12 +201,14 @@ struct Game {
   RS_HD int qseat(int i) const { return (queue >> (3 + 4 * i)) & 3; }
   RS_HD int qstage(int i) const { return (queue >> (5 + 4 * i)) & 3; }
   RS_HD void qset(int n, const int* seats, const int* stages) {
+    RS_CHECK(n >= 0 && n <= 5);
     uint32_t q = (uint32_t)n;
     for (int i = 0; i < n; i++) q |= ((uint32_t)seats[i] | ((uint32_t)stages[i] << 2)) << (3 + 4 * i);
     queue = q;
   }
   RS_HD void qpop() {
     int n = qn();
+    RS_CHECK(n > 0);
     uint32_t entries = (queue >> 7) & 0xFFFFu;
     queue = (uint32_t)(n - 1) | (entries << 3);
   }
@@ -214,6 +216,7 @@ struct Game {
   RS_HD int rseat(int i) const { return (rons >> (2 + 2 * i)) & 3; }
   RS_HD void rpush(int s) {
     int n = rn();
+    RS_CHECK(n < 3 && (unsigned)s < 4u);
     rons = (rons & ~3u) | (uint32_t)(n + 1) | ((uint32_t)s << (2 + 2 * n));
   }
   RS_HD int dealer() const { return kyoku % 4; }

@@ -265,6 +265,13 @@ int host_tables_load(const uint8_t* blob, int64_t size) {
   finalize(T, sd, hd);
   if (T.ns != NS || T.nh != NH || T.na != NA || T.nb != NB) return -4;
   std::lock_guard<std::mutex> lk(g_mu);
+  if (g_tables.ready) {
+    // tables already built / loaded: host_tables() hands out references and
+    // device copies are made once per device, so the live tables are never
+    // replaced; an identical blob is a no-op, a different one an error
+    const bool same = T.suit_words == g_tables.suit_words && T.honor_words == g_tables.honor_words;
+    return same ? 0 : -5;
+  }
   g_tables = std::move(T);
   return 0;
 }

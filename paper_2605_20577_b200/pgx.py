@@ -17,9 +17,11 @@ through `BatchEnv`.
 from __future__ import annotations
 
 import ctypes as C
+import threading
 from dataclasses import dataclass, field
 
 import numpy as np
+
 import torch
 
 from . import abi, records
@@ -99,22 +101,29 @@ class EnvState:
 
 
 class _Runner:
-    """one batch-of-1 device handle per (config, device)"""
+    """one batch-of-1 device handle per (config, device), shared by every
+    caller of the facade; `lock` is held from loading a state through
+    reading the result, so threads stepping different games (the
+    reference's service runs sync handlers in a threadpool) never see each
+    other's state"""
 
     _cache: dict = {}
+    _cache_lock = threading.Lock()
 
     def __init__(self, config: EnvConfig, device):
         self.env = BatchEnv(1, config, device=device)
         self.obs = alloc_observations(1, self.env.device)
         self.current: EnvState | None = None  # the state the handle holds
+        self.lock = threading.RLock()
 
     @classmethod
     def get(cls, config: EnvConfig, device=None) -> "_Runner":
         dev = torch.device(device if device is not None else "cuda")
         key = (config, str(dev))
-        if key not in cls._cache:
-            cls._cache[key] = cls(config, dev)
-        return cls._cache[key]
+        with cls._cache_lock:
+            if key not in cls._cache:
+                cls._cache[key] = cls(config, dev)
+            return cls._cache[key]
 
     def load(self, state: EnvState):
         if self.current is not state:
@@ -163,9 +172,10 @@ def _wrap(config: EnvConfig, rec: abi.rs_env_rec, events, results, game_legal=No
 def init(seed: int, config: EnvConfig = EnvConfig(), device=None) -> EnvState:
     """env/core.py:81-82"""
     r = _Runner.get(config, device)
-    r.env.init(torch.tensor([_signed64(seed)], dtype=torch.int64))
-    st = _initial(config, r.env.export(0))
-    r.current = st
+    with r.lock:
+        r.env.init(torch.tensor([_signed64(seed)], dtype=torch.int64))
+        st = _initial(config, r.env.export(0))
+        r.current = st
     return st
 
 
@@ -184,11 +194,13 @@ def step(state: EnvState, action: int) -> EnvState:
     if state.terminated or state.truncated:
         raise ContractError("cannot step a finished episode")
     r = _Runner.get(state.config, None)
-    r.load(state)
     acts = torch.tensor([_action32(action)], dtype=torch.int32)
-    r.env.step(acts)
-    st = _advance(state, r.env.export(0))
-    r.current = st
+    with r.lock:
+        r.load(state)
+        r.env.step(acts)
+        rec = r.env.export(0)
+        st = _advance(state, rec)
+        r.current = st
     return st
 
 
@@ -221,10 +233,12 @@ def observe(state: EnvState, seat: int) -> Observation:
     if not 0 <= seat <= 3:
         raise ValueError(f"bad seat {seat}")
     r = _Runner.get(state.config, None)
-    r.load(state)
-    seats = torch.tensor([seat], dtype=torch.int8, device=r.env.device)
-    o = r.env.observe(seats, out=r.obs)
-    torch.cuda.synchronize(r.env.device)
+    with r.lock:
+        r.load(state)
+        seats = torch.tensor([seat], dtype=torch.int8, device=r.env.device)
+        o = r.env.observe(seats, out=r.obs)
+        torch.cuda.synchronize(r.env.device)
+        o = {k: v.cpu() for k, v in o.items()}
     ev = o["event_tokens"][0].tolist()
     return Observation(
         hand_tokens=tuple(o["hand_tokens"][0].tolist()), event_tokens=tuple(tuple(e) for e in ev),
@@ -245,9 +259,10 @@ def heuristic_policy(state: EnvState, legal: tuple | None = None) -> int:
     if not state.legal:
         raise ValueError("no legal actions")
     r = _Runner.get(state.config, None)
-    r.load(state)
-    a = r.env.heuristic_actions()
-    return int(a[0].item())
+    with r.lock:
+        r.load(state)
+        a = r.env.heuristic_actions()
+        return int(a[0].item())
 
 
 # --- rng.py:18-65 and policies.py:17-22 on the host (pure functions) ---

@@ -3,6 +3,7 @@
 from __future__ import annotations
 
 import ctypes as C
+import os
 import subprocess
 from pathlib import Path
 
@@ -15,8 +16,11 @@ _lib = None
 def lib():
     global _lib
     if _lib is None:
-        subprocess.check_call(["make", "-s", "-C", str(_HERE)])
-        L = C.CDLL(str(_HERE / "libhostcheck.so"))
+        # HOSTCHECK_LIB: another build of the same source (the sanitized one,
+        # tests/test_hostcheck_sanitized.py)
+        name = os.environ.get("HOSTCHECK_LIB", "libhostcheck.so")
+        subprocess.check_call(["make", "-s", "-C", str(_HERE), name])
+        L = C.CDLL(str(_HERE / name))
         vp = C.c_void_p
         L.hc_create.restype = vp
         L.hc_create.argtypes = [C.c_int, vp]

@@ -19,7 +19,12 @@ struct HC {
   Soa S;
   Tabs T;
   Cfg C;
-  std::vector<char> mem;
+  // one allocation per array, so the sanitized build
+  // (tests/test_hostcheck_sanitized.py) sees an overrun of any of them
+  std::vector<void*> parts;
+  ~HC() {
+    for (void* p : parts) free(p);
+  }
 };
 
 extern "C" {
@@ -30,7 +35,6 @@ void* hc_create(int n, const rs_config* cfg) {
   h->C = Cfg{cfg->rule, cfg->mode, cfg->reward_scheme, cfg->illegal_penalty, cfg->max_steps,
              cfg->kazoe, cfg->double_yakuman, cfg->agari_yame, cfg->renchan_cap};
   h->T = Tabs{ht.suit_cls.data(), ht.honor_cls.data(), ht.t1.data(), ht.t2.data(), ht.t3.data()};
-  size_t off = 0;
   std::vector<std::pair<void**, size_t>> plan;
   Soa& S = h->S;
   S.n = n;
@@ -41,13 +45,12 @@ void* hc_create(int n, const rs_config* cfg) {
   plan.push_back({(void**)&S.events, 64 * 2 * (size_t)n});
   plan.push_back({(void**)&S.evobs, (size_t)EVOBS_BYTES * n});
   plan.push_back({(void**)&S.results, sizeof(rs_result_rec) * (size_t)n});
-  for (auto& p : plan) off += (p.second + 255) & ~(size_t)255;
-  h->mem.assign(off + 256, 0);
-  char* base = (char*)(((uintptr_t)h->mem.data() + 255) & ~(uintptr_t)255);
-  off = 0;
   for (auto& p : plan) {
-    *p.first = base + off;
-    off += (p.second + 255) & ~(size_t)255;
+    void* m = nullptr;
+    if (posix_memalign(&m, 256, p.second)) abort();  // exact size: no slack past the array
+    memset(m, 0, p.second);
+    *p.first = m;
+    h->parts.push_back(m);
   }
   return h;
 }
