@@ -21,3 +21,17 @@ for cfg in "default RINSHAN_X=0" "stage1 RINSHAN_STAGE=1" "stage2 RINSHAN_STAGE=
       -p no:cacheprovider > $out/$1.log 2>&1
   echo "$1 ($2) rc=$? $(tail -1 $out/$1.log)" | tee -a $out/summary.txt
 done
+# canary: the bounds build must trap on a deliberate out-of-range wall read
+# (k_check with fast == 2 exists only under RS_BOUNDS)
+env RINSHAN_LIB=build_variants/bounds.so RINSHAN_NO_BUILD=1 timeout 300 python - > $out/canary.log 2>&1 <<'PY'
+import torch
+from paper_2605_20577_b200.env import BatchEnv, EnvConfig
+env = BatchEnv(64, EnvConfig()).init(seed=1)
+flags = torch.zeros(64, dtype=torch.int32, device="cuda")
+env._L.rs_check_invariants(env._h, 2, flags.data_ptr(), torch.cuda.current_stream().cuda_stream)
+torch.cuda.synchronize()
+print("canary NOT caught")
+PY
+rc=$?
+if [ $rc -ne 0 ] && ! grep -q "NOT caught" $out/canary.log; then echo "canary trapped (rc=$rc): ok" | tee -a $out/summary.txt
+else echo "canary NOT caught" | tee -a $out/summary.txt; fi
