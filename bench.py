@@ -424,7 +424,7 @@ def ncu_summary(rule: str, n: int):
         return None, None
     if pj.get("rule") != rule or pj.get("batch") != n:
         return None, None
-    extra = {k: pj[k] for k in ("warp_inst_per_env_step", "divergence") if k in pj}
+    extra = {k: pj[k] for k in ("warp_inst_per_env_step", "branch_efficiency", "divergence") if k in pj}
     extra["source"] = "profiles/ncu_rollout_summary.json (" + str(pj.get("report")) + ")"
     return pj.get("dram_bytes_per_launch"), {"ncu": extra}
 
