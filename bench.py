@@ -593,7 +593,8 @@ def e2e_run(args, env, dev, world, obs_to_host: bool):
     the random policy's next action) and writes the result (rewards, flags,
     player, packed legal mask, next action) -- and with `obs_to_host` the
     232-byte observation of every env -- into pinned host memory; one
-    CUDA-graph replay and a stream sync per step.  The host feeds the next
+    CUDA-graph replay per step, the host waiting on the completion word the
+    kernel writes after its last result store.  The host feeds the next
     actions back.  >= 100 timed steps."""
     import torch
 
@@ -606,10 +607,11 @@ def e2e_run(args, env, dev, world, obs_to_host: bool):
     hs = HostStepper(env, autoreset=True, observe=True, policy=True, obs_to_host=obs_to_host)
     env.random_actions(out=hs._act_dev)
     hs.actions.copy_(hs._act_dev.cpu())
+    acts, nxt = hs.actions.numpy(), hs.next_actions.numpy()  # views of the pinned buffers
 
     def one():
         hs.step()
-        hs.actions.copy_(hs.next_actions)  # host-side: the next step's inputs
+        acts[:] = nxt  # host-side: the next step's inputs
 
     for _ in range(max(3, args.warmup)):
         one()
@@ -630,7 +632,8 @@ def e2e_run(args, env, dev, world, obs_to_host: bool):
     res = {"value": value, "unit": UNIT, "h2d_bytes_per_step": hs.bytes_h2d, "d2h_bytes_per_step": hs.bytes_d2h,
            "api": "HostStepper.step (one-node CUDA graph: the fused step+autoreset+observe+policy kernel "
                   "reads the actions from and writes the result block"
-                  + (" and the observations" if obs_to_host else "") + " to mapped pinned host memory)",
+                  + (" and the observations" if obs_to_host else "") + " to mapped pinned host memory; the host "
+                  "polls the kernel's completion word)",
            "steps": steps}
     hs.close()
     return res

@@ -29,6 +29,8 @@
  *                                              launch + one copy; service/sessions.py
  *                                              state reads, batched sessions)
  *   rs_import_env     tests/engine_helpers.py:58-105 craft() (crafted states)
+ *   rs_set_done_flag  (no counterpart: the reference steps in-process) completion
+ *                                              word of host-driven steps (HostStepper)
  *   rs_debug_score    scoring/score.py:45-82   score_win(ctx, kazoe, double_yakuman)
  *                                              over WinContext (scoring/context.py:19-57),
  *                                              the device scorer alone (parity harness)
@@ -316,6 +318,13 @@ int rs_step_ex(rs_handle* h, const int32_t* actions_dev, int32_t flags, const rs
  * recs[n] (device or mapped pinned host memory) */
 int rs_step_rec_out(rs_handle* h, const int32_t* actions, int32_t flags, rs_step_rec* recs,
                     const rs_obs_out* obs, void* stream);
+/* Completion word for host-driven stepping: after every rs_step_ex /
+ * rs_step_rec_out launch, once all of its per-env outputs are visible to
+ * the host, the kernel writes an incremented sequence number into
+ * *host_flag (mapped pinned host memory), so a host thread can poll one
+ * word instead of sleeping in a stream synchronize.  The sequence
+ * continues from the word's value at this call; NULL turns it off. */
+int rs_set_done_flag(rs_handle* h, uint32_t* host_flag);
 /* seats_dev: device int8[n] or NULL for each env's current player */
 int rs_observe(rs_handle* h, const int8_t* seats_dev, const rs_obs_out* obs, void* stream);
 /* random policy over each env's legal list using its policy stream */

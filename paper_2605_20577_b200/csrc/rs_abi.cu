@@ -164,14 +164,16 @@ struct StepOut {
   uint8_t* status;
 };
 
-// stage the packed t3 | t1 | t2 block into shared memory; the engine reads
-// it at compile-time offsets (rs_hand.cuh t1_at / t2_at / t3_at).
+// -DRS_TABLES_SMEM: stage the packed t3 | t1 | t2 block into shared memory;
+// the engine reads it at compile-time offsets (rs_hand.cuh t1_at / t2_at /
+// t3_at).  Default build: the tables stay in global memory (read through
+// L1, kept in L2 by the persisting window) and these are no-ops.
 // One elected thread issues a single TMA bulk copy (cp.async.bulk, no tensor
 // map needed for a contiguous block) completing on an mbarrier; the other
 // warps spend no instructions on the copy and wait on the barrier phase.
 __shared__ __align__(8) uint64_t s_tables_bar;
 __device__ __forceinline__ void tables_wait() {
-#if defined(RS_TABLES_GLOBAL)
+#if !defined(RS_TABLES_SMEM)
   return;
 #endif
   const uint32_t bar_addr = (uint32_t)__cvta_generic_to_shared(&s_tables_bar);
@@ -204,7 +206,7 @@ __device__ __forceinline__ uint32_t cluster_rank() {
 // wait on its barrier before exiting (peers write into its shared memory).
 __device__ __forceinline__ void tables_begin(const DevTables& D, int grp_log2) {
   const uint32_t bar_addr = (uint32_t)__cvta_generic_to_shared(&s_tables_bar);
-#if defined(RS_TABLES_GLOBAL)
+#if !defined(RS_TABLES_SMEM)
   if (threadIdx.x == 0) s_grp_log2 = grp_log2;
   __syncthreads();
   return;
@@ -386,15 +388,43 @@ __global__ void __launch_bounds__(BLOCK) k_init(const __grid_constant__ Soa S, c
 // dependent chain; the SMs' issue slots are idle), fewer envs per warp also
 // means fewer divergent paths per warp, and the idle lanes join their env.
 
+// Completion signal of a step launch in mapped host memory
+// (rs_set_done_flag): a host thread waiting for the step's results polls
+// one word instead of sleeping in a stream synchronize.  Every working
+// warp publishes its stores system-wide and counts itself in; the last one
+// bumps the sequence number the host watches and re-arms the counter for
+// the next launch (launches on one stream are ordered).
+struct Done {
+  uint32_t* ctr;                 // device: [0] warps done this launch, [1] sequence
+  volatile uint32_t* host_flag;  // mapped pinned host word: the last sequence completed
+  uint32_t warps;                // working warps of the launch
+};
+__device__ __noinline__ void signal_done(const Done& d, uint32_t working, int lane) {
+  __threadfence_system();  // this lane's record / observation stores, before the count
+  __syncwarp(working);
+  if (lane == (int)(__ffs(working) - 1)) {
+    if (atomicAdd(d.ctr, 1u) == d.warps - 1) {
+      __threadfence();  // every other warp's count (and so its fenced stores) happened before
+      const uint32_t seq = d.ctr[1] + 1u;
+      d.ctr[1] = seq;
+      d.ctr[0] = 0u;
+      __threadfence_system();
+      *d.host_flag = seq;
+    }
+  }
+}
+
 __global__ void __launch_bounds__(ROLL_BLOCK, ROLL_MINB) k_step(const __grid_constant__ Soa S, const __grid_constant__ DevTables D,
     const __grid_constant__ Cfg C, const int32_t* actions, int flags, rs_obs_out obs, int32_t* next_actions,
     StepOut out, int epw, int staged, int glog2, int check, rs_step_rec* recs, const int32_t* order,
-    uint8_t* kind_out, int prefetch) {
+    uint8_t* kind_out, int prefetch, Done done) {
   tables_begin(D, glog2);  // the action and header loads overlap the table copy
   const Tabs T{};
   const int lane = threadIdx.x & 31;
   const int q = ((blockIdx.x * blockDim.x + threadIdx.x) >> 5) * epw + (lane >> glog2);
-  if ((lane >> glog2) >= epw || q >= S.n) {
+  const bool idle = (lane >> glog2) >= epw || q >= S.n;
+  const uint32_t working = done.host_flag ? __ballot_sync(0xFFFFFFFFu, !idle) : 0u;
+  if (idle) {
     tables_wait();  // (cluster launches: peers may still be writing this CTA's tables)
     return;
   }
@@ -478,6 +508,7 @@ __global__ void __launch_bounds__(ROLL_BLOCK, ROLL_MINB) k_step(const __grid_con
     for (int i = lane & ((1 << glog2) - 1); i < 10; i += 1 << glog2) dst[i] = word(i);
   }
   if (staged && dirty && sub == 0) stage_wait_all();
+  if (done.host_flag) signal_done(done, working, lane);
 }
 
 __global__ void __launch_bounds__(BLOCK) k_policy(const __grid_constant__ Soa S, const __grid_constant__ DevTables D,
@@ -797,6 +828,10 @@ struct rs_handle {
   int cluster;
   int occ_cl_key[8], occ_cl_val[8];  // co-resident clusters per (block, smem)
   int prefetch;  // RINSHAN_PREFETCH: L1 prefetch of an env's lines before its step (prefetch_env)
+  // rs_set_done_flag: the step launches' completion word in mapped host
+  // memory and its device-side counter / sequence
+  uint32_t* done_flag = nullptr;
+  uint32_t* done_ctr = nullptr;
   // per-env observation scratch of the wide trajectory digest (digest_obs),
   // allocated by the first rollout that asks for digests
   void* dig_obs_mem = nullptr;
@@ -969,6 +1004,11 @@ struct DeviceScope {
     if (prev >= 0) cudaSetDevice(prev);
   }
 };
+
+Done done_of(const rs_handle* h, const Launch& L) {
+  if (!h->done_flag) return Done{nullptr, nullptr, 0u};
+  return Done{h->done_ctr, h->done_flag, (uint32_t)((h->n + L.epw - 1) / L.epw)};
+}
 
 StepOut step_out(rs_handle* h, const rs_step_out* o) {
   StepOut s{};
@@ -1201,6 +1241,7 @@ int rs_destroy(rs_handle* h) {
   cudaFree(h->sort_tmp);
   cudaFree(h->export_buf);
   cudaFree(h->dig_obs_mem);
+  cudaFree(h->done_ctr);
   delete h;
   return 0;
 }
@@ -1242,7 +1283,7 @@ int rs_step_ex(rs_handle* h, const int32_t* actions_dev, int32_t flags, const rs
   CUDA_TRY(launch_tables(h, k_step, L.grid, L.block, L.smem, st, h->S, h->D, h->cfg, actions_dev, flags, o,
                          next_actions_dev, step_out(h, out), L.epw, L.staged, L.glog2, h->check_steps,
                          (rs_step_rec*)nullptr, L.ordered ? (const int32_t*)h->order : nullptr,
-                         L.ordered ? h->kind : nullptr, h->prefetch));
+                         L.ordered ? h->kind : nullptr, h->prefetch, done_of(h, L)));
   return finish_step_out(h, out, st);
 }
 
@@ -1262,7 +1303,24 @@ int rs_step_rec_out(rs_handle* h, const int32_t* actions, int32_t flags, rs_step
   CUDA_TRY(launch_tables(h, k_step, L.grid, L.block, L.smem, st, h->S, h->D, h->cfg, actions, flags, o,
                          (int32_t*)nullptr, StepOut{}, L.epw, L.staged, L.glog2, h->check_steps, recs,
                          L.ordered ? (const int32_t*)h->order : nullptr, L.ordered ? h->kind : nullptr,
-                         h->prefetch));
+                         h->prefetch, done_of(h, L)));
+  return 0;
+}
+
+int rs_set_done_flag(rs_handle* h, uint32_t* host_flag) {
+  if (!h) return set_err(RS_E_ARG, "rs_set_done_flag: null handle");
+  const DeviceScope device_scope(h->device);
+  if (host_flag && !h->done_ctr) {
+    CUDA_TRY(cudaMalloc(&h->done_ctr, 2 * sizeof(uint32_t)));
+    CUDA_TRY(cudaMemset(h->done_ctr, 0, 2 * sizeof(uint32_t)));
+  }
+  if (host_flag) {
+    // the sequence starts again from the host word's current value
+    CUDA_TRY(cudaDeviceSynchronize());
+    const uint32_t init[2] = {0u, *host_flag};
+    CUDA_TRY(cudaMemcpy(h->done_ctr, init, sizeof(init), cudaMemcpyHostToDevice));
+  }
+  h->done_flag = host_flag;
   return 0;
 }
 

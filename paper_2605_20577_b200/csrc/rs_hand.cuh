@@ -169,9 +169,9 @@ __constant__ const uint8_t* c_suit_cls;
 __constant__ const uint8_t* c_honor_cls;
 __constant__ const uint8_t* c_tblock;  // the t3 | t1 | t2 | pow block in global memory
 #endif
-// -DRS_TABLES_GLOBAL (experiment): read the factored tables through the
-// read-only cache instead of staging them into shared memory
-#if defined(RS_TABLES_GLOBAL) && defined(__CUDA_ARCH__)
+// the factored tables through the read-only cache (default) or from the
+// shared-memory stage (-DRS_TABLES_SMEM, rs_tables.h)
+#if !defined(RS_TABLES_SMEM) && defined(__CUDA_ARCH__)
 #define RS_TBL(off) (c_tblock + (off))
 #elif defined(__CUDA_ARCH__)
 #define RS_TBL(off) (g_smem + (off))

@@ -36,8 +36,17 @@ constexpr int T1_OFF = T3_BYTES;
 constexpr int T2_OFF = T1_OFF + NS * NS;
 constexpr int POW_OFF = (T2_OFF + NS * NH + 3) & ~3;  // u32[34]: code delta per kind
 constexpr int SMEM_TABLE_BYTES = POW_OFF + 4 * 34;
-// per-thread 144-byte wall slots for the deal follow the tables
+// The stepping kernels read the factored tables through L1 from global
+// memory (the default; every CTA used to wait ~3 us for its 38.7 KB copy at
+// the start of a K=1 launch) or, built with -DRS_TABLES_SMEM, from a copy
+// staged into shared memory by one TMA bulk copy per CTA (optionally
+// multicast over a thread-block cluster).  The deal's shuffle scratch
+// starts the dynamic shared memory, after the staged tables if any.
+#if defined(RS_TABLES_SMEM)
 constexpr int WALL_SLOT_OFF = (SMEM_TABLE_BYTES + 15) & ~15;
+#else
+constexpr int WALL_SLOT_OFF = 0;
+#endif
 
 struct HostTables {
   bool ready = false;

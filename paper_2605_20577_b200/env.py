@@ -14,6 +14,7 @@ from __future__ import annotations
 import ctypes as C
 from dataclasses import dataclass
 
+import numpy as np
 import torch
 
 from . import abi
@@ -413,6 +414,16 @@ class HostStepper:
             truncated=d["truncated"].data_ptr(), status=d["status"].data_ptr())
         self.bytes_h2d = 4 * n
         self.bytes_d2h = self.BYTES_PER_ENV * n + (OBS_BYTES * n if obs_to_host else 0)
+        # completion word (rs_set_done_flag): when the kernel itself writes
+        # every result into pinned memory, the host polls one word the
+        # kernel bumps after its last store instead of sleeping in a stream
+        # synchronize (~15 us less per step)
+        self._flag = None
+        if self._packed:
+            self._flag = torch.zeros(1, dtype=torch.int32, pin_memory=True)
+            self._flag_np = self._flag.numpy().view(np.uint32)
+            check(env._L.rs_set_done_flag(env._h, self._flag.data_ptr()), "rs_set_done_flag")
+            self._seq = 0
         self._graph = None
         if graph:
             # no eager warm-up: a step mutates the envs, and nothing in the
@@ -499,9 +510,31 @@ class HostStepper:
         """one step; returns when the host result views are valid (graph
         replays run on the current stream)"""
         self.launch()
-        torch.cuda.current_stream(self.env.device).synchronize()
+        self.wait()
         return self
 
+    def wait(self):
+        """until the launched step's results are in the host views"""
+        stream = torch.cuda.current_stream(self.env.device)
+        if self._flag is None:
+            stream.synchronize()
+            return
+        target = (self._seq + 1) & 0xFFFFFFFF
+        f = self._flag_np
+        spins = 0
+        while f[0] != target:
+            spins += 1
+            if spins & 0xFFFFF == 0 and stream.query():  # the stream is idle: surface any fault
+                stream.synchronize()
+                if f[0] != target:
+                    raise RuntimeError("HostStepper: the step finished without signalling completion")
+        self._seq = target
+
     def close(self):
-        """drop the captured graph (the pinned buffers go with the object)"""
+        """drop the captured graph and the completion word (the pinned
+        buffers go with the object)"""
         self._graph = None
+        if self._flag is not None and getattr(self.env, "_h", None):
+            torch.cuda.current_stream(self.env.device).synchronize()
+            self.env._L.rs_set_done_flag(self.env._h, None)
+            self._flag = None
