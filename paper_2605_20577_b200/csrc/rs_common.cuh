@@ -48,6 +48,29 @@ inline uint4 make_uint4(uint32_t x, uint32_t y, uint32_t z, uint32_t w) { return
 #define RS_CHECK(c) ((void)0)
 #endif
 
+// Measured alternatives kept buildable (tools/build_variant.sh -D...):
+//   -DRS_AB_OFF_WIN16   observation window over 4 lanes instead of 8 / 16
+//   -DRS_CLAIM_LANES    opponents' claim checks on three lanes of the env's
+//                       group, combined by one warp reduction (2 % slower at
+//                       4,096 envs: the checks diverge per lane anyway)
+//   -DRS_SWAP5          the deal's swap chain five swaps per load round
+//                       (neutral to -0.7 %: resets are not the launch tail)
+#if defined(RS_AB_OFF_WIN16)
+#define RS_WIN16 0
+#else
+#define RS_WIN16 1
+#endif
+#if defined(RS_CLAIM_LANES)
+#define RS_CLAIM_LANES_ON 1
+#else
+#define RS_CLAIM_LANES_ON 0
+#endif
+#if defined(RS_SWAP5)
+#define RS_SWAP5_ON 1
+#else
+#define RS_SWAP5_ON 0
+#endif
+
 namespace rs {
 
 #if defined(__CUDACC__)
@@ -115,6 +138,14 @@ RS_HD uint32_t grp_mask() {
   return G == 32 ? 0xFFFFFFFFu : (((1u << G) - 1u) << ((threadIdx.x & 31) & ~(uint32_t)(G - 1)));
 #else
   return 1u;
+#endif
+}
+RS_HD uint32_t grp_or32(uint32_t x) {
+#if defined(__CUDA_ARCH__)
+  if (grp_size() == 1) return x;
+  return __reduce_or_sync(grp_mask(), x);
+#else
+  return x;
 #endif
 }
 RS_HD uint64_t grp_or64(uint64_t x) {

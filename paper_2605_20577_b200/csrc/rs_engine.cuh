@@ -118,6 +118,47 @@ RS_COLD void emit_event(uint16_t* ring, uint32_t* ob, uint32_t p, int rule, int 
 #define RS_OL_STANDS_Q RS_HD
 #endif
 
+// Five consecutive Fisher-Yates swaps (rng.py:59-65) i, i-1, .., i-4 with
+// targets j[0..4] on a byte array: the ten positions are loaded at once,
+// the swaps are resolved in registers (a later swap reads what an earlier
+// one of the batch wrote: a target j[v] can equal a later position i-u or a
+// later target), and the ten stores issue in swap order, so the chain costs
+// one load round trip per five swaps instead of one per swap.
+RS_HD void swap5(uint8_t* w, int i, const int* j) {
+  if (!RS_SWAP5_ON) {  // the plain chain (default; -DRS_SWAP5: batched)
+    for (int u = 0; u < 5; u++) {
+      const uint8_t t = w[i - u];
+      w[i - u] = w[j[u]];
+      w[j[u]] = t;
+    }
+    return;
+  }
+  int x[5], y[5];
+#pragma unroll
+  for (int u = 0; u < 5; u++) {
+    x[u] = w[i - u];
+    y[u] = w[j[u]];
+  }
+  int av[5], bv[5];
+#pragma unroll
+  for (int u = 0; u < 5; u++) {
+    int ca = x[u], cb = y[u];
+#pragma unroll
+    for (int v = 0; v < u; v++) {
+      if (j[v] == i - u) ca = bv[v];
+      if (j[v] == j[u]) cb = bv[v];
+    }
+    if (j[u] == i - u) cb = ca;
+    av[u] = cb;
+    bv[u] = ca;
+  }
+#pragma unroll
+  for (int u = 0; u < 5; u++) {
+    w[i - u] = (uint8_t)av[u];
+    w[j[u]] = (uint8_t)bv[u];
+  }
+}
+
 struct Engine {
   const Soa& S;
   const Tabs& T;
@@ -208,12 +249,7 @@ struct Engine {
           int j[5];
 #pragma unroll
           for (int u = 0; u < 5; u++) j[u] = J[i - u];
-#pragma unroll
-          for (int u = 0; u < 5; u++) {
-            const uint8_t t = w[i - u];
-            w[i - u] = w[j[u]];
-            w[j[u]] = t;
-          }
+          swap5(w, i, j);
         }
       }
       __syncwarp(gm);
@@ -235,12 +271,7 @@ struct Engine {
         for (int u = 0; u < 5; u++)
           j[u] = (int)randbelow_from(stream_value(g.rng_key, c + 1 + u), (uint32_t)(i - u + 1));
         c += 5;
-#pragma unroll
-        for (int u = 0; u < 5; u++) {
-          const uint8_t t = w[i - u];
-          w[i - u] = w[j[u]];
-          w[j[u]] = t;
-        }
+        swap5(w, i, j);
       }
 #if defined(__CUDA_ARCH__)
       for (int k = 0; k < WALL_STRIDE / 16; k++)  // (scratch: 4-byte aligned)
@@ -738,19 +769,34 @@ struct Engine {
       q |= ((uint32_t)s | ((uint32_t)stage << 2)) << (3 + 4 * n);
       n++;
     };
-    for (int off = 1; off <= 3; off++) {
+    // claims of the three opponents: bit 3 (off - 1) ron, + 1 pon / kan,
+    // + 2 chi (the left seat only)
+    const bool open_ok = !chankan && g.live() >= 1;
+    auto claims_of = [&](int off) -> uint32_t {
       const int s = (discarder + off) & 3;
-      if (can_ron(s, tile, chankan)) push(s, ST_RON);
-    }
-    if (!chankan && g.live() >= 1) {
-      for (int off = 1; off <= 3; off++) {
-        const int s = (discarder + off) & 3;
-        if (hi::riichi(info(s))) continue;
-        if (count_of(s, kind) >= 2) push(s, ST_PONKAN);
+      uint32_t b = can_ron(s, tile, chankan) ? 1u : 0u;
+      if (open_ok && !hi::riichi(info(s))) {
+        if (count_of(s, kind) >= 2) b |= 2u;
+        if (off == 1 && kind < 27 && can_chi(s, kind)) b |= 4u;
       }
-      const int s = (discarder + 1) & 3;
-      if (kind < 27 && !hi::riichi(info(s)) && can_chi(s, kind)) push(s, ST_CHI);
+      return b << (3 * (off - 1));
+    };
+    uint32_t claims = 0;
+    if (RS_CLAIM_LANES_ON && grp_size() >= 4) {
+      // lane group: lanes 1-3 of the env's group check one opponent each
+      // and the group combines the claim bits with one warp reduction
+      const int sub = grp_sub();
+      claims = grp_or32(sub >= 1 && sub <= 3 ? claims_of(sub) : 0u);
+    } else {
+      claims = claims_of(1) | claims_of(2) | claims_of(3);
     }
+    // queue order (engine.py:498-531): rons from the discarder's right,
+    // then pon / kan in seat order, then chi
+    for (int off = 1; off <= 3; off++)
+      if ((claims >> (3 * (off - 1))) & 1u) push((discarder + off) & 3, ST_RON);
+    for (int off = 1; off <= 3; off++)
+      if ((claims >> (3 * (off - 1) + 1)) & 1u) push((discarder + off) & 3, ST_PONKAN);
+    if (claims & 4u) push((discarder + 1) & 3, ST_CHI);
     if (!n) return false;
     g.phase = PH_CALL;
     g.call_tile = tile;

