@@ -29,8 +29,9 @@
  *                                              launch + one copy; service/sessions.py
  *                                              state reads, batched sessions)
  *   rs_import_env     tests/engine_helpers.py:58-105 craft() (crafted states)
- *   rs_set_done_flag  (no counterpart: the reference steps in-process) completion
- *                                              word of host-driven steps (HostStepper)
+ *   rs_set_done_flag, rs_signal_done (no counterpart: the reference steps
+ *                                              in-process) completion word of host-driven
+ *                                              steps (HostStepper)
  *   rs_debug_score    scoring/score.py:45-82   score_win(ctx, kazoe, double_yakuman)
  *                                              over WinContext (scoring/context.py:19-57),
  *                                              the device scorer alone (parity harness)
@@ -311,20 +312,29 @@ int rs_step(rs_handle* h, const int32_t* actions_dev, const rs_step_out* out, vo
 #define RS_STEP_OBSERVE 2
 /* next_actions_dev from heuristic_policy instead of random_policy */
 #define RS_STEP_HEURISTIC 4
+/* bump the completion word (rs_set_done_flag) once every output of the
+ * step is visible to the host */
+#define RS_STEP_SIGNAL 8
 int rs_step_ex(rs_handle* h, const int32_t* actions_dev, int32_t flags, const rs_step_out* out,
                const rs_obs_out* obs, int32_t* next_actions_dev, void* stream);
 /* rs_step_ex with the per-env outputs and the next action (random, or
  * heuristic with RS_STEP_HEURISTIC) written as one rs_step_rec per env into
- * recs[n] (device or mapped pinned host memory) */
+ * recs[n] (device or mapped pinned host memory); next_actions (may be
+ * NULL): the next actions also as one contiguous int32[n] (what a host
+ * loop feeding them back reads: 4 bytes per env instead of a strided
+ * gather over the records) */
 int rs_step_rec_out(rs_handle* h, const int32_t* actions, int32_t flags, rs_step_rec* recs,
-                    const rs_obs_out* obs, void* stream);
-/* Completion word for host-driven stepping: after every rs_step_ex /
- * rs_step_rec_out launch, once all of its per-env outputs are visible to
- * the host, the kernel writes an incremented sequence number into
- * *host_flag (mapped pinned host memory), so a host thread can poll one
- * word instead of sleeping in a stream synchronize.  The sequence
- * continues from the word's value at this call; NULL turns it off. */
+                    const rs_obs_out* obs, int32_t* next_actions, void* stream);
+/* Completion word for host-driven stepping: after an rs_step_ex /
+ * rs_step_rec_out launch with RS_STEP_SIGNAL, once all of its per-env
+ * outputs are visible to the host, the kernel writes an incremented
+ * sequence number into *host_flag (mapped pinned host memory), so a host
+ * thread can poll one word instead of sleeping in a stream synchronize;
+ * rs_signal_done bumps it after whatever precedes it on `stream` (a copy of
+ * device outputs to the host).  The sequence continues from the word's
+ * value at this call; NULL turns it off. */
 int rs_set_done_flag(rs_handle* h, uint32_t* host_flag);
+int rs_signal_done(rs_handle* h, void* stream);
 /* seats_dev: device int8[n] or NULL for each env's current player */
 int rs_observe(rs_handle* h, const int8_t* seats_dev, const rs_obs_out* obs, void* stream);
 /* random policy over each env's legal list using its policy stream */

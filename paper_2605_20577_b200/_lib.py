@@ -28,7 +28,7 @@ SYMBOLS = (
     "rs_num_envs", "rs_state_bytes", "rs_init", "rs_init_indexed", "rs_step", "rs_step_ex", "rs_step_rec_out",
     "rs_observe",
     "rs_policy_random", "rs_policy_heuristic", "rs_rollout", "rs_rollout_policy", "rs_autoreset", "rs_check_invariants", "rs_export_env", "rs_export_envs", "rs_import_env", "rs_record_sizes", "rs_debug_rollout_cycles",
-    "rs_debug_score", "rs_set_done_flag",
+    "rs_debug_score", "rs_set_done_flag", "rs_signal_done",
 )
 
 _lib = None
@@ -84,7 +84,7 @@ def lib():
         L.rs_init_indexed.argtypes = [vp, u64, i64, vp, vp]
         L.rs_step.argtypes = [vp, vp, vp, vp]
         L.rs_step_ex.argtypes = [vp, vp, i32, vp, vp, vp, vp]
-        L.rs_step_rec_out.argtypes = [vp, vp, i32, vp, vp, vp]
+        L.rs_step_rec_out.argtypes = [vp, vp, i32, vp, vp, vp, vp]
         L.rs_observe.argtypes = [vp, vp, vp, vp]
         L.rs_policy_random.argtypes = [vp, vp, vp]
         L.rs_rollout.argtypes = [vp, i32, vp, i32, vp, vp, vp, vp, vp]
@@ -99,6 +99,7 @@ def lib():
         L.rs_debug_rollout_cycles.argtypes = [vp, i32, vp, vp, vp]
         if hasattr(L, "rs_set_done_flag"):
             L.rs_set_done_flag.argtypes = [vp, vp]
+            L.rs_signal_done.argtypes = [vp, vp]
         if hasattr(L, "rs_debug_score"):  # (A/B builds of older sources lack it)
             L.rs_debug_score.argtypes = [vp, i64, vp, vp, i32]
         if L.rs_abi_version() != 1:

@@ -31,6 +31,11 @@ RIVER_RIICHI = 2
 RIVER_CALLED = 4
 STATUS_INVARIANT = 4
 ACTION_SKIP = -(1 << 31)  # RS_ACTION_SKIP: the env is not stepped
+# rs_step_ex / rs_step_rec_out flags
+STEP_AUTORESET = 1
+STEP_OBSERVE = 2
+STEP_HEURISTIC = 4
+STEP_SIGNAL = 8
 # rs_check_invariants bits (include/rinshan.h RS_INV_*)
 INV_SCORE_SUM = 1
 INV_TILES = 2

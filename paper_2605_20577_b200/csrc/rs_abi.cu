@@ -414,6 +414,10 @@ __device__ __noinline__ void signal_done(const Done& d, uint32_t working, int la
   }
 }
 
+// rs_signal_done: the completion word after the work queued before it on
+// the stream (e.g. a copy of the observations to the host)
+__global__ void k_signal(Done done) { signal_done(done, 0xFFFFFFFFu, (int)(threadIdx.x & 31)); }
+
 __global__ void __launch_bounds__(ROLL_BLOCK, ROLL_MINB) k_step(const __grid_constant__ Soa S, const __grid_constant__ DevTables D,
     const __grid_constant__ Cfg C, const int32_t* actions, int flags, rs_obs_out obs, int32_t* next_actions,
     StepOut out, int epw, int staged, int glog2, int check, rs_step_rec* recs, const int32_t* order,
@@ -1005,8 +1009,8 @@ struct DeviceScope {
   }
 };
 
-Done done_of(const rs_handle* h, const Launch& L) {
-  if (!h->done_flag) return Done{nullptr, nullptr, 0u};
+Done done_of(const rs_handle* h, const Launch& L, int flags) {
+  if (!h->done_flag || !(flags & RS_STEP_SIGNAL)) return Done{nullptr, nullptr, 0u};
   return Done{h->done_ctr, h->done_flag, (uint32_t)((h->n + L.epw - 1) / L.epw)};
 }
 
@@ -1283,12 +1287,12 @@ int rs_step_ex(rs_handle* h, const int32_t* actions_dev, int32_t flags, const rs
   CUDA_TRY(launch_tables(h, k_step, L.grid, L.block, L.smem, st, h->S, h->D, h->cfg, actions_dev, flags, o,
                          next_actions_dev, step_out(h, out), L.epw, L.staged, L.glog2, h->check_steps,
                          (rs_step_rec*)nullptr, L.ordered ? (const int32_t*)h->order : nullptr,
-                         L.ordered ? h->kind : nullptr, h->prefetch, done_of(h, L)));
+                         L.ordered ? h->kind : nullptr, h->prefetch, done_of(h, L, flags)));
   return finish_step_out(h, out, st);
 }
 
 int rs_step_rec_out(rs_handle* h, const int32_t* actions, int32_t flags, rs_step_rec* recs,
-                    const rs_obs_out* obs, void* stream) {
+                    const rs_obs_out* obs, int32_t* next_actions, void* stream) {
   if (!h || !actions || !recs) return set_err(RS_E_ARG, "rs_step_rec_out: null argument");
   if ((flags & RS_STEP_OBSERVE) && !obs) return set_err(RS_E_ARG, "RS_STEP_OBSERVE needs obs buffers");
   const DeviceScope device_scope(h->device);
@@ -1301,9 +1305,17 @@ int rs_step_rec_out(rs_handle* h, const int32_t* actions, int32_t flags, rs_step
     if (rc) return rc;
   }
   CUDA_TRY(launch_tables(h, k_step, L.grid, L.block, L.smem, st, h->S, h->D, h->cfg, actions, flags, o,
-                         (int32_t*)nullptr, StepOut{}, L.epw, L.staged, L.glog2, h->check_steps, recs,
+                         next_actions, StepOut{}, L.epw, L.staged, L.glog2, h->check_steps, recs,
                          L.ordered ? (const int32_t*)h->order : nullptr, L.ordered ? h->kind : nullptr,
-                         h->prefetch, done_of(h, L)));
+                         h->prefetch, done_of(h, L, flags)));
+  return 0;
+}
+
+int rs_signal_done(rs_handle* h, void* stream) {
+  if (!h || !h->done_flag) return set_err(RS_E_ARG, "rs_signal_done: no completion word (rs_set_done_flag)");
+  const DeviceScope device_scope(h->device);
+  k_signal<<<1, 32, 0, (cudaStream_t)stream>>>(Done{h->done_ctr, h->done_flag, 1u});
+  CUDA_TRY(cudaGetLastError());
   return 0;
 }
 

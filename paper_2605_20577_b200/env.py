@@ -366,11 +366,13 @@ class HostStepper:
     graph.  Either way a step costs one graph launch.
 
     Host result views (valid after `step()` returns): rewards f32[n,4],
-    legal_bits i32[n,4], next_actions i32[n], current_player i8[n],
+    legal_bits i32[n,4], next_actions i32[n] (contiguous), current_player i8[n],
     terminated / truncated / status u8[n]; with `obs_to_host` (and
     `observe`) also `observations`, the current player's observation of
-    every env (observe.py:81-124) in pinned host memory, written by the
-    same kernel over the host link.
+    every env (observe.py:81-124) in pinned host memory: the kernel writes
+    it to a device block and one copy moves the block (232 bytes per env)
+    to the host inside the same graph (the kernel writing it over the host
+    link directly was ~2x slower: small scattered stores).
     """
 
     BYTES_PER_ENV = 40
@@ -384,6 +386,7 @@ class HostStepper:
             if not observe:
                 raise ValueError("obs_to_host needs observe=True")
             self._obs_host, self.observations = alloc_observations_block(n, pinned=True)
+            self._obs_dev_buf, self._obs_dev = alloc_observations_block(n, pinned=False, device=dev)
         self.env = env
         self.n = n
         self.autoreset, self.observe, self.policy = autoreset, observe, policy
@@ -405,6 +408,11 @@ class HostStepper:
         views = self._rec_views if self._packed else self._views
         d, h = views(self._res_dev), views(self._res_host)
         self.rewards, self.legal_bits, self.next_actions = h["rewards"], h["legal_bits"], h["next_actions"]
+        if self._packed:
+            # the next actions also as one contiguous pinned int32[n] (what a
+            # host loop feeding them back reads; the records hold them too)
+            self._next_host = torch.zeros(n, dtype=torch.int32, pin_memory=True)
+            self.next_actions = self._next_host
         self.current_player, self.terminated = h["current_player"], h["terminated"]
         self.truncated, self.status = h["truncated"], h["status"]
         self._dev_views = d
@@ -413,7 +421,7 @@ class HostStepper:
             rewards=d["rewards"].data_ptr(), terminated=d["terminated"].data_ptr(),
             truncated=d["truncated"].data_ptr(), status=d["status"].data_ptr())
         self.bytes_h2d = 4 * n
-        self.bytes_d2h = self.BYTES_PER_ENV * n + (OBS_BYTES * n if obs_to_host else 0)
+        self.bytes_d2h = self.BYTES_PER_ENV * n + (OBS_BYTES * n if obs_to_host else 0) + (4 * n if self._packed else 0)
         # completion word (rs_set_done_flag): when the kernel itself writes
         # every result into pinned memory, the host polls one word the
         # kernel bumps after its last store instead of sleeping in a stream
@@ -466,7 +474,7 @@ class HostStepper:
 
     def _obs_target(self) -> Observations:
         if self.observations is not None:
-            return self.observations
+            return self._obs_dev
         env = self.env
         if env._obs is None:
             env._obs = alloc_observations(env.n, env.device)
@@ -477,9 +485,15 @@ class HostStepper:
             env = self.env
             ost = obs_struct(self._obs_target()) if self.observe else None
             flags = (1 if self.autoreset else 0) | (2 if self.observe else 0)
+            if self.observations is None:
+                flags |= abi.STEP_SIGNAL  # the kernel's own stores complete the step
             check(env._L.rs_step_rec_out(env._h, self.actions.data_ptr(), flags, self._res_host.data_ptr(),
-                                         C.byref(ost) if ost is not None else None, env._stream()),
+                                         C.byref(ost) if ost is not None else None, self._next_host.data_ptr(),
+                                         env._stream()),
                   "rs_step_rec_out")
+            if self.observations is not None:
+                self._obs_host.copy_(self._obs_dev_buf, non_blocking=True)
+                check(env._L.rs_signal_done(env._h, env._stream()), "rs_signal_done")
             return
         if self.zero_copy != "none":
             env = self.env
@@ -491,13 +505,17 @@ class HostStepper:
                                     env._stream()), "rs_step_ex")
             if self.zero_copy == "actions":
                 self._res_host.copy_(self._res_dev, non_blocking=True)
+            if self.observations is not None:
+                self._obs_host.copy_(self._obs_dev_buf, non_blocking=True)
             return
         self._act_dev.copy_(self.actions, non_blocking=True)
         if self.observations is not None:
-            self.env._obs = self.observations  # written over the host link
+            self.env._obs = self._obs_dev
         self.env.step(self._act_dev, autoreset=self.autoreset, observe=self.observe,
                       next_actions=self._dev_views["next_actions"] if self.policy else None, out=self._out)
         self._res_host.copy_(self._res_dev, non_blocking=True)
+        if self.observations is not None:
+            self._obs_host.copy_(self._obs_dev_buf, non_blocking=True)
 
     def launch(self):
         """enqueue one step (graph replay) without waiting"""

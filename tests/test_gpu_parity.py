@@ -356,3 +356,33 @@ def test_fused_trajectory_equals_single_steps(rule):
         assert torch.equal(traj["status"][t], b.status), t
         for key in ("hand_tokens", "event_tokens", "scores", "dora_indicator_tokens"):
             assert torch.equal(obs_a[key][t], obs_b[key]), (t, key)
+
+
+@pytest.mark.parametrize("zero_copy", (True, False))
+def test_host_stepper_observations_to_host(zero_copy):
+    """HostStepper(obs_to_host=True): after every step the host-side
+    observations equal a device observe() of each env's current player, and
+    the completion word (RS_STEP_SIGNAL / rs_signal_done) never lets the
+    host read a step early (the result block and next actions agree with
+    the env's own state)"""
+    from paper_2605_20577_b200.env import HostStepper
+
+    n = 257
+    env = BatchEnv(n, EnvConfig(rule="red")).init(seed=21)
+    hs = HostStepper(env, autoreset=True, observe=True, policy=True, zero_copy=zero_copy, obs_to_host=True)
+    first = torch.empty(n, dtype=torch.int32, device="cuda")
+    env.random_actions(out=first)
+    hs.actions.copy_(first.cpu())
+    acts, nxt = hs.actions.numpy(), hs.next_actions.numpy()
+    for t in range(40):
+        hs.step()
+        host_obs = {k: v.clone() for k, v in hs.observations.items()}
+        cp = hs.current_player.clone()
+        acts[:] = nxt
+        from paper_2605_20577_b200.env import alloc_observations
+
+        dev_obs = env.observe(cp.to(torch.int8).cuda(), out=alloc_observations(n, "cuda"))
+        torch.cuda.synchronize()
+        for k, v in dev_obs.items():
+            assert torch.equal(host_obs[k], v.cpu()), (t, k)
+    hs.close()

@@ -56,7 +56,7 @@ recs = torch.empty(n * 40, dtype=torch.uint8, device=dev)
 
 
 def step_dev():
-    env._L.rs_step_rec_out(env._h, acts.data_ptr(), 3, recs.data_ptr(), C.byref(ost), s.cuda_stream)
+    env._L.rs_step_rec_out(env._h, acts.data_ptr(), 3, recs.data_ptr(), C.byref(ost), None, s.cuda_stream)
     acts.copy_(recs.view(torch.int32).view(n, 10)[:, 8])
 
 
