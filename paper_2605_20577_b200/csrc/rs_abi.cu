@@ -339,12 +339,28 @@ __device__ __forceinline__ void write_step_out(const StepOut& o, int64_t e, cons
 }
 
 // the kind of an env's next step, for grouping envs with the same branch
-// structure into the same warps (large batches): 0 auto-reset, 1 call
-// phase, 2 turn with a drawn tile, 3 other turn (after a call)
+// structure into the same warps (large batches).  RS_KIND_BITS 2: 0
+// auto-reset, 1 call phase, 2 turn with a drawn tile, 3 other turn (after
+// a call).  RS_KIND_BITS 3 also splits the call phase by the head of the
+// queue (ron: a win evaluation) and the drawn turns by the actor's hand --
+// in riichi (tsumogiri or a kan only), tenpai or complete and closed (the
+// riichi discard filter, the tsumo check), open, other.
+#ifndef RS_KIND_BITS
+#define RS_KIND_BITS 2
+#endif
 __device__ __forceinline__ uint8_t next_kind(const Engine& E) {
   if (E.g.env_terminated || E.g.env_truncated) return 0;
+#if RS_KIND_BITS == 2
   if (E.g.phase == PH_CALL) return 1;
   return E.g.drawn >= 0 ? 2 : 3;
+#else
+  if (E.g.phase == PH_CALL) return E.g.qstage(0) == ST_RON ? 1 : 2;
+  if (E.g.drawn < 0) return 7;
+  const uint32_t inf = E.info(E.g.actor);
+  if (hi::riichi(inf)) return 3;
+  if (hi::nmelds(inf)) return 6;
+  return hi::shanten(inf) <= 0 ? 4 : 5;
+#endif
 }
 
 __global__ void k_iota(int32_t* a, int n) {
@@ -445,7 +461,7 @@ __global__ void __launch_bounds__(ROLL_BLOCK, ROLL_MINB) k_step(const __grid_con
     __syncwarp(gm);  // the slot's barrier is initialised for the whole group
     stage_wait(sb, 0);
   }
-  if (prefetch && !staged) prefetch_env(S, e, sub, 1 << glog2, prefetch);
+  if ((prefetch & 3) && !staged) prefetch_env(S, e, sub, 1 << glog2, prefetch & 3);
   const int action = actions[e];  // may live in mapped host memory (HostStepper)
   Engine E(S, T, C, e, staged ? g_smem + sb : S.blk + (size_t)e * BLK_BYTES);
   E.load();
@@ -597,7 +613,7 @@ __global__ void __launch_bounds__(ROLL_BLOCK, ROLL_MINB) k_rollout(const __grid_
       stage_wait(sb, phase);
       phase ^= 1u;
     }
-    if (prefetch && !staged) prefetch_env(S, e, sub, 1 << glog2, prefetch);
+    if ((prefetch & 3) && !staged) prefetch_env(S, e, sub, 1 << glog2, prefetch & 3);
     Engine E(S, T, C, e, staged ? g_smem + sb : S.blk + (size_t)e * BLK_BYTES);
     E.load();
     uint64_t d = digests ? digests[e] : 0ull;
@@ -965,7 +981,7 @@ Launch step_launch(rs_handle* h, bool persistent) {
 int order_envs(rs_handle* h, cudaStream_t st) {
   size_t bytes = h->sort_tmp_bytes;
   CUDA_TRY(cub::DeviceRadixSort::SortPairs(h->sort_tmp, bytes, h->kind, h->kind_sorted, h->iota, h->order, h->n, 0,
-                                           2, st));
+                                           RS_KIND_BITS, st));
   return 0;
 }
 
@@ -1202,7 +1218,7 @@ int rs_create(rs_handle** out, int64_t n_envs, const rs_config* cfg, int32_t dev
   h->sort_tmp = nullptr;
   h->sort_tmp_bytes = 0;
   if ((err = cub::DeviceRadixSort::SortPairs(nullptr, h->sort_tmp_bytes, h->kind, h->kind_sorted, h->iota, h->order,
-                                             (int)n, 0, 2)))
+                                             (int)n, 0, RS_KIND_BITS)))
     return cleanup(err, "sort size query");
   if ((err = cudaMalloc(&h->sort_tmp, std::max<size_t>(h->sort_tmp_bytes, 16)))) return cleanup(err, "sort scratch");
   const void* kernels[] = {(const void*)k_init, (const void*)k_step, (const void*)k_policy,
@@ -1221,6 +1237,7 @@ int rs_create(rs_handle** out, int64_t n_envs, const rs_config* cfg, int32_t dev
   const char* prefetch_env_s = getenv("RINSHAN_PREFETCH");
   // measured on B200 (tools/prefetch_ab.sh): block lines +1-1.5 % at 4,096-16,384 envs, neutral at 1 M;
   // the observer streams too (2) cost HBM traffic at large batches (1 M envs -7 %)
+  // the next observer's stream alone (after the header load, k_rollout): neutral at 4,096 envs, -1 % at 1 M
   h->prefetch = prefetch_env_s ? std::max(0, std::min(2, atoi(prefetch_env_s))) : 1;
   const char* stage_env = getenv("RINSHAN_STAGE");
   h->stage_mode = stage_env ? std::max(0, std::min(2, atoi(stage_env))) : 0;
