@@ -355,7 +355,8 @@ struct Engine {
 
   // ------------------------------------------------------ win evaluation
   // engine.py:345-375 (_win_context)
-  RS_HD void win_input(int seat, const Hand& h, int win_tile, bool tsumo, bool chankan, WinIn& w) const {
+  // one out-of-line copy for its four callers (cold: win checks and settlements)
+  RS_COLD void win_input(int seat, const Hand& h, int win_tile, bool tsumo, bool chankan, WinIn& w) const {
     const uint32_t inf = h.info;
     w.conc.c[0] = nib_counts(h.w0);
     w.conc.c[1] = nib_counts(h.w1);
@@ -405,6 +406,7 @@ struct Engine {
     }
     // dora.py:9-26
     int dora = 0, ura = 0;
+#pragma unroll 1
     for (int i = 0; i < 5; i++)
       if (i < g.dora_count) {
         dora += all.get(dora_kind(wall(122 + 2 * i) >> 2));

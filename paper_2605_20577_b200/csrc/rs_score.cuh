@@ -432,6 +432,7 @@ RS_COLD bool score_win(const WinIn& w, Reading& best, bool first_only) {
 // yaku id (yakuman multiplicity for yakuman hands), the reading's totals and
 // the dora parts of the win context
 RS_HD void fill_win_rec(rs_win_rec& x, const Reading& rd, const WinIn& w) {
+#pragma unroll 1
   for (int id = 0; id < 40; id++) {
     int han = 0;
     if ((rd.mask >> id) & 1) {
