@@ -574,9 +574,10 @@ __device__ __noinline__ uint64_t digest_wide(uint64_t d, int a, const Engine& E,
 // the fused rollout: the packed header stays in registers for all K steps.
 // Persistent grid (at most the resident CTA count): each CTA stages the
 // tables once and walks env tiles grid-stride.
-// WIDE: the test / parity instantiation that folds the wide digest
-// (digest_wide) when `digests` is given; the production instantiation has
-// none of that code (-2.5 % launch time at 4,096 envs when it shared it)
+// WIDE: the test / debug instantiation -- the wide digest (digest_wide)
+// when `digests` is given, the invariant checker after every step with
+// RINSHAN_CHECK; the production instantiation has none of that code
+// (-2.5 % launch time at 4,096 envs when it shared the digest)
 template <bool WIDE>
 __global__ void __launch_bounds__(ROLL_BLOCK, ROLL_MINB) k_rollout(const __grid_constant__ Soa S, const __grid_constant__ DevTables D,
     const __grid_constant__ Cfg C, int steps, rs_obs_out obs,
@@ -639,7 +640,7 @@ __global__ void __launch_bounds__(ROLL_BLOCK, ROLL_MINB) k_rollout(const __grid_
       const int a = policy == RS_POLICY_HEURISTIC ? E.heuristic_action(E.load_legal()) : E.random_action(E.load_legal());
       const int actor = E.g.current_player;
       st = E.step(a, m, r);
-      if (check && check_invariants(E, true)) inv = true;  // debug: every step
+      if (WIDE && check && check_invariants(E, true)) inv = true;  // debug: every step
       if (actions_log) actions_log[(size_t)t * S.n + e] = (int16_t)a;
       if (actors_log) actors_log[(size_t)t * S.n + e] = (int8_t)(actor | (reset ? 4 : 0));
       // per-step outputs into [steps][n] trajectory buffers (rs_rollout_policy traj)
@@ -1416,7 +1417,8 @@ int rs_rollout_policy(rs_handle* h, int32_t steps, int32_t policy, const rs_obs_
     const int rc = order_envs(h, st);
     if (rc) return rc;
   }
-  CUDA_TRY(launch_tables(h, digests_dev ? k_rollout<true> : k_rollout<false>, L.grid, L.block, L.smem, st, h->S,
+  CUDA_TRY(launch_tables(h, (digests_dev || h->check_steps) ? k_rollout<true> : k_rollout<false>, L.grid, L.block,
+                         L.smem, st, h->S,
                          h->D, h->cfg, steps, o, obs ? obs_slots : 0, actions_log, actors_log, step_out(h, traj), stats_dev, digests_dev,
                          h->dig_obs, step_out(h, out), L.epw, nullptr, L.staged, policy, L.glog2, h->check_steps,
                          L.ordered ? (const int32_t*)h->order : nullptr, L.ordered ? h->kind : nullptr,

@@ -1087,7 +1087,7 @@ struct Engine {
     if (g.terminated || g.truncated) terminal_rewards(r);
     else r[0] = r[1] = r[2] = r[3] = 0.0f;
   }
-  RS_HD void terminal_rewards(float* r) const {
+  RS_COLD void terminal_rewards(float* r) const {  // game end only
     if (C.reward_scheme == RS_REWARD_RANK) {
       const double RR[4] = {1.0, 0.333, -0.333, -1.0};
       for (int s = 0; s < 4; s++) {

@@ -366,9 +366,15 @@ RS_HD void finish_hand(const Tabs& T, Hand& h) {
   h.waits = (sh == 0 && hi::nconc(h.info) + 3 * melds == 13) ? compute_waits(T, h, melds) : 0ull;
 }
 
-// add / remove one tile without the rebuild (hand_add / hand_remove parts)
+// add / remove one tile without the rebuild (hand_add / hand_remove parts);
+// -DRS_OL_HANDOPS puts them out of line (A/B)
+#if defined(RS_OL_HANDOPS)
+#define RS_OL_HANDOP RS_COLD
+#else
+#define RS_OL_HANDOP RS_HD
+#endif
 // tok: 0 no-red tokens, 1 red-rule tokens, -1 scratch copy (tokens unused)
-RS_HD void hand_put(const Tabs& T, Hand& h, int t, int tok) {
+RS_OL_HANDOP void hand_put(const Tabs& T, Hand& h, int t, int tok) {
   RS_CHECK((unsigned)t < (unsigned)RS_NUM_TILES && !h.has(t) && hi::nconc(h.info) < 14);
   const int k = t >> 2, s = kind_suit(k);
   h.set_word(t >> 5, h.word(t >> 5) | (1u << (t & 31)));
@@ -378,7 +384,7 @@ RS_HD void hand_put(const Tabs& T, Hand& h, int t, int tok) {
   h.info = hi::set_nconc(h.info, hi::nconc(h.info) + 1);
   if (tok >= 0) tok_insert(h.tlo, h.thi, token_of(t, tok == 1));
 }
-RS_HD void hand_take(const Tabs& T, Hand& h, int t, int tok) {
+RS_OL_HANDOP void hand_take(const Tabs& T, Hand& h, int t, int tok) {
   RS_CHECK((unsigned)t < (unsigned)RS_NUM_TILES && h.has(t) && hi::nconc(h.info) > 0);
   const int k = t >> 2, s = kind_suit(k);
   h.set_word(t >> 5, h.word(t >> 5) & ~(1u << (t & 31)));
