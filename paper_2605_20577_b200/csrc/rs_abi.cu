@@ -563,6 +563,7 @@ __global__ void __launch_bounds__(BLOCK) k_observe(const __grid_constant__ Soa S
 // lanes write quarters of the window, so the group syncs around it)
 __device__ __noinline__ uint64_t digest_wide(uint64_t d, int a, const Engine& E, const Mask115& m, const float* r,
                                              const rs_obs_out& dobs, uint32_t gm) {
+  __syncwarp(gm);  // the ring entries other lanes of the group wrote
   d = digest_state(digest_step(d, a, E, m, r), E);
   write_obs(E, E.g.current_player, dobs, E.e);
   __syncwarp(gm);

@@ -82,11 +82,24 @@ struct Mask115 {
 // observe() will encode it (observe.py:92-106), into the four observer
 // streams
 RS_HD void emit_event_impl(uint16_t* ring, uint32_t* ob, uint32_t p, int rule, int type, int actor, int tile) {
-  ring[p] = (uint16_t)(type | ((actor + 1) << 4) | ((tile + 1) << 7));
   const uint32_t ty = (uint32_t)(type <= 8 ? type : type - 1);  // ron / tsumo share token 8
   const uint32_t tok = tile < 0 ? 37u
                        : (rule == RS_RULE_RED && is_red_tile(tile)) ? (uint32_t)(34 + red_index_of_kind(tile >> 2))
                                                                     : (uint32_t)(tile >> 2);
+  if (RS_EMIT_LANES_ON && grp_size() >= 4) {
+    // lane group: lane o < 4 writes observer o's entry (one store
+    // instruction for the four streams), lane 0 the ring; readers in the
+    // group sync first (grp_sync in write_obs / digest_wide)
+    const int o = grp_sub();
+    if (o == 0) ring[p] = (uint16_t)(type | ((actor + 1) << 4) | ((tile + 1) << 7));
+    if (o < 4) {
+      const uint32_t rel = actor >= 0 ? (uint32_t)((actor - o) & 3) : 0u;
+      const uint32_t t = (type == EV_DRAW && actor != o) ? 37u : tok;
+      ob[o * EVOBS_SLOTS + p] = ty | (rel << 8) | (t << 16);
+    }
+    return;
+  }
+  ring[p] = (uint16_t)(type | ((actor + 1) << 4) | ((tile + 1) << 7));
 #pragma unroll
   for (int o = 0; o < 4; o++) {
     const uint32_t rel = actor >= 0 ? (uint32_t)((actor - o) & 3) : 0u;

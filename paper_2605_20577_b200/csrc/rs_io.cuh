@@ -50,6 +50,7 @@ RS_HD void write_obs(const Engine& E, int seat, const rs_obs_out& obs, int64_t o
     // each -- the same instructions on different data, so the warp runs
     // the quarter body once
     const int G = grp_size(), sub = grp_sub();
+    if (RS_EMIT_LANES_ON && G >= 4) grp_sync();  // entries written by other lanes of the group
     if (G >= 8 && RS_WIN16) {
       // 8+ lanes per env: lane `sub` encodes slots [per * sub, per * (sub + 1))
       // (per = 4 at 16+ lanes, 8 at 8): independent loads, 3 words per 4
