@@ -18,6 +18,7 @@
 
 #include <algorithm>
 #include <mutex>
+#include <new>
 #include <string>
 
 #include <cub/device/device_radix_sort.cuh>
@@ -43,10 +44,24 @@ constexpr int BLOCK = 128;
 // dynamic shared memory: the staged tables, then either one stage slot per
 // env of the CTA (staged stepping kernels) or a 144-byte shuffle scratch
 // per thread (kernels working on the blocks in HBM)
+// -DRS_ENGINE_SMEM (measured alternative): the stepping kernels' Engine
+// objects (the game header and the env context, addressed through `this`
+// by the out-of-line members) live in a per-thread shared-memory slot
+// instead of the thread's local memory, which misses L1 at large batches
+// (ncu: ~100 local loads per warp-step at 262 K envs, 32 % L1 hits).
+// 26 % slower at 4,096 envs, 4 % at 1 M: in local memory the compiler
+// keeps most header fields in registers between the out-of-line calls.
+#if defined(RS_ENGINE_SMEM)
+constexpr int ENGINE_SLOT = (int)((sizeof(Engine) + 15) & ~(size_t)15);
+#else
+constexpr int ENGINE_SLOT = 0;
+#endif
 constexpr int smem_staged(int block, int slots, int glog2 = 0) {
-  return WALL_SLOT_OFF + scratch_bytes(block, glog2) + slots * (int)SLOT_BYTES;
+  return WALL_SLOT_OFF + scratch_bytes(block, glog2) + block * ENGINE_SLOT + slots * (int)SLOT_BYTES;
 }
-constexpr int smem_for(int block, int glog2 = 0) { return WALL_SLOT_OFF + scratch_bytes(block, glog2); }
+constexpr int smem_for(int block, int glog2 = 0) {
+  return WALL_SLOT_OFF + scratch_bytes(block, glog2) + block * ENGINE_SLOT;
+}
 // bytes of the staged t3 | t1 | t2 block (a TMA bulk copy is a multiple of 16 B)
 constexpr uint32_t STAGE_BYTES = (SMEM_TABLE_BYTES + 15u) & ~15u;
 
@@ -275,9 +290,19 @@ __device__ __forceinline__ void prefetch_env(const Soa& S, int e, int sub, int G
 // copy completing on the slot's mbarrier, the step runs on shared memory,
 // and the block moves back with one bulk copy (bulk_group).
 __device__ __forceinline__ uint32_t slot_off(int slot, int glog2) {  // after the shuffle scratch
-  const uint32_t o = (uint32_t)WALL_SLOT_OFF + (uint32_t)scratch_bytes((int)blockDim.x, glog2) + (uint32_t)slot * SLOT_BYTES;
+  const uint32_t o = (uint32_t)WALL_SLOT_OFF + (uint32_t)scratch_bytes((int)blockDim.x, glog2) +
+                     blockDim.x * (uint32_t)ENGINE_SLOT + (uint32_t)slot * SLOT_BYTES;
   return o;
 }
+// this thread's Engine slot (RS_ENGINE_SMEM), after the shuffle scratch
+__device__ __forceinline__ uint8_t* engine_slot(int glog2) {
+  return g_smem + WALL_SLOT_OFF + scratch_bytes((int)blockDim.x, glog2) + threadIdx.x * ENGINE_SLOT;
+}
+#if defined(RS_ENGINE_SMEM)
+#define RS_ENGINE(name, glog2, ...) Engine& name = *new (engine_slot(glog2)) Engine(__VA_ARGS__)
+#else
+#define RS_ENGINE(name, glog2, ...) Engine name(__VA_ARGS__)
+#endif
 __device__ __forceinline__ uint32_t smem_addr(uint32_t off) {
   return (uint32_t)__cvta_generic_to_shared(g_smem) + off;
 }
@@ -463,7 +488,7 @@ __global__ void __launch_bounds__(ROLL_BLOCK, ROLL_MINB) k_step(const __grid_con
   }
   if ((prefetch & 3) && !staged) prefetch_env(S, e, sub, 1 << glog2, prefetch & 3);
   const int action = actions[e];  // may live in mapped host memory (HostStepper)
-  Engine E(S, T, C, e, staged ? g_smem + sb : S.blk + (size_t)e * BLK_BYTES);
+  RS_ENGINE(E, glog2, S, T, C, e, staged ? g_smem + sb : S.blk + (size_t)e * BLK_BYTES);
   E.load();
   tables_wait();
   Mask115 m;
@@ -616,7 +641,7 @@ __global__ void __launch_bounds__(ROLL_BLOCK, ROLL_MINB) k_rollout(const __grid_
       phase ^= 1u;
     }
     if ((prefetch & 3) && !staged) prefetch_env(S, e, sub, 1 << glog2, prefetch & 3);
-    Engine E(S, T, C, e, staged ? g_smem + sb : S.blk + (size_t)e * BLK_BYTES);
+    RS_ENGINE(E, glog2, S, T, C, e, staged ? g_smem + sb : S.blk + (size_t)e * BLK_BYTES);
     E.load();
     uint64_t d = digests ? digests[e] : 0ull;
     if (!tables_ready) {
