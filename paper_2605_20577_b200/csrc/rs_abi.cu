@@ -1210,7 +1210,6 @@ int rs_create(rs_handle** out, int64_t n_envs, const rs_config* cfg, int32_t dev
   }
   Part parts[] = {
       {(void**)&S.blk, (size_t)BLK_BYTES * n},
-      {(void**)&S.mtiles, 64 * n},           {(void**)&S.minfo, 64 * n},
       {(void**)&S.river, 4 * RS_MAX_RIVER * 2 * n},
       {(void**)&S.events, 64 * 2 * n},
       {(void**)&S.evobs, (size_t)EVOBS_BYTES * n},

@@ -213,11 +213,11 @@ struct Engine {
   }
   RS_HD uint32_t meld_info(int s, int i) const {
     RS_CHECK((unsigned)s < 4u && (unsigned)i < 4u);
-    return S.minfo[at(s * 4 + i)];
+    return sword(bp, W_MELD + 2 * (4 * s + i) + 1);
   }
   RS_HD uint32_t meld_tiles(int s, int i) const {
     RS_CHECK((unsigned)s < 4u && (unsigned)i < 4u);
-    return S.mtiles[at(s * 4 + i)];
+    return sword(bp, W_MELD + 2 * (4 * s + i));
   }
 
   // engine.py:100-102 (64-slot ring; the full history is reconstructed by
@@ -910,8 +910,8 @@ struct Engine {
     for (int i = 0; i < nids; i++) packed |= (uint32_t)t[i] << (8 * i);
     const int nm = hi::nmelds(h.info);
     RS_CHECK((unsigned)seat < 4u && (unsigned)nm < 4u && nids >= 3 && nids <= 4);
-    S.mtiles[at(seat * 4 + nm)] = packed;
-    S.minfo[at(seat * 4 + nm)] = mi::make(type, nids, from, called);
+    sword(bp, W_MELD + 2 * (4 * seat + nm)) = packed;
+    sword(bp, W_MELD + 2 * (4 * seat + nm) + 1) = mi::make(type, nids, from, called);
     h.info = hi::set_nmelds(h.info, nm + 1);
   }
   // engine.py:696-702
@@ -996,9 +996,9 @@ struct Engine {
           int t[4] = {(int)(mt & 255), (int)((mt >> 8) & 255), (int)((mt >> 16) & 255), tile};
           for (int a = 1; a < 4; a++)
             for (int b = a; b > 0 && t[b - 1] > t[b]; b--) { const int x = t[b]; t[b] = t[b - 1]; t[b - 1] = x; }
-          S.mtiles[at(seat * 4 + i)] = (uint32_t)t[0] | ((uint32_t)t[1] << 8) | ((uint32_t)t[2] << 16) |
+          sword(bp, W_MELD + 2 * (4 * seat + i)) = (uint32_t)t[0] | ((uint32_t)t[1] << 8) | ((uint32_t)t[2] << 16) |
                                        ((uint32_t)t[3] << 24);
-          S.minfo[at(seat * 4 + i)] = mi::make(M_KAN_ADDED, 4, mi::from(mf), mi::called(mf));
+          sword(bp, W_MELD + 2 * (4 * seat + i) + 1) = mi::make(M_KAN_ADDED, 4, mi::from(mf), mi::called(mf));
         }
       }
     hand_take(T, h, tile, tok());

@@ -407,8 +407,8 @@ RS_COLD void import_env(Engine& E, const rs_env_rec& r) {
       const rs_meld_rec& m = hr.melds[i];
       uint32_t packed = 0;
       for (int j = 0; j < m.n_tiles; j++) packed |= (uint32_t)m.tiles[j] << (8 * j);
-      S.mtiles[(size_t)(s * 4 + i) * S.n + E.e] = packed;
-      S.minfo[(size_t)(s * 4 + i) * S.n + E.e] = mi::make(m.type, m.n_tiles, m.from_seat, m.called_tile);
+      sword(E.bp, W_MELD + 2 * (4 * s + i)) = packed;
+      sword(E.bp, W_MELD + 2 * (4 * s + i) + 1) = mi::make(m.type, m.n_tiles, m.from_seat, m.called_tile);
     }
     uint64_t rk = 0;
     for (int i = 0; i < hr.n_river; i++) {

@@ -40,7 +40,7 @@ constexpr int EVOBS_BYTES = 4 * EVOBS_SLOTS * 4;             // per env
 constexpr uint32_t EVOBS_PAD = 37u << 16;                    // (0, 0, 37)
 
 // ------------------------------------------------ the env block (HBM)
-// 100 words then the 144-byte wall; in shared memory each env's slot adds
+// 132 words then the 144-byte wall; in shared memory each env's slot adds
 // its mbarrier (the bulk copy's completion) and pads to 16 bytes
 constexpr uint32_t W_HDR = 0;      // 4 x uint4 packed game scalars (Game::pack)
 constexpr uint32_t W_SCORES = 16;  // int4
@@ -52,17 +52,20 @@ constexpr uint32_t W_HCODE = 72;   // 4 seats x 4 base-5 codes m, p, s, z
 constexpr uint32_t W_HCLS = 88;    // 4 seats: table class per suit (4 x u8)
 constexpr uint32_t W_HINFO = 92;   // 4 seats: packed HandState flags
 constexpr uint32_t W_LEGAL = 96;   // 4 words env-view legal mask
-constexpr uint32_t W_WORDS = 100;
-constexpr uint32_t BLK_WALL = 4 * W_WORDS;               // 400: wall bytes
-constexpr uint32_t BLK_BYTES = BLK_WALL + WALL_STRIDE;   // 544 per env in HBM (34 x 16 B)
+// melds: seat s, meld i at words W_MELD + 2 (4 s + i): tile ids (4 x u8),
+// then type | n | from | called -- a seat's four melds are one 32-byte
+// sector, prefetched with the rest of the block (they used to be
+// field-major arrays: a DRAM round trip per meld read at large batches)
+constexpr uint32_t W_MELD = 100;
+constexpr uint32_t W_WORDS = 132;
+constexpr uint32_t BLK_WALL = 4 * W_WORDS;               // 528: wall bytes
+constexpr uint32_t BLK_BYTES = BLK_WALL + WALL_STRIDE;   // 672 per env in HBM (42 x 16 B)
 constexpr uint32_t SLOT_BAR = BLK_BYTES;                 // mbarrier of the slot
-constexpr uint32_t SLOT_BYTES = BLK_BYTES + 16;          // 560 per env in shared memory
+constexpr uint32_t SLOT_BYTES = BLK_BYTES + 16;          // 688 per env in shared memory
 
 struct Soa {
   int n;
-  uint8_t* blk;      // [n][544] env blocks (layout above)
-  uint32_t* mtiles;  // [4 seat][4 meld][n] tile ids (4 x u8)
-  uint32_t* minfo;   // [4 seat][4 meld][n] type | n | from | called
+  uint8_t* blk;      // [n][672] env blocks (layout above)
   uint16_t* river;   // [4 seat][40][n] tile | flags << 8
   uint16_t* events;  // [n][64] ring (128 B per env): type | (actor+1) << 4 | (tile+1) << 7
   // [n][4 observer][64] the same ring pre-encoded for each observer as
@@ -95,8 +98,7 @@ constexpr int64_t canonical_state_bytes() {
 }
 
 inline int64_t bytes_per_env() {
-  return BLK_BYTES + 4 * 4 * 4 + 4 * 4 * 4 + 4 * RS_MAX_RIVER * 2 + RS_EVENT_WINDOW * 2 + EVOBS_BYTES +
-         (int64_t)sizeof(rs_result_rec);
+  return BLK_BYTES + 4 * RS_MAX_RIVER * 2 + RS_EVENT_WINDOW * 2 + EVOBS_BYTES + (int64_t)sizeof(rs_result_rec);
 }
 
 struct Cfg {

@@ -39,8 +39,6 @@ void* hc_create(int n, const rs_config* cfg) {
   Soa& S = h->S;
   S.n = n;
   plan.push_back({(void**)&S.blk, (size_t)BLK_BYTES * n});
-  plan.push_back({(void**)&S.mtiles, 16 * 4 * (size_t)n});
-  plan.push_back({(void**)&S.minfo, 16 * 4 * (size_t)n});
   plan.push_back({(void**)&S.river, 4 * RS_MAX_RIVER * 2 * (size_t)n});
   plan.push_back({(void**)&S.events, 64 * 2 * (size_t)n});
   plan.push_back({(void**)&S.evobs, (size_t)EVOBS_BYTES * n});
