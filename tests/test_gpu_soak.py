@@ -57,11 +57,15 @@ def test_bit_exact_on_1e5_hands(rule, monkeypatch):
 
 
 @pytest.mark.parametrize("rule", ("no-red", "red"))
-def test_heuristic_soak_matches_oracle(rule):
+def test_heuristic_soak_matches_oracle(rule, monkeypatch):
     """the heuristic policy (policies.py:51-109) reaches tenpai, riichi,
     calls and wins at rates random play never does: 65,536 envs x 500 fused
     heuristic steps (>= 10^5 hands), every trajectory digest equal to the
-    oracle's, plus the device invariant checker clean afterwards"""
+    oracle's, the fast invariants after every step and the full checker
+    clean afterwards"""
+    from paper_2605_20577_b200 import abi
+
+    monkeypatch.setenv("RINSHAN_CHECK", "1")
     n, steps, seed, chunk = 65536, 500, 4242, 2048
     env = BatchEnv(n, EnvConfig(rule=rule)).init(seed=seed, index_base=0)
     digests = torch.zeros(n, dtype=torch.int64, device="cuda")
@@ -69,6 +73,7 @@ def test_heuristic_soak_matches_oracle(rule):
     env.rollout(steps, digests=digests, stats=stats, policy="heuristic")
     flags = env.check_invariants(fast=False)
     torch.cuda.synchronize()
+    assert int((env.status.int() & abi.STATUS_INVARIANT).count_nonzero().item()) == 0
     got = [int(x) & ((1 << 64) - 1) for x in digests.cpu().tolist()]
     games = int(stats[1].item())
     assert int(flags.count_nonzero().item()) == 0
