@@ -276,10 +276,10 @@ __device__ __forceinline__ void prefetch_env(const Soa& S, int e, int sub, int G
   const uintptr_t b0 = (uintptr_t)(S.blk + (size_t)e * BLK_BYTES) & ~(uintptr_t)127;
   const uintptr_t b1 = ((uintptr_t)(S.blk + (size_t)e * BLK_BYTES) + BLK_BYTES - 1) & ~(uintptr_t)127;
   const int nb = (int)((b1 - b0) >> 7) + 1;
-  const int total = nb + (mode >= 2 ? EVOBS_BYTES / 128 : 0);
+  const int total = nb + (mode >= 2 ? RS_EVENT_WINDOW * 4 / 128 : 0);
   for (int k = sub; k < total; k += G) {
     const uintptr_t a = k < nb ? b0 + ((uintptr_t)k << 7)
-                               : (uintptr_t)(S.evobs + (size_t)e * (4 * EVOBS_SLOTS)) + ((uintptr_t)(k - nb) << 7);
+                               : (uintptr_t)(S.events + (size_t)e * RS_EVENT_WINDOW) + ((uintptr_t)(k - nb) << 7);
     asm volatile("prefetch.global.L1 [%0];" ::"l"(a));
   }
 }
@@ -1211,8 +1211,7 @@ int rs_create(rs_handle** out, int64_t n_envs, const rs_config* cfg, int32_t dev
   Part parts[] = {
       {(void**)&S.blk, (size_t)BLK_BYTES * n},
       {(void**)&S.river, 4 * RS_MAX_RIVER * 2 * n},
-      {(void**)&S.events, 64 * 2 * n},
-      {(void**)&S.evobs, (size_t)EVOBS_BYTES * n},
+      {(void**)&S.events, 64 * 4 * n},
       {(void**)&S.results, sizeof(rs_result_rec) * n},
       {(void**)&h->legal_bits_tmp, 16 * n},  {(void**)&h->rec_dev, sizeof(rs_env_rec)},
       {(void**)&h->kind, n},                 {(void**)&h->kind_sorted, n},

@@ -50,10 +50,6 @@ inline uint4 make_uint4(uint32_t x, uint32_t y, uint32_t z, uint32_t w) { return
 
 // Measured alternatives kept buildable (tools/build_variant.sh -D...):
 //   -DRS_AB_OFF_WIN16   observation window over 4 lanes instead of 8 / 16
-//   -DRS_EMIT_LANES     lane o of a group writes observer o's entry of an
-//                       event (instead of every lane all four): 1.5 % slower
-//                       at 4,096 envs, fused -3 % (the syncs and lane
-//                       branches cost more than three stores)
 //   -DRS_CLAIM_LANES    opponents' claim checks on three lanes of the env's
 //                       group, combined by one warp reduction (2 % slower at
 //                       4,096 envs: the checks diverge per lane anyway)
@@ -68,11 +64,6 @@ inline uint4 make_uint4(uint32_t x, uint32_t y, uint32_t z, uint32_t w) { return
 #define RS_CLAIM_LANES_ON 1
 #else
 #define RS_CLAIM_LANES_ON 0
-#endif
-#if defined(RS_EMIT_LANES)
-#define RS_EMIT_LANES_ON 1
-#else
-#define RS_EMIT_LANES_ON 0
 #endif
 #if defined(RS_SWAP5)
 #define RS_SWAP5_ON 1

@@ -78,38 +78,34 @@ struct Mask115 {
   }
 };
 
-// engine.py:100-102 event, written into the env's 64-slot ring and, as
-// observe() will encode it (observe.py:92-106), into the four observer
-// streams
-RS_HD void emit_event_impl(uint16_t* ring, uint32_t* ob, uint32_t p, int rule, int type, int actor, int tile) {
-  const uint32_t ty = (uint32_t)(type <= 8 ? type : type - 1);  // ron / tsumo share token 8
+// engine.py:100-102 event, written into the env's 64-slot ring as one word:
+// bits 0-14 the event (type | (actor + 1) << 4 | (tile + 1) << 7), bits
+// 16-19 its observation type token (ron / tsumo share token 8) and bits
+// 20-25 its visible tile token (observe.py:92-106: red fives 34-36, none
+// 37) -- everything observe() needs except the observer, so one store per
+// event (round 1 also kept the event pre-encoded for each of the four
+// observers: four more scattered sector writes per event, 1 KB per env)
+RS_HD uint32_t event_word(int rule, int type, int actor, int tile) {
+  const uint32_t ty = (uint32_t)(type <= 8 ? type : type - 1);
   const uint32_t tok = tile < 0 ? 37u
                        : (rule == RS_RULE_RED && is_red_tile(tile)) ? (uint32_t)(34 + red_index_of_kind(tile >> 2))
                                                                     : (uint32_t)(tile >> 2);
-  if (RS_EMIT_LANES_ON && grp_size() >= 4) {
-    // lane group: lane o < 4 writes observer o's entry (one store
-    // instruction for the four streams), lane 0 the ring; readers in the
-    // group sync first (grp_sync in write_obs / digest_wide)
-    const int o = grp_sub();
-    if (o == 0) ring[p] = (uint16_t)(type | ((actor + 1) << 4) | ((tile + 1) << 7));
-    if (o < 4) {
-      const uint32_t rel = actor >= 0 ? (uint32_t)((actor - o) & 3) : 0u;
-      const uint32_t t = (type == EV_DRAW && actor != o) ? 37u : tok;
-      ob[o * EVOBS_SLOTS + p] = ty | (rel << 8) | (t << 16);
-    }
-    return;
-  }
-  ring[p] = (uint16_t)(type | ((actor + 1) << 4) | ((tile + 1) << 7));
-#pragma unroll
-  for (int o = 0; o < 4; o++) {
-    const uint32_t rel = actor >= 0 ? (uint32_t)((actor - o) & 3) : 0u;
-    const uint32_t t = (type == EV_DRAW && actor != o) ? 37u : tok;  // opponents' draws hidden
-    ob[o * EVOBS_SLOTS + p] = ty | (rel << 8) | (t << 16);
-  }
+  return (uint32_t)(type | ((actor + 1) << 4) | ((tile + 1) << 7)) | (ty << 16) | (tok << 20);
 }
+// the event as observer `seat` sees it (observe.py:92-106): type token,
+// relative actor, visible tile token (opponents' draws hidden) in bytes 0-2
+RS_HD uint32_t event_view(uint32_t x, int seat) {
+  const uint32_t a1 = (x >> 4) & 7u;  // actor + 1, 0 for none
+  const uint32_t rel = a1 ? (a1 + 3u - (uint32_t)seat) & 3u : 0u;
+  const bool hidden = (x & 15u) == (uint32_t)EV_DRAW && a1 != (uint32_t)seat + 1u;
+  const uint32_t tok = hidden ? 37u : (x >> 20) & 63u;
+  return ((x >> 16) & 15u) | (rel << 8) | (tok << 16);
+}
+// the canonical event (type | (actor + 1) << 4 | (tile + 1) << 7)
+RS_HD uint32_t event_raw(uint32_t x) { return x & 0x7FFFu; }
 // out of line, called with scalars (19 emit sites; DESIGN §4 item 25)
-RS_COLD void emit_event(uint16_t* ring, uint32_t* ob, uint32_t p, int rule, int type, int actor, int tile) {
-  emit_event_impl(ring, ob, p, rule, type, actor, tile);
+RS_COLD void emit_event(uint32_t* ring, uint32_t p, int rule, int type, int actor, int tile) {
+  ring[p] = event_word(rule, type, actor, tile);
 }
 
 // engine members that can go out of line for a smaller hot code footprint
@@ -223,8 +219,7 @@ struct Engine {
   // engine.py:100-102 (64-slot ring; the full history is reconstructed by
   // the host while stepping)
   RS_HD void emit(int type, int actor, int tile) {
-    emit_event(S.events + (uint32_t)e * RS_EVENT_WINDOW, S.evobs + (uint32_t)e * (4 * EVOBS_SLOTS),
-               g.events_len & 63u, C.rule, type, actor, tile);
+    emit_event(S.events + (uint32_t)e * RS_EVENT_WINDOW, g.events_len & 63u, C.rule, type, actor, tile);
     g.events_len++;
   }
 

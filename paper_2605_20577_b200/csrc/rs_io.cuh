@@ -40,7 +40,7 @@ RS_HD void write_obs(const Engine& E, int seat, const rs_obs_out& obs, int64_t o
     // of the window is ring entry (len + i) & 63 of the observer's
     // pre-encoded stream (Engine::emit), pads while i < 64 - len; pack 4
     // triples into 3 words with byte permutes
-    const uint32_t* ob = S.evobs + (uint32_t)E.e * (4 * EVOBS_SLOTS) + (uint32_t)seat * EVOBS_SLOTS;
+    const uint32_t* ring = S.events + (uint32_t)E.e * RS_EVENT_WINDOW;
     const uint32_t len = g.events_len;
     const int pad = len >= 64u ? 0 : 64 - (int)len;
     uint4* dst = reinterpret_cast<uint4*>(obs.event_tokens + o * 192);
@@ -50,7 +50,6 @@ RS_HD void write_obs(const Engine& E, int seat, const rs_obs_out& obs, int64_t o
     // each -- the same instructions on different data, so the warp runs
     // the quarter body once
     const int G = grp_size(), sub = grp_sub();
-    if (RS_EMIT_LANES_ON && G >= 4) grp_sync();  // entries written by other lanes of the group
     if (G >= 8 && RS_WIN16) {
       // 8+ lanes per env: lane `sub` encodes slots [per * sub, per * (sub + 1))
       // (per = 4 at 16+ lanes, 8 at 8): independent loads, 3 words per 4
@@ -62,7 +61,8 @@ RS_HD void write_obs(const Engine& E, int seat, const rs_obs_out& obs, int64_t o
           const int i0 = per * sub + c;
           uint32_t v[4];
 #pragma unroll
-          for (int j = 0; j < 4; j++) v[j] = i0 + j < pad ? EVOBS_PAD : ob[(len + (uint32_t)(i0 + j)) & 63u];
+          for (int j = 0; j < 4; j++)
+            v[j] = i0 + j < pad ? EVOBS_PAD : event_view(ring[(len + (uint32_t)(i0 + j)) & 63u], seat);
           d32[3 * c / 4] = byte_perm(v[0], v[1], 0x4210);
           d32[3 * c / 4 + 1] = byte_perm(v[1], v[2], 0x5421);
           d32[3 * c / 4 + 2] = byte_perm(v[2], v[3], 0x6542);
@@ -89,9 +89,9 @@ RS_HD void write_obs(const Engine& E, int seat, const rs_obs_out& obs, int64_t o
       }
     };
     if (pad == 0)  // a full window (every step after the first 64 events)
-      emit_window([&](int i) -> uint32_t { return ob[(len + (uint32_t)i) & 63u]; });
+      emit_window([&](int i) -> uint32_t { return event_view(ring[(len + (uint32_t)i) & 63u], seat); });
     else
-      emit_window([&](int i) -> uint32_t { return i < pad ? EVOBS_PAD : ob[i - pad]; });
+      emit_window([&](int i) -> uint32_t { return i < pad ? EVOBS_PAD : event_view(ring[i - pad], seat); });
     }
   }
   if (obs.shanten) obs.shanten[o] = (int8_t)hi::shanten(h.info);
@@ -217,7 +217,7 @@ RS_COLD uint64_t digest_state(uint64_t d, const Engine& E) {
     uint32_t v[4];
     for (int k = 0; k < 4; k++) {
       const int idx = (int)g.events_len - 1 - (j + k);
-      v[k] = idx >= 0 ? S.events[(size_t)E.e * RS_EVENT_WINDOW + (idx & 63)] : 0u;
+      v[k] = idx >= 0 ? event_raw(S.events[(size_t)E.e * RS_EVENT_WINDOW + (idx & 63)]) : 0u;
     }
     d = dfold(d, dpack4(v[0], v[1], v[2], v[3]));
   }
@@ -346,7 +346,7 @@ RS_COLD void export_env(Engine& E, const Cfg& C, rs_env_rec& r) {
   for (int i = 0; i < 64; i++) {
     if (i < cnt) {
       const uint32_t idx = (g.events_len - (uint32_t)cnt + (uint32_t)i) & 63u;
-      const uint32_t ev = S.events[(uint32_t)E.e * RS_EVENT_WINDOW + idx];
+      const uint32_t ev = event_raw(S.events[(uint32_t)E.e * RS_EVENT_WINDOW + idx]);
       r.events[i][0] = (int16_t)(ev & 15);
       r.events[i][1] = (int16_t)((int)((ev >> 4) & 7) - 1);
       r.events[i][2] = (int16_t)((int)((ev >> 7) & 255) - 1);

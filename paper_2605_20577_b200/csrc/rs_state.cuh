@@ -35,9 +35,7 @@ constexpr int ENV_SCRATCH = 288;  // 148 + 136, 16-byte multiple
 RS_HD constexpr int scratch_bytes(int block, int glog2) {
   return glog2 == 0 ? block * SCRATCH_STRIDE : (block >> glog2) * ENV_SCRATCH;
 }
-constexpr int EVOBS_SLOTS = RS_EVENT_WINDOW;                 // per observer
-constexpr int EVOBS_BYTES = 4 * EVOBS_SLOTS * 4;             // per env
-constexpr uint32_t EVOBS_PAD = 37u << 16;                    // (0, 0, 37)
+constexpr uint32_t EVOBS_PAD = 37u << 16;  // an observation window pad slot (0, 0, 37)
 
 // ------------------------------------------------ the env block (HBM)
 // 132 words then the 144-byte wall; in shared memory each env's slot adds
@@ -67,11 +65,10 @@ struct Soa {
   int n;
   uint8_t* blk;      // [n][672] env blocks (layout above)
   uint16_t* river;   // [4 seat][40][n] tile | flags << 8
-  uint16_t* events;  // [n][64] ring (128 B per env): type | (actor+1) << 4 | (tile+1) << 7
-  // [n][4 observer][64] the same ring pre-encoded for each observer as
-  // observe() emits it (type token, relative actor, visible tile token);
-  // observe() reads the window slots (len + i) & 63 and synthesizes pads
-  uint32_t* evobs;
+  // [n][64] ring (256 B per env) of event words (rs_engine.cuh event_word):
+  // the event and its observer-independent tokens; observe() reads the
+  // window slots (len + i) & 63 and synthesizes pads
+  uint32_t* events;
   rs_result_rec* results;  // [n] last kyoku result (written at kyoku end)
 };
 
@@ -98,7 +95,7 @@ constexpr int64_t canonical_state_bytes() {
 }
 
 inline int64_t bytes_per_env() {
-  return BLK_BYTES + 4 * RS_MAX_RIVER * 2 + RS_EVENT_WINDOW * 2 + EVOBS_BYTES + (int64_t)sizeof(rs_result_rec);
+  return BLK_BYTES + 4 * RS_MAX_RIVER * 2 + RS_EVENT_WINDOW * 4 + (int64_t)sizeof(rs_result_rec);
 }
 
 struct Cfg {

@@ -40,8 +40,7 @@ void* hc_create(int n, const rs_config* cfg) {
   S.n = n;
   plan.push_back({(void**)&S.blk, (size_t)BLK_BYTES * n});
   plan.push_back({(void**)&S.river, 4 * RS_MAX_RIVER * 2 * (size_t)n});
-  plan.push_back({(void**)&S.events, 64 * 2 * (size_t)n});
-  plan.push_back({(void**)&S.evobs, (size_t)EVOBS_BYTES * n});
+  plan.push_back({(void**)&S.events, 64 * 4 * (size_t)n});
   plan.push_back({(void**)&S.results, sizeof(rs_result_rec) * (size_t)n});
   for (auto& p : plan) {
     void* m = nullptr;
