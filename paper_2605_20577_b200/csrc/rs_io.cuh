@@ -37,9 +37,9 @@ RS_HD void write_obs(const Engine& E, int seat, const rs_obs_out& obs, int64_t o
   }
   if (obs.event_tokens) {
     // 64 x (type, rel actor, token), oldest first, padded (0,0,37): slot i
-    // of the window is ring entry (len + i) & 63 of the observer's
-    // pre-encoded stream (Engine::emit), pads while i < 64 - len; pack 4
-    // triples into 3 words with byte permutes
+    // of the window is ring entry (len + i) & 63 seen by this observer
+    // (event_view), pads while i < 64 - len; pack 4 triples into 3 words
+    // with byte permutes
     const uint32_t* ring = S.events + (uint32_t)E.e * RS_EVENT_WINDOW;
     const uint32_t len = g.events_len;
     const int pad = len >= 64u ? 0 : 64 - (int)len;
