@@ -60,6 +60,8 @@ def parse(argv=None):
                    help="torch.distributed backend at N>1 (default: nccl; the reference arm always uses gloo)")
     p.add_argument("--cpu-seconds", type=float, default=10.0, help="CPU baseline sample budget (wall seconds)")
     p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-python-ref", action="store_true",
+                   help="reference arm: skip timing the Python reference itself (baseline/_ref)")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-fused", action="store_true", help="skip the fused 100-step rollout timing")
     p.add_argument("--no-rows", action="store_true", help="skip the red / 1M-env extra rows")
@@ -325,6 +327,7 @@ def reference_arm(args, rank, world):
     warm = args.steady_warm + args.warmup
     sps, threads, wall, games = cpu_rollout(args, n, args.steps, warm)
     per_step = cpu_rollout_per_step(args, n, min(args.steps, 50), warm)
+    pyref = None if args.no_python_ref else python_reference(args, n)
     line = {
         "impl": "reference",
         "metric": METRIC,
@@ -350,10 +353,37 @@ def reference_arm(args, rank, world):
         "per_step_barrier": {"value": per_step, "unit": UNIT,
                              "protocol": "the same shards step-major with a barrier after every batch step"},
         "games_completed": games,
+        "python_reference": pyref,
         "e2e": {"value": sps, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
     return 0
+
+
+def python_reference(args, n):
+    """The Python reference itself (mjsim, installed into baseline/_ref from
+    /root/reference with pip --no-index), its own bench CLI on this box's
+    cores: `python -m mjsim.cli bench --batch n --steps 100` (the paper's
+    100 batch steps, fresh games, the runner's 0.25 s warm-up).  For
+    context beside the oracle port, which is the arm's value."""
+    ref = ROOT / "baseline" / "_ref"
+    if not (ref / "mjsim" / "__init__.py").exists():
+        return {"unavailable": "baseline/_ref not installed (pip install --no-index --target baseline/_ref <reference>)"}
+    threads = host_threads()
+    env = dict(os.environ, PYTHONPATH=str(ref), MJSIM_TABLE_PATH="/tmp/mjsim_ref_tables/suit_tables.bin",
+               NUMBA_CACHE_DIR="/tmp/mjsim_ref_numba")
+    cmd = [sys.executable, "-m", "mjsim.cli", "bench", "--rule", args.rule, "--mode", args.mode, "--batch", str(n),
+           "--steps", "100", "--seed", str(args.seed), "--threads", str(threads)]
+    try:
+        out = subprocess.run(cmd, capture_output=True, text=True, timeout=240, env=env).stdout
+        row = [ln for ln in out.splitlines() if ln and not ln.startswith("#") and not ln.startswith("batch")][-1]
+        batch, wall, sps, games = row.split(",")
+        return {"value": float(sps), "unit": UNIT, "cores": threads, "wall_seconds": float(wall),
+                "games_completed": int(games), "sample": f"{n} envs x 100 env steps, fresh games",
+                "cmd": "python -m mjsim.cli bench --rule %s --mode %s --batch %d --steps 100 --threads %d"
+                       % (args.rule, args.mode, n, threads)}
+    except (subprocess.TimeoutExpired, IndexError, ValueError) as e:
+        return {"unavailable": f"mjsim bench failed: {type(e).__name__}"}
 
 
 # ----------------------------------------------------------------- GPU side

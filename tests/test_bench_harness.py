@@ -57,7 +57,7 @@ def test_reference_arm_two_ranks_on_gloo():
     """the driver launches --impl reference like our arm: rank 0 alone
     times the whole-job workload (world x batch envs), one JSON line"""
     r = _torchrun(2, ["--impl", "reference", "--gpus", "2", "--steps", "4", "--warmup", "1", "--steady-warm", "20",
-                      "--batch", "96"])
+                      "--batch", "96", "--no-python-ref"])
     assert r.returncode == 0, r.stderr[-2000:]
     ls = _lines(r.stdout)
     assert len(ls) == 1
@@ -68,8 +68,8 @@ def test_reference_arm_two_ranks_on_gloo():
     # the same envs stepped by one process: identical games (trajectories
     # depend on the global index only)
     r1 = subprocess.run([sys.executable, str(ROOT / "bench.py"), "--impl", "reference", "--steps", "4", "--warmup",
-                         "1", "--steady-warm", "20", "--batch", "192"], capture_output=True, text=True, cwd=ROOT,
-                        timeout=300)
+                         "1", "--steady-warm", "20", "--batch", "192", "--no-python-ref"], capture_output=True, text=True,
+                        cwd=ROOT, timeout=300)
     assert r1.returncode == 0
     assert _lines(r1.stdout)[0]["games_completed"] == line["games_completed"]
 
