@@ -551,10 +551,10 @@ struct Engine {
       m.set(A_PON);
       if (count_of(seat, kind) >= 3 && kan_draw_ok()) m.set(A_KAN_OPEN);
     } else {
-      const int n = kind % 9;
-      if (n <= 6 && count_of(seat, kind + 1) && count_of(seat, kind + 2)) m.set(A_CHI_LOW);
-      if (n >= 1 && n <= 7 && count_of(seat, kind - 1) && count_of(seat, kind + 1)) m.set(A_CHI_MID);
-      if (n >= 2 && count_of(seat, kind - 2) && count_of(seat, kind - 1)) m.set(A_CHI_HIGH);
+      const uint32_t c = chi_bits(seat, kind);
+      if (c & 1u) m.set(A_CHI_LOW);
+      if (c & 2u) m.set(A_CHI_MID);
+      if (c & 4u) m.set(A_CHI_HIGH);
     }
   }
 
@@ -762,12 +762,24 @@ struct Engine {
     }
     g.pending_dora = 0;
   }
-  RS_HD bool can_chi(int s, int kind) const {
+  // the chi variants seat s could make with a discarded suit tile of
+  // `kind` (bit 0 low, 1 mid, 2 high; engine.py:320-327): presence of kinds
+  // kind-2 .. kind+2 from at most two words of the seat's tile set
+  RS_HD uint32_t chi_bits(int s, int kind) const {
     const int n = kind % 9;
-    return (n <= 6 && count_of(s, kind + 1) && count_of(s, kind + 2)) ||
-           (n >= 1 && n <= 7 && count_of(s, kind - 1) && count_of(s, kind + 1)) ||
-           (n >= 2 && count_of(s, kind - 2) && count_of(s, kind - 1));
+    const int base = kind >= 2 ? kind - 2 : 0, j = base >> 3;  // j <= 3 for a suit kind
+    const uint64_t v = (uint64_t)sword(bp, W_HMASK + 5 * s + j) | ((uint64_t)sword(bp, W_HMASK + 5 * s + j + 1) << 32);
+    const uint64_t x = v >> (4 * (base - 8 * j));
+    const uint32_t pm = (uint32_t)((x | (x >> 1) | (x >> 2) | (x >> 3)) & 0x11111ull);  // a bit per nibble
+    const int off = kind - base;  // kind's nibble in x
+    auto has = [&](int d) -> uint32_t { return (pm >> (4 * (off + d))) & 1u; };
+    uint32_t b = 0;
+    if (n <= 6) b |= has(1) & has(2);
+    if (n >= 1 && n <= 7) b |= (has(-1) & has(1)) << 1;
+    if (n >= 2) b |= (has(-2) & has(-1)) << 2;
+    return b;
   }
+  RS_HD bool can_chi(int s, int kind) const { return chi_bits(s, kind) != 0; }
   // engine.py:498-531
   RS_OL_CALL_Q bool begin_call_phase(int tile, int discarder, bool chankan) {
     const int kind = tile >> 2;
