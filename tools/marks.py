@@ -3,7 +3,7 @@ import os, sys, ctypes as C, torch
 os.environ['RINSHAN_LIB'] = 'build_variants/_rinshan_marks.so'
 sys.path.insert(0, '.')
 from paper_2605_20577_b200.env import BatchEnv, EnvConfig, alloc_observations, obs_struct
-n = 4096
+n = int(sys.argv[1]) if len(sys.argv) > 1 else 4096
 env = BatchEnv(n, EnvConfig(rule='no-red')).init(seed=0)
 env.rollout(50)
 marks = torch.zeros(200000 * 8, dtype=torch.int64, device='cuda')
