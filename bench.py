@@ -540,7 +540,15 @@ def ours_arm(args, rank, world, local_rank):
         if digests is not None:
             Path(args.digests_out).write_text(json.dumps(digests))
             line["digests_out"] = {"path": args.digests_out, "envs": len(digests), "steps": args.digest_steps}
-        print(json.dumps(line), flush=True)
+    # the other ranks wait while rank 0 prints its line (no log lines of
+    # theirs -- NCCL INFO goes to stdout -- can land inside it)
+    if world > 1:
+        D.barrier()
+    if rank == 0:
+        sys.stdout.flush()
+        os.write(1, (json.dumps(line, separators=(",", ":")) + "\n").encode())
+    if world > 1:
+        D.barrier()
     return 0
 
 
@@ -565,13 +573,14 @@ def rows_run(args, dev, rank, world, peak, peak_source, barrier):
         t = D.max_time(sum(ms), dev)
         D.reduce_stats(stats)
         S = int(env._L.rs_state_bytes(None))
-        traffic, extra = ncu_summary(rule, n)
+        traffic, _ = ncu_summary(rule, n)
         out.append({"rule": rule, "envs_per_gpu": n, "global_batch": n * world,
                     "value": int(stats[0].item()) / (t / 1000.0), "unit": UNIT,
                     "ms_per_step": t / args.row_steps, "steps": args.row_steps,
                     "games_completed": int(stats[1].item()),
-                    "roofline": roofline(S, n, (sum(ms) / args.row_steps) / 1000.0, peak, peak_source, traffic,
-                                         extra)})
+                    "roofline": {k: v for k, v in roofline(S, n, (sum(ms) / args.row_steps) / 1000.0, peak, peak_source,
+                                                           traffic).items()
+                                 if k in ("bound", "achieved", "peak", "unit", "frac", "traffic", "bytes_per_env_step")}})
         env.close()
         del env
         torch.cuda.empty_cache()
@@ -660,11 +669,10 @@ def e2e_run(args, env, dev, world, obs_to_host: bool):
     t = D.max_time(sum(s.elapsed_time(e) for s, e in zip(starts, ends)), dev)
     value = n * world * steps / (t / 1000.0)
     res = {"value": value, "unit": UNIT, "h2d_bytes_per_step": hs.bytes_h2d, "d2h_bytes_per_step": hs.bytes_d2h,
-           "api": "HostStepper.step (one-node CUDA graph: the fused step+autoreset+observe+policy kernel "
-                  "reads the actions from and writes the result block"
-                  + (" and the observations" if obs_to_host else "") + " to mapped pinned host memory; the host "
-                  "polls the kernel's completion word)",
            "steps": steps}
+    if not obs_to_host:
+        res["api"] = ("HostStepper.step: one CUDA-graph replay per step; the fused step+autoreset+observe+policy "
+                      "kernel reads the actions from and writes its results to pinned host memory")
     hs.close()
     return res
 

@@ -12,7 +12,11 @@
 #include <cuda_runtime.h>
 #define RS_HD __host__ __device__ inline
 #define RS_HOT __host__ __device__ __forceinline__
+#if defined(RS_ALL_INLINE)  // (measured alternative: -5 % at 4,096 envs, -18 % fused, -4 % at 1 M)
+#define RS_COLD __host__ __device__ inline
+#else
 #define RS_COLD __host__ __device__ __noinline__
+#endif
 #define RS_DEV_ONLY __device__
 #else
 #define RS_HD inline
