@@ -80,11 +80,21 @@ def parse(argv=None):
 
 # ------------------------------------------------------------ K=1 timing
 
-def timed_launches(env, stats, steps: int, warmup: int, steady_warm: int, dev, barrier=None):
+L2_BYTES = 126 << 20  # B200 L2
+
+
+def state_exceeds_l2(env) -> bool:
+    """the envs' device state alone is larger than L2 (the timing rules'
+    alternative to flushing L2 between timed launches)"""
+    return env.n * int(env._L.rs_state_bytes(None)) > 4 * L2_BYTES
+
+
+def timed_launches(env, stats, steps: int, warmup: int, steady_warm: int, dev, barrier=None, flush_l2=True):
     """The bench step: one k_rollout launch of one env step per env (auto-
     reset, random policy, step, legal mask, observation of the current
     player into a device buffer), CUDA events on the launching stream around
-    each launch, a 256 MiB write between launches flushing L2 (untimed).
+    each launch, a 256 MiB write between launches flushing L2 (untimed;
+    `flush_l2` False when the state itself is several times the L2).
     Returns the per-launch device times (ms)."""
     import ctypes as C
 
@@ -124,7 +134,8 @@ def timed_launches(env, stats, steps: int, warmup: int, steady_warm: int, dev, b
         barrier()
     torch.cuda.synchronize()
     for i in range(steps):
-        flush.fill_(i & 255)
+        if flush_l2:
+            flush.fill_(i & 255)
         starts[i].record(stream)
         launch()
         ends[i].record(stream)
@@ -189,9 +200,11 @@ def sweep(args):
             launch()
         reps = max(3, min(args.steps, int(2e7 // (n * k)) + 1))
         ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(reps)]
+        big = state_exceeds_l2(env)
         torch.cuda.synchronize()
         for i in range(reps):
-            flush.fill_(i & 255)
+            if not big:
+                flush.fill_(i & 255)
             ev[i][0].record(stream)
             launch()
             ev[i][1].record(stream)
@@ -201,7 +214,7 @@ def sweep(args):
         S = int(env._L.rs_state_bytes(None))
         gbs = (2 * S + 272) * n * k / (ms / reps / 1000) / 1e9
         print(json.dumps({"sweep": True, "rule": args.rule, "envs": n, "fuse": k, "warm_steps": args.sweep_warm,
-                          "launches": reps,
+                          "launches": reps, "l2_flush": not big,
                           "ms_per_launch": ms / reps, "env_steps_per_s": sps, "hbm_gbs_algorithmic": gbs}),
               flush=True)
         env.close()
@@ -569,12 +582,15 @@ def rows_run(args, dev, rank, world, peak, peak_source, barrier):
         env = BatchEnv(n, EnvConfig(rule=rule, mode=args.mode), device=dev).init(seed=args.seed,
                                                                                   index_base=rank * n)
         stats = torch.zeros(3, dtype=torch.int64, device=dev)
-        ms = timed_launches(env, stats, args.row_steps, 3, args.steady_warm, dev, barrier)
+        big = state_exceeds_l2(env)
+        ms = timed_launches(env, stats, args.row_steps, 3, args.steady_warm, dev, barrier, flush_l2=not big)
         t = D.max_time(sum(ms), dev)
         D.reduce_stats(stats)
         S = int(env._L.rs_state_bytes(None))
         traffic, _ = ncu_summary(rule, n)
         out.append({"rule": rule, "envs_per_gpu": n, "global_batch": n * world,
+                    "l2": "state larger than L2 (%.1f GB), no flush" % (n * S / 1e9) if big
+                          else "flushed between timed steps",
                     "value": int(stats[0].item()) / (t / 1000.0), "unit": UNIT,
                     "ms_per_step": t / args.row_steps, "steps": args.row_steps,
                     "games_completed": int(stats[1].item()),
