@@ -19,6 +19,7 @@ from __future__ import annotations
 
 import argparse
 import json
+import os
 import sys
 import time
 from pathlib import Path
@@ -90,7 +91,8 @@ def main():
     p.add_argument("--no-graph", dest="graph", action="store_false",
                    help="run the rollout eagerly instead of replaying it as one CUDA graph")
     args = p.parse_args()
-    print(json.dumps(run(args)))
+    # one write per line: ranks share stdout under torchrun
+    os.write(1, (json.dumps(run(args)) + "\n").encode())
 
 
 def run(args) -> dict:

@@ -78,31 +78,41 @@ struct Mask115 {
   }
 };
 
-// engine.py:100-102 event, written into the env's 64-slot ring as one word:
-// bits 0-14 the event (type | (actor + 1) << 4 | (tile + 1) << 7), bits
-// 16-19 its observation type token (ron / tsumo share token 8) and bits
-// 20-25 its visible tile token (observe.py:92-106: red fives 34-36, none
-// 37) -- everything observe() needs except the observer, so one store per
-// event (round 1 also kept the event pre-encoded for each of the four
-// observers: four more scattered sector writes per event, 1 KB per env)
+// engine.py:100-102 event, written into the env's 64-slot ring as one word
+// laid out for observe() (observe.py:92-106), which decodes four slots at a
+// time with byte permutes (rs_io.cuh view4):
+//   byte 0: observation type token (ron / tsumo share 8) | bit 4 + s: the
+//           tile is hidden from observer s (an opponent's draw)
+//   byte 1: bits 2s..2s+1: the actor relative to observer s (0 without one)
+//   byte 2: visible tile token (red fives 34-36, none 37) | bit 6: has an actor
+//   byte 3: tile copy (tile & 3) | bit 2: has a tile | bits 3-6: event type
+// -- the event itself (type, actor, tile) stays recoverable (event_raw) for
+// export, import and the digest.  One store per event (round 1 also kept
+// the event pre-encoded for each of the four observers: four more
+// scattered sector writes per event, 1 KB per env).
 RS_HD uint32_t event_word(int rule, int type, int actor, int tile) {
   const uint32_t ty = (uint32_t)(type <= 8 ? type : type - 1);
   const uint32_t tok = tile < 0 ? 37u
                        : (rule == RS_RULE_RED && is_red_tile(tile)) ? (uint32_t)(34 + red_index_of_kind(tile >> 2))
                                                                     : (uint32_t)(tile >> 2);
-  return (uint32_t)(type | ((actor + 1) << 4) | ((tile + 1) << 7)) | (ty << 16) | (tok << 20);
-}
-// the event as observer `seat` sees it (observe.py:92-106): type token,
-// relative actor, visible tile token (opponents' draws hidden) in bytes 0-2
-RS_HD uint32_t event_view(uint32_t x, int seat) {
-  const uint32_t a1 = (x >> 4) & 7u;  // actor + 1, 0 for none
-  const uint32_t rel = a1 ? (a1 + 3u - (uint32_t)seat) & 3u : 0u;
-  const bool hidden = (x & 15u) == (uint32_t)EV_DRAW && a1 != (uint32_t)seat + 1u;
-  const uint32_t tok = hidden ? 37u : (x >> 20) & 63u;
-  return ((x >> 16) & 15u) | (rel << 8) | (tok << 16);
+  uint32_t hid = 0, rel = 0;
+  if (actor >= 0) {
+    if (type == EV_DRAW) hid = 0xFu & ~(1u << actor);
+    for (int o = 0; o < 4; o++) rel |= (uint32_t)((actor - o) & 3) << (2 * o);
+  }
+  return ty | (hid << 4) | (rel << 8) | (tok << 16) | ((actor >= 0 ? 1u : 0u) << 22) |
+         ((uint32_t)(tile >= 0 ? tile & 3 : 0) << 24) | ((tile >= 0 ? 1u : 0u) << 26) | ((uint32_t)type << 27);
 }
 // the canonical event (type | (actor + 1) << 4 | (tile + 1) << 7)
-RS_HD uint32_t event_raw(uint32_t x) { return x & 0x7FFFu; }
+RS_HD uint32_t event_raw(uint32_t x) {
+  const uint32_t type = (x >> 27) & 15u;
+  const uint32_t a1 = ((x >> 22) & 1u) ? ((x >> 8) & 3u) + 1u : 0u;
+  const uint32_t tok = (x >> 16) & 63u;
+  const int tile = ((x >> 26) & 1u) ? (tok >= 34 ? 16 + 36 * (int)(tok - 34) : (int)(4 * tok + ((x >> 24) & 3u))) : -1;
+  return type | (a1 << 4) | ((uint32_t)(tile + 1) << 7);
+}
+// a window pad slot: (0, 0, 37) for every observer
+constexpr uint32_t EVENT_PAD = 37u << 16;
 // out of line, called with scalars (19 emit sites; DESIGN §4 item 25)
 RS_COLD void emit_event(uint32_t* ring, uint32_t p, int rule, int type, int actor, int tile) {
   ring[p] = event_word(rule, type, actor, tile);

@@ -13,6 +13,27 @@ RS_HD int tile_token(int t, int rule) {
 }
 RS_HD int ev_token(int type) { return type <= 8 ? type : type - 1; }  // win events merge (observe.py:26-39)
 
+// four window slots (event words, rs_engine.cuh event_word) as observer
+// `seat` sees them, packed as write_obs emits them: 4 x (type token,
+// relative actor, visible tile token) in 3 words.  Byte-parallel: the
+// slots' bytes are gathered into one word per field and decoded four at a
+// time (~5.5 instructions per slot instead of ~12).
+RS_HD void view4(uint32_t x0, uint32_t x1, uint32_t x2, uint32_t x3, int seat, uint32_t& w0, uint32_t& w1,
+                 uint32_t& w2) {
+  const uint32_t p = byte_perm(x0, x1, 0x5140), q = byte_perm(x2, x3, 0x5140);
+  const uint32_t b0 = byte_perm(p, q, 0x5410), b1 = byte_perm(p, q, 0x7632);
+  const uint32_t b2 = byte_perm(byte_perm(x0, x1, 0x7362), byte_perm(x2, x3, 0x7362), 0x5410);
+  const uint32_t ty = b0 & 0x0F0F0F0Fu;
+  const uint32_t hid = (b0 >> (4 + seat)) & 0x01010101u;
+  const uint32_t rel = (b1 >> (2 * seat)) & 0x03030303u;
+  const uint32_t m = hid * 0xFFu;  // 0x00 / 0xFF per byte
+  const uint32_t tok = ((b2 & 0x3F3F3F3Fu) & ~m) | (0x25252525u & m);  // hidden: 37
+  const uint32_t yr = byte_perm(ty, rel, 0x5140), yr2 = byte_perm(ty, rel, 0x7362);
+  w0 = byte_perm(yr, tok, 0x2410);                          // y0 r0 t0 y1
+  w1 = byte_perm(byte_perm(yr, tok, 0x0053), yr2, 0x5410);  // r1 t1 y2 r2
+  w2 = byte_perm(tok, yr2, 0x3762);                         // t2 y3 r3 t3
+}
+
 // observe(state, seat) (observe.py:81-124), written into slot `o` of `obs`
 RS_HD void write_obs(const Engine& E, int seat, const rs_obs_out& obs, int64_t o) {
   RS_ACC(4);
@@ -37,9 +58,9 @@ RS_HD void write_obs(const Engine& E, int seat, const rs_obs_out& obs, int64_t o
   }
   if (obs.event_tokens) {
     // 64 x (type, rel actor, token), oldest first, padded (0,0,37): slot i
-    // of the window is ring entry (len + i) & 63 seen by this observer
-    // (event_view), pads while i < 64 - len; pack 4 triples into 3 words
-    // with byte permutes
+    // of the window is ring entry (len + i) & 63 seen by this observer,
+    // pads while i < 64 - len; 4 slots decode and pack into 3 words at a
+    // time (view4)
     const uint32_t* ring = S.events + (uint32_t)E.e * RS_EVENT_WINDOW;
     const uint32_t len = g.events_len;
     const int pad = len >= 64u ? 0 : 64 - (int)len;
@@ -50,48 +71,41 @@ RS_HD void write_obs(const Engine& E, int seat, const rs_obs_out& obs, int64_t o
     // each -- the same instructions on different data, so the warp runs
     // the quarter body once
     const int G = grp_size(), sub = grp_sub();
+    // slot i: ring entry (len + i) & 63, or a pad while i < pad (also right
+    // when len < 64: (len + i) & 63 = i - pad)
+    auto ev = [&](int i) -> uint32_t { return i < pad ? EVENT_PAD : ring[(len + (uint32_t)i) & 63u]; };
     if (G >= 8 && RS_WIN16) {
       // 8+ lanes per env: lane `sub` encodes slots [per * sub, per * (sub + 1))
-      // (per = 4 at 16+ lanes, 8 at 8): independent loads, 3 words per 4
-      // slots, stored as u32 -- the group's stores form one 192-byte burst
+      // (per = 4 at 16+ lanes, 8 at 8), stored as u32 -- the group's stores
+      // form one 192-byte burst
       const int L = G >= 16 ? 16 : 8, per = 64 / L;
       if (sub < L) {
         uint32_t* d32 = reinterpret_cast<uint32_t*>(obs.event_tokens + o * 192) + sub * (3 * per / 4);
         for (int c = 0; c < per; c += 4) {
           const int i0 = per * sub + c;
-          uint32_t v[4];
-#pragma unroll
-          for (int j = 0; j < 4; j++)
-            v[j] = i0 + j < pad ? EVOBS_PAD : event_view(ring[(len + (uint32_t)(i0 + j)) & 63u], seat);
-          d32[3 * c / 4] = byte_perm(v[0], v[1], 0x4210);
-          d32[3 * c / 4 + 1] = byte_perm(v[1], v[2], 0x5421);
-          d32[3 * c / 4 + 2] = byte_perm(v[2], v[3], 0x6542);
+          uint32_t w0, w1, w2;
+          view4(ev(i0), ev(i0 + 1), ev(i0 + 2), ev(i0 + 3), seat, w0, w1, w2);
+          d32[3 * c / 4] = w0;
+          d32[3 * c / 4 + 1] = w1;
+          d32[3 * c / 4 + 2] = w2;
         }
       }
     } else {
-    auto emit_window = [&](auto slot) {
+      // four quarters of 16 slots, each loaded completely before its stores
+      // (stores to the output could alias the ring as far as the compiler
+      // knows); with 2 or 4 lanes, lane `sub` takes quarters sub, sub + G
       for (int q = sub; q < 4; q += G) {
         uint32_t v[16];
 #pragma unroll
-        for (int j = 0; j < 16; j++) v[j] = slot(16 * q + j);
+        for (int j = 0; j < 16; j++) v[j] = ev(16 * q + j);
         uint32_t w[12];
 #pragma unroll
-        for (int r = 0; r < 4; r++) {
-          const int i0 = 4 * r;
-          w[3 * r] = byte_perm(v[i0], v[i0 + 1], 0x4210);
-          w[3 * r + 1] = byte_perm(v[i0 + 1], v[i0 + 2], 0x5421);
-          w[3 * r + 2] = byte_perm(v[i0 + 2], v[i0 + 3], 0x6542);
-        }
+        for (int r = 0; r < 4; r++) view4(v[4 * r], v[4 * r + 1], v[4 * r + 2], v[4 * r + 3], seat, w[3 * r], w[3 * r + 1], w[3 * r + 2]);
         uint4* d = dst + 3 * q;
         d[0] = make_uint4(w[0], w[1], w[2], w[3]);
         d[1] = make_uint4(w[4], w[5], w[6], w[7]);
         d[2] = make_uint4(w[8], w[9], w[10], w[11]);
       }
-    };
-    if (pad == 0)  // a full window (every step after the first 64 events)
-      emit_window([&](int i) -> uint32_t { return event_view(ring[(len + (uint32_t)i) & 63u], seat); });
-    else
-      emit_window([&](int i) -> uint32_t { return i < pad ? EVOBS_PAD : event_view(ring[i - pad], seat); });
     }
   }
   if (obs.shanten) obs.shanten[o] = (int8_t)hi::shanten(h.info);

@@ -35,7 +35,6 @@ constexpr int ENV_SCRATCH = 288;  // 148 + 136, 16-byte multiple
 RS_HD constexpr int scratch_bytes(int block, int glog2) {
   return glog2 == 0 ? block * SCRATCH_STRIDE : (block >> glog2) * ENV_SCRATCH;
 }
-constexpr uint32_t EVOBS_PAD = 37u << 16;  // an observation window pad slot (0, 0, 37)
 
 // ------------------------------------------------ the env block (HBM)
 // 132 words then the 144-byte wall; in shared memory each env's slot adds

@@ -113,7 +113,11 @@ def test_ppo_two_ranks_on_one_gpu_gloo():
            "--horizon", "16", "--iters", "2", "--epochs", "1", "--minibatch", "1024", "--dist-backend", "gloo"]
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT, env=dict(os.environ, OMP_NUM_THREADS="1"))
     assert r.returncode == 0, r.stderr[-3000:]
-    outs = [json.loads(ln) for ln in r.stdout.splitlines() if ln.startswith("{")]
+    dec, outs, i = json.JSONDecoder(), [], r.stdout.find("{")
+    while i >= 0:  # every JSON object in the output, however the ranks' lines interleave
+        obj, end = dec.raw_decode(r.stdout, i)
+        outs.append(obj)
+        i = r.stdout.find("{", end)
     assert len(outs) == 2 and {o["rank"] for o in outs} == {0, 1}
     for o in outs:
         assert o["world"] == 2 and o["env_steps_all_ranks"] == 2 * 2 * 128 * 16
