@@ -62,19 +62,30 @@ struct Mask115 {
     return (w >> (a & 31)) & 1u;
   }
   RS_HD int count() const { return popc32(m[0]) + popc32(m[1]) + popc32(m[2]) + popc32(m[3]); }
-  // the i-th set bit (ascending ids, engine.py:258)
+  // the i-th set bit (ascending ids, engine.py:258); -1 when i >= count().
+  // Branch-free (the 32 envs of a warp have different masks and ranks at
+  // large batches): the word by prefix counts, then a binary search over
+  // half / byte / nibble / pair popcounts (__fns is emulated in software on
+  // sm_100)
   RS_HD int nth(int i) const {
-    for (int w = 0; w < 4; w++) {
-      uint32_t x = w == 0 ? m[0] : w == 1 ? m[1] : w == 2 ? m[2] : m[3];
-      const int c = popc32(x);
-      if (i < c) {
-        // (a loop: __fns is emulated in software on sm_100 and costs more)
-        for (int j = 0; j < i; j++) x &= x - 1;
-        return 32 * w + ctz32(x);
-      }
-      i -= c;
+    const int c0 = popc32(m[0]), c1 = popc32(m[1]), c2 = popc32(m[2]);
+    int w = 0;
+    uint32_t x = m[0];
+    if (i >= c0) { i -= c0; w = 1; x = m[1]; }
+    if (w == 1 && i >= c1) { i -= c1; w = 2; x = m[2]; }
+    if (w == 2 && i >= c2) { i -= c2; w = 3; x = m[3]; }
+    if (i >= popc32(x)) return -1;
+    int pos = 0;
+#pragma unroll
+    for (int half = 16; half >= 1; half >>= 1) {
+      const uint32_t lo = x & ((1u << half) - 1u);
+      const int c = popc32(lo);
+      const bool up = i >= c;
+      i -= up ? c : 0;
+      x = up ? x >> half : lo;
+      pos += up ? half : 0;
     }
-    return -1;
+    return 32 * w + pos;
   }
 };
 
@@ -782,12 +793,12 @@ struct Engine {
     const uint64_t x = v >> (4 * (base - 8 * j));
     const uint32_t pm = (uint32_t)((x | (x >> 1) | (x >> 2) | (x >> 3)) & 0x11111ull);  // a bit per nibble
     const int off = kind - base;  // kind's nibble in x
-    auto has = [&](int d) -> uint32_t { return (pm >> (4 * (off + d))) & 1u; };
-    uint32_t b = 0;
-    if (n <= 6) b |= has(1) & has(2);
-    if (n >= 1 && n <= 7) b |= (has(-1) & has(1)) << 1;
-    if (n >= 2) b |= (has(-2) & has(-1)) << 2;
-    return b;
+    // (branch-free: a shift below the window reads bit 0 and is masked off)
+    auto has = [&](int d) -> uint32_t { return (pm >> (4 * (off + d > 0 ? off + d : 0))) & 1u; };
+    const uint32_t lo = (uint32_t)(n <= 6) & has(1) & has(2);
+    const uint32_t mid = (uint32_t)(n >= 1 && n <= 7) & has(-1) & has(1);
+    const uint32_t hi = (uint32_t)(n >= 2) & has(-2) & has(-1);
+    return lo | (mid << 1) | (hi << 2);
   }
   RS_HD bool can_chi(int s, int kind) const { return chi_bits(s, kind) != 0; }
   // engine.py:498-531

@@ -21,15 +21,21 @@ struct Hand {
   uint64_t waits;
   uint64_t tlo, thi;            // sorted observation tokens, 16 bytes, pad 37
 
+  // dynamic word / code index as selects (no branches: the 32 envs of a
+  // warp index different words at large batches)
   RS_HD uint32_t word(int i) const {
-    return i == 0 ? w0 : i == 1 ? w1 : i == 2 ? w2 : i == 3 ? w3 : w4;
+    uint32_t x = w4;
+    x = i == 3 ? w3 : x;
+    x = i == 2 ? w2 : x;
+    x = i == 1 ? w1 : x;
+    return i == 0 ? w0 : x;
   }
   RS_HD void set_word(int i, uint32_t v) {
-    if (i == 0) w0 = v;
-    else if (i == 1) w1 = v;
-    else if (i == 2) w2 = v;
-    else if (i == 3) w3 = v;
-    else w4 = v;
+    w0 = i == 0 ? v : w0;
+    w1 = i == 1 ? v : w1;
+    w2 = i == 2 ? v : w2;
+    w3 = i == 3 ? v : w3;
+    w4 = i >= 4 ? v : w4;
   }
   RS_HD bool has(int t) const { return (word(t >> 5) >> (t & 31)) & 1u; }
   RS_HD uint32_t nibble(int k) const { return (word(k >> 3) >> ((k & 7) * 4)) & 0xFu; }
@@ -37,11 +43,12 @@ struct Hand {
   RS_HD int lowest_of_kind(int k) const { return 4 * k + ctz32(nibble(k)); }
   RS_HD uint32_t code(int s) const { return s == 0 ? cm : s == 1 ? cp : s == 2 ? cs : cz; }
   RS_HD void set_code(int s, uint32_t v) {
-    if (s == 0) cm = v;
-    else if (s == 1) cp = v;
-    else if (s == 2) cs = v;
-    else cz = v;
+    cm = s == 0 ? v : cm;
+    cp = s == 1 ? v : cp;
+    cs = s == 2 ? v : cs;
+    cz = s >= 3 ? v : cz;
   }
+
   // 34-bit mask of kinds with count >= t
   RS_HD uint64_t kinds_ge(int t) const {
     return (uint64_t)nib_ge(nib_counts(w0), t) | ((uint64_t)nib_ge(nib_counts(w1), t) << 8) |
