@@ -96,28 +96,28 @@ RS_HD int tok_rank(uint64_t lo, uint64_t hi, uint32_t v) {  // bytes < v
   const uint64_t H = 0x8080808080808080ull, vv = 0x0101010101010101ull * v;
   return 16 - popc64(((lo | H) - vv) & H) - popc64(((hi | H) - vv) & H);
 }
-RS_HD uint64_t low_bytes(int p) { return p <= 0 ? 0ull : (p >= 8 ? ~0ull : (~0ull >> (64 - 8 * p))); }
+// the low p bytes (0 <= p <= 8) of a 64-bit word
+RS_HD uint64_t low_bytes(int p) { return p >= 8 ? ~0ull : ((1ull << (8 * (p & 7))) - 1ull); }
+// insert / remove token v in the sorted 16-byte register (lo | hi << 64):
+// both halves' results are computed and selected, no branch (the envs of a
+// warp insert at different positions)
 RS_HD void tok_insert(uint64_t& lo, uint64_t& hi, uint32_t v) {
   const int p = tok_rank(lo, hi, v);
-  if (p < 8) {
-    const uint64_t m = low_bytes(p), carry = lo >> 56;
-    lo = (lo & m) | ((uint64_t)v << (8 * p)) | ((lo & ~m) << 8);
-    hi = (hi << 8) | carry;
-  } else {
-    const uint64_t m = low_bytes(p - 8);
-    hi = (hi & m) | ((uint64_t)v << (8 * (p - 8))) | ((hi & ~m) << 8);
-  }
+  const bool low = p < 8;
+  const int q = low ? p : p - 8;
+  const uint64_t m = low_bytes(q), x = low ? lo : hi;
+  const uint64_t ins = (x & m) | ((uint64_t)v << (8 * q)) | ((x & ~m) << 8);
+  hi = low ? (hi << 8) | (lo >> 56) : ins;
+  lo = low ? ins : lo;
 }
 RS_HD void tok_remove(uint64_t& lo, uint64_t& hi, uint32_t v) {  // v present
   const int p = tok_rank(lo, hi, v);
-  if (p < 8) {
-    const uint64_t m = low_bytes(p);
-    lo = (lo & m) | ((lo >> 8) & ~m) | (hi << 56);
-    hi = (hi >> 8) | (0x25ull << 56);
-  } else {
-    const uint64_t m = low_bytes(p - 8);
-    hi = (hi & m) | ((hi >> 8) & ~m) | (0x25ull << 56);
-  }
+  const bool low = p < 8;
+  const int q = low ? p : p - 8;
+  const uint64_t m = low_bytes(q), x = low ? lo : hi;
+  const uint64_t rem = (x & m) | ((x >> 8) & ~m);
+  lo = low ? rem | (hi << 56) : lo;
+  hi = low ? (hi >> 8) | (0x25ull << 56) : rem | (0x25ull << 56);
 }
 RS_HD uint32_t token_of(int t, bool red) {
   return (red && is_red_tile(t)) ? (uint32_t)(34 + red_index_of_kind(t >> 2)) : (uint32_t)(t >> 2);
@@ -265,14 +265,15 @@ RS_HD void special_shanten(const Hand& h, int& seven, int& kokushi) {
 }
 // shanten_codes (shanten.py:172-182)
 RS_HD int full_shanten_impl(const Tabs& T, const Hand& h, int melds) {
-  int s = std_shanten_cls(T, h.cls, melds);
-  if (melds == 0 && s > -1) {
-    int sp, kk;
-    special_shanten(h, sp, kk);
-    if (sp < s) s = sp;
-    if (s > -1 && kk < s) s = kk;
-  }
-  return s;
+  const int s = std_shanten_cls(T, h.cls, melds);
+  // seven pairs / thirteen orphans count only for closed hands that are not
+  // complete (shanten.py:172-182); evaluated unconditionally and selected
+  // (the envs of a warp differ in melds, and most need it)
+  int sp, kk;
+  special_shanten(h, sp, kk);
+  const int a = sp < s ? sp : s;
+  const int b = (a > -1 && kk < a) ? kk : a;
+  return (melds == 0 && s > -1) ? b : s;
 }
 // one out-of-line copy shared by every call site: the engine inlines its
 // hand updates in many places, and eight inlined copies of the shanten
