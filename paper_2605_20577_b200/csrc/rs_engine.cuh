@@ -741,11 +741,12 @@ struct Engine {
   // ------------------------------------------------------ call handling
   // engine.py:580-591
   RS_HD void mark_passed_furiten(int kind, int discarder) {
+#pragma unroll
     for (int s = 0; s < 4; s++) {
-      if (s == discarder) continue;
       const uint32_t inf = info(s);
-      if (hi::shanten(inf) == 0 && ((waits(s) >> kind) & 1))
-        set_info(s, hi::riichi(inf) ? hi::set_perm(inf, 1) : hi::set_temp(inf, 1));
+      // (the waits load for every seat: no branch on the shanten)
+      const bool hit = s != discarder && hi::shanten(inf) == 0 && ((waits(s) >> kind) & 1);
+      if (hit) set_info(s, hi::riichi(inf) ? hi::set_perm(inf, 1) : hi::set_temp(inf, 1));
     }
   }
   // engine.py:594-615
@@ -856,10 +857,12 @@ struct Engine {
     const int kind = action < 34 ? action : (action == 34 ? 4 : action == 35 ? 13 : 22);
     const bool want_red = action >= 34;
     const bool red_rule = C.rule == RS_RULE_RED;
-    if (g.drawn >= 0 && (g.drawn >> 2) == kind && (red_rule && is_red_tile(g.drawn)) == want_red) return g.drawn;
+    // both candidates computed and selected (no branch)
+    const bool drawn_ok = g.drawn >= 0 && (g.drawn >> 2) == kind && (red_rule && is_red_tile(g.drawn)) == want_red;
     uint32_t nib = h.nibble(kind);
-    if (red_rule && red_index_of_kind(kind) >= 0) nib = want_red ? (nib & 1u) : (nib & ~1u);
-    return 4 * kind + ctz32(nib);
+    const uint32_t keep = want_red ? 1u : ~1u;
+    nib = (red_rule && red_index_of_kind(kind) >= 0) ? (nib & keep) : nib;
+    return drawn_ok ? g.drawn : 4 * kind + ctz32(nib);
   }
   // engine.py:458-486
   RS_HD void apply_discard(int seat, int action) {
