@@ -50,15 +50,21 @@ enum : int { M_CHI = 0, M_PON = 1, M_KAN_OPEN = 2, M_KAN_CLOSED = 3, M_KAN_ADDED
 struct Mask115 {
   uint32_t m[4];
   RS_HD void clear() { m[0] = m[1] = m[2] = m[3] = 0; }
+  // dynamic word index as selects (no branches)
   RS_HD void set(int a) {
     const uint32_t b = 1u << (a & 31);
-    if ((a >> 5) == 0) m[0] |= b;
-    else if ((a >> 5) == 1) m[1] |= b;
-    else if ((a >> 5) == 2) m[2] |= b;
-    else m[3] |= b;
+    const int w = a >> 5;
+    m[0] |= w == 0 ? b : 0u;
+    m[1] |= w == 1 ? b : 0u;
+    m[2] |= w == 2 ? b : 0u;
+    m[3] |= w >= 3 ? b : 0u;
   }
   RS_HD bool test(int a) const {
-    const uint32_t w = (a >> 5) == 0 ? m[0] : (a >> 5) == 1 ? m[1] : (a >> 5) == 2 ? m[2] : m[3];
+    const int i = a >> 5;
+    uint32_t w = m[3];
+    w = i == 2 ? m[2] : w;
+    w = i == 1 ? m[1] : w;
+    w = i == 0 ? m[0] : w;
     return (w >> (a & 31)) & 1u;
   }
   RS_HD int count() const { return popc32(m[0]) + popc32(m[1]) + popc32(m[2]) + popc32(m[3]); }

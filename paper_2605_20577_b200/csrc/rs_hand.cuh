@@ -41,7 +41,12 @@ struct Hand {
   RS_HD uint32_t nibble(int k) const { return (word(k >> 3) >> ((k & 7) * 4)) & 0xFu; }
   RS_HD int count(int k) const { return popc32(nibble(k)); }
   RS_HD int lowest_of_kind(int k) const { return 4 * k + ctz32(nibble(k)); }
-  RS_HD uint32_t code(int s) const { return s == 0 ? cm : s == 1 ? cp : s == 2 ? cs : cz; }
+  RS_HD uint32_t code(int s) const {
+    uint32_t x = cz;
+    x = s == 2 ? cs : x;
+    x = s == 1 ? cp : x;
+    return s == 0 ? cm : x;
+  }
   RS_HD void set_code(int s, uint32_t v) {
     cm = s == 0 ? v : cm;
     cp = s == 1 ? v : cp;
