@@ -295,5 +295,13 @@ RS_HD uint32_t kind_pow_calc(int k) {
   return k < 27 ? pow5(8 - k % 9) : pow5(6 - (k - 27));
 }
 RS_HD int kind_suit(int k) { return k < 27 ? k / 9 : 3; }
+// 5^d for d in 0..8 from the bits of d: selects and two multiplies, no
+// memory (the per-kind table was a dependent load in every hand update)
+RS_HD uint32_t pow5_bits(int d) {
+  uint32_t p = (d & 1) ? 5u : 1u;
+  p *= (d & 2) ? 25u : 1u;
+  p *= (d & 4) ? 625u : 1u;
+  return (d & 8) ? 390625u : p;  // d == 8
+}
 
 }  // namespace rs

@@ -251,6 +251,58 @@ struct Engine {
   }
 
   // ------------------------------------------------------ rng / dealing
+  // deal 4-4-4 then 1 from the dealer (engine.py:142-151): the seat at
+  // offset i = (s - dealer) & 3 receives wall positions 16r + 4i .. +3 and
+  // 48 + i (its 4-tile blocks are aligned words of the shuffled wall)
+  RS_HD Hand dealt_hand(const uint8_t* w, int i) const {
+    Hand h;
+    h.w0 = h.w1 = h.w2 = h.w3 = h.w4 = 0;
+    h.cm = h.cp = h.cs = h.cz = 0;
+    const uint32_t* w32 = reinterpret_cast<const uint32_t*>(w);
+#pragma unroll
+    for (int r = 0; r < 3; r++) {
+      const uint32_t q = w32[4 * r + i];
+#pragma unroll
+      for (int j = 0; j < 4; j++) deal_tile(h, (int)((q >> (8 * j)) & 255u));
+    }
+    deal_tile(h, w[48 + i]);
+    h.cls = class_of(T, 0, h.cm) | (class_of(T, 1, h.cp) << 8) | (class_of(T, 2, h.cs) << 16) |
+            (class_of(T, 3, h.cz) << 24);
+    tokens_from_set(h, C.rule == RS_RULE_RED);
+    h.info = hi::set_nconc(hi::set_riichi_index(0u, -1), 13);
+    return h;
+  }
+#if defined(__CUDA_ARCH__)
+  // lane group of 4+: lane sub builds seat sub & 3 (the four deals' table
+  // lookups in parallel instead of one seat after the other); the waits of
+  // a 13-tile tenpai deal (rare) are then scanned by the whole group
+  RS_HD void deal_group(const uint8_t* w, int dealer) {
+    const int sub = grp_sub();
+    const uint32_t gm = grp_mask();
+    const int s = sub & 3;
+    Hand h = dealt_hand(w, (s - dealer) & 3);
+    RS_MARK(6);
+    const int sh = full_shanten(T, h, 0);
+    h.info = hi::set_shanten(h.info, sh);
+    h.waits = 0ull;
+    if (sub < 4) {
+      store_hand(bp, s, h);
+      sdword(bp, W_HRKIND + 2 * s) = 0ull;
+    }
+    RS_MARK(7);
+    uint32_t tenpai = __ballot_sync(gm, sub < 4 && sh == 0);
+    tenpai = (tenpai >> ((threadIdx.x & 31) - sub)) & 15u;
+    __syncwarp(gm);
+    while (tenpai) {
+      const int t = __ffs(tenpai) - 1;
+      tenpai &= tenpai - 1;
+      const uint64_t wv = compute_waits(T, load_hand(bp, t), 0);
+      if (sub == 0) sdword(bp, W_HWAITS + 2 * t) = wv;
+      __syncwarp(gm);
+    }
+  }
+#endif
+
   // engine.py:139-164 (_start_kyoku) with tiles.py:142-144 / rng.py:59-65
   RS_COLD void start_kyoku() {
     // the swap chain is a dependent load / store sequence: it runs in shared
@@ -279,6 +331,7 @@ struct Engine {
       for (int i = 135 - sub; i > 0; i -= G)
         J[i] = (uint8_t)randbelow_from(stream_value(g.rng_key, c + 1 + (uint64_t)(135 - i)), (uint32_t)(i + 1));
       __syncwarp(gm);
+      RS_MARK(0);
       if (sub == 0) {
         for (int i = 135; i > 0; i -= 5) {  // 135 = 27 x 5
           int j[5];
@@ -316,29 +369,18 @@ struct Engine {
     g.rng_counter = (uint32_t)c;
     RS_MARK(2);
     const int dealer = g.dealer();
-    // deal 4-4-4 then 1 from the dealer (engine.py:142-151): seat s at
-    // offset i = (s - dealer) & 3 receives positions 16r + 4i .. +3 and 48 + i
-    for (int s = 0; s < 4; s++) {
-      const int i = (s - dealer) & 3;
-      Hand h;
-      h.w0 = h.w1 = h.w2 = h.w3 = h.w4 = 0;
-      h.cm = h.cp = h.cs = h.cz = 0;
-      // the seat's 4-tile blocks are aligned words of the wall
-      const uint32_t* w32 = reinterpret_cast<const uint32_t*>(w);
-#pragma unroll
-      for (int r = 0; r < 3; r++) {
-        const uint32_t q = w32[4 * r + i];
-#pragma unroll
-        for (int j = 0; j < 4; j++) deal_tile(h, (int)((q >> (8 * j)) & 255u));
+#if defined(__CUDA_ARCH__)
+    if (G >= 4) {
+      deal_group(w, dealer);
+    } else
+#endif
+    {
+      for (int s = 0; s < 4; s++) {
+        Hand h = dealt_hand(w, (s - dealer) & 3);
+        finish_hand(T, h);
+        store_hand(bp, s, h);
+        sdword(bp, W_HRKIND + 2 * s) = 0ull;
       }
-      deal_tile(h, w[48 + i]);
-      h.cls = class_of(T, 0, h.cm) | (class_of(T, 1, h.cp) << 8) | (class_of(T, 2, h.cs) << 16) |
-              (class_of(T, 3, h.cz) << 24);
-      tokens_from_set(h, C.rule == RS_RULE_RED);
-      h.info = hi::set_nconc(hi::set_riichi_index(0u, -1), 13);
-      finish_hand(T, h);
-      store_hand(bp, s, h);
-      sdword(bp, W_HRKIND + 2 * s) = 0ull;
     }
     g.cursor = 52;
     g.kan_draws = 0;

@@ -155,7 +155,7 @@ RS_HD void tokens_from_set(Hand& h, bool red) {
   h.thi = hi;
 }
 
-RS_HD uint32_t kind_pow(int k);  // below (staged table on the device)
+RS_HD uint32_t kind_pow_table(int k);  // below (table on the device)
 
 // branchless accumulation of one dealt tile into the set and the suit codes
 RS_HD void deal_tile(Hand& h, int t) {
@@ -167,7 +167,7 @@ RS_HD void deal_tile(Hand& h, int t) {
   h.w3 |= wi == 3 ? bit : 0u;
   h.w4 |= wi == 4 ? bit : 0u;
   const int k = t >> 2, s = kind_suit(k);
-  const uint32_t p = kind_pow(k);
+  const uint32_t p = kind_pow_table(k);
   h.cm += s == 0 ? p : 0u;
   h.cp += s == 1 ? p : 0u;
   h.cs += s == 2 ? p : 0u;
@@ -218,8 +218,19 @@ RS_HD uint32_t t3_at(const Tabs& T, int i) {
 #endif
 }
 RS_HD int cls_byte(uint32_t cls, int s) { return (cls >> (8 * s)) & 255; }
-// base-5 code delta of one tile of kind k (staged table on the device)
+// base-5 code delta of one tile of kind k: computed in the hand updates of
+// the step (no dependent load); the deal's 13 independent lookups read the
+// table (fewer instructions in cold code: DESIGN §4 item 48)
 RS_HD uint32_t kind_pow(int k) {
+#if defined(__CUDA_ARCH__) && defined(RS_POW_TABLE)
+  return reinterpret_cast<const uint32_t*>(RS_TBL(POW_OFF))[k];
+#elif defined(__CUDA_ARCH__)
+  return pow5_bits(k < 27 ? 8 - (k - 9 * (k / 9)) : 33 - k);
+#else
+  return kind_pow_calc(k);
+#endif
+}
+RS_HD uint32_t kind_pow_table(int k) {
 #if defined(__CUDA_ARCH__)
   return reinterpret_cast<const uint32_t*>(RS_TBL(POW_OFF))[k];
 #else
