@@ -13,7 +13,8 @@
 namespace rs {
 
 // phase timestamps for build-time profiling experiments (-DRS_PROFILE_MARKS)
-// RS_PROFILE_MARKS=1: phases of init_game (RS_MARK); =2: phases of a step (RS_SMARK)
+// RS_PROFILE_MARKS=1: phases of init_game (RS_MARK); =2: phases of a step (RS_SMARK);
+// =4: phases of a win (RS_WMARK)
 #if defined(RS_PROFILE_MARKS) && defined(__CUDA_ARCH__)
 #define RS_MARK_AT(i)                                                                        \
   do {                                                                                       \
@@ -23,6 +24,11 @@ namespace rs {
 #define RS_MARK_AT(i) \
   do {                \
   } while (0)
+#endif
+#if defined(RS_PROFILE_MARKS) && RS_PROFILE_MARKS == 4
+#define RS_WMARK(i) RS_MARK_AT(i)
+#else
+#define RS_WMARK(i) do {} while (0)
 #endif
 #if defined(RS_PROFILE_MARKS) && RS_PROFILE_MARKS == 2
 #define RS_MARK(i) do {} while (0)
@@ -449,6 +455,9 @@ struct Engine {
       reds = (int)h.has(16) + (int)h.has(52) + (int)h.has(88);
       if (!tsumo && is_red_tile(win_tile)) reds++;
     }
+    // cold code: loops kept rolled (an instruction of a path run once per
+    // launch costs its fetch, DESIGN §4 item 49)
+    #pragma unroll 1
     for (int i = 0; i < 4; i++) {
       if (i < w.nmelds) {
         const uint32_t mf = meld_info(seat, i), mt = meld_tiles(seat, i);
@@ -456,6 +465,7 @@ struct Engine {
         w.mbase[i] = (mt & 255) >> 2;
         if (w.mtype[i] != M_KAN_CLOSED) w.closed = false;
         const int nt = mi::ntiles(mf);
+        #pragma unroll 1
         for (int j = 0; j < 4; j++)
           if (j < nt) {
             const int t = (mt >> (8 * j)) & 255;
@@ -723,11 +733,14 @@ struct Engine {
   }
   // engine.py:764-779
   RS_COLD void apply_tsumo(int seat) {
+    RS_WMARK(0);
     const Hand h = load_hand(bp, seat);
     WinIn w;
     win_input(seat, h, g.drawn, true, false, w);
+    RS_WMARK(1);
     Reading rd;
     score_win(w, rd, false);
+    RS_WMARK(2);
     begin_result(RS_RES_TSUMO);
     rs_result_rec& r = result();
     int deltas[4], hc;
@@ -743,10 +756,13 @@ struct Engine {
     emit(EV_TSUMO, seat, g.drawn);
     end_result();
     const int dealer = g.dealer();
+    RS_WMARK(3);
     advance_round(seat == dealer, seat != dealer);
+    RS_WMARK(4);
   }
   // engine.py:782-807
   RS_COLD void apply_ron_wins() {
+    RS_WMARK(0);
     const int loser = g.call_from;
     const int nw = g.rn();
     int w4[3];
@@ -768,8 +784,10 @@ struct Engine {
       const Hand h = load_hand(bp, seat);
       WinIn w;
       win_input(seat, h, g.call_tile, false, g.call_chankan, w);
+      RS_WMARK(1);
       Reading rd;
       score_win(w, rd, false);
+      RS_WMARK(2);
       const int honba = i == 0 ? g.honba : 0, dep = i == 0 ? g.deposits : 0;
       int deltas[4], hc;
       settle(false, rd.base, dealer, seat, loser, honba, dep, deltas, &hc);
@@ -783,7 +801,9 @@ struct Engine {
     g.deposits = 0;
     end_result();
     clear_call();
+    RS_WMARK(3);
     advance_round(dealer_won, !dealer_won);
+    RS_WMARK(4);
   }
 
   // ------------------------------------------------------ call handling

@@ -142,7 +142,7 @@ RS_HD void tokens_from_set(Hand& h, bool red) {
     if ((w[1] >> 20) & 1u) { push(35); w[1] &= ~(1u << 20); }  // tile 52
     if ((w[0] >> 16) & 1u) { push(34); w[0] &= ~(1u << 16); }  // tile 16
   }
-#pragma unroll
+#pragma unroll 1
   for (int i = 4; i >= 0; i--) {
     uint32_t x = w[i];
     while (x) {

@@ -120,6 +120,7 @@ RS_HD int chuuren(const WinIn& w) {
   const uint64_t present = w.conc.ge(1);
   if (present & HONOR_MASK) return 0;
   int suit = -1;
+  #pragma unroll 1
   for (int s = 0; s < 3; s++)
     if ((present >> (9 * s)) & 0x1FF) {
       if (suit >= 0) return 0;
@@ -127,6 +128,7 @@ RS_HD int chuuren(const WinIn& w) {
     }
   if (suit < 0) return 0;
   int extra = -1;
+  #pragma unroll 1
   for (int i = 0; i < 9; i++) {
     const int d = w.conc.get(9 * suit + i) - ((i == 0 || i == 8) ? 3 : 1);
     if (d == 0) continue;
@@ -145,6 +147,7 @@ struct Blocks {
 };
 RS_HD void make_blocks(const WinIn& w, const int* keys, int nsets, int wait_block, Blocks& b) {
   b.n = 0;
+  #pragma unroll 1
   for (int i = 0; i < nsets; i++) {
     const bool run = keys[i] < 64;
     b.start[b.n] = keys[i] & 63;
@@ -154,6 +157,7 @@ RS_HD void make_blocks(const WinIn& w, const int* keys, int nsets, int wait_bloc
     b.ronfill[b.n] = !w.tsumo && i == wait_block && !run;
     b.n++;
   }
+  #pragma unroll 1
   for (int i = 0; i < w.nmelds; i++) {
     b.start[b.n] = w.mbase[i];
     b.run[b.n] = w.mtype[i] == 0;
@@ -173,6 +177,7 @@ RS_HD void standard_reading(const WinIn& w, int pair, const int* keys, int nsets
   int concealed_trips = 0, kans = 0;
   bool all_trip = true, has_run = false, outside = is_orphan(pair);
   int fu_blocks = 0;
+  #pragma unroll 1
   for (int i = 0; i < b.n; i++) {
     const int s = b.start[i];
     if (b.run[i]) {
@@ -239,6 +244,7 @@ RS_HD void standard_reading(const WinIn& w, int pair, const int* keys, int nsets
     if ((trip >> w.round_wind) & 1) m |= 1ull << Y_ROUND;
     if (run_starts & (run_starts >> 9) & (run_starts >> 18) & 0x7Full) m |= 1ull << Y_SANSHOKU_DOUJUN;
     if (trip & (trip >> 9) & (trip >> 18) & 0x1FFull) m |= 1ull << Y_SANSHOKU_DOUKOU;
+    #pragma unroll 1
     for (int s = 0; s < 3; s++)
       if (((run_starts >> (9 * s)) & 0x49ull) == 0x49ull) { m |= 1ull << Y_ITTSU; break; }
     const bool has_honor = (present & HONOR_MASK) != 0;
@@ -367,10 +373,12 @@ RS_COLD bool score_win(const WinIn& w, Reading& best, bool first_only) {
     // lowest kind as a triplet (bit 0) or a run (bit 1)
     uint32_t decs[16];
     int nd = 0;
+    #pragma unroll 1
     for (int choice = 0; choice < (1 << needed); choice++) {
       Counts c = base;
       int keys[4];
       bool ok = true;
+      #pragma unroll 1
       for (int d = 0; d < needed && ok; d++) {
         const int i = c.lowest();
         if (i >= 34) { ok = false; break; }
@@ -386,20 +394,25 @@ RS_COLD bool score_win(const WinIn& w, Reading& best, bool first_only) {
       }
       if (!ok || !c.empty()) continue;
       // sorted(sets): insertion sort of <= 4 keys, packed 7 bits each
+      #pragma unroll 1
       for (int a = 1; a < needed; a++)
         for (int q = a; q > 0 && keys[q - 1] > keys[q]; q--) { int t = keys[q]; keys[q] = keys[q - 1]; keys[q - 1] = t; }
       uint32_t packed = 0;
+      #pragma unroll 1
       for (int d = 0; d < needed; d++) packed = (packed << 7) | (uint32_t)keys[d];
       // keep decs sorted ascending (results sorted by set tuple)
       int q = nd++;
       while (q > 0 && decs[q - 1] > packed) { decs[q] = decs[q - 1]; q--; }
       decs[q] = packed;
     }
+    #pragma unroll 1
     for (int di = 0; di < nd; di++) {
       int keys[4];
+      #pragma unroll 1
       for (int d = 0; d < needed; d++) keys[d] = (decs[di] >> (7 * (needed - 1 - d))) & 127;
       // wait_placements (yaku.py:158-174)
       const int k = w.win_kind;
+      #pragma unroll 1
       for (int i = 0; i <= needed; i++) {
         int blk, wait;
         if (i < needed) {
@@ -454,6 +467,7 @@ RS_HD void fill_win_rec(rs_win_rec& x, const Reading& rd, const WinIn& w) {
 // settle (points.py:56-86)
 RS_HD void settle(bool tsumo, int base, int dealer, int winner, int loser, int honba, int deposits,
                   int* deltas, int* honba_comp) {
+  #pragma unroll 1
   for (int s = 0; s < 4; s++) deltas[s] = 0;
   const bool dealer_win = winner == dealer;
   if (!tsumo) {
@@ -463,6 +477,7 @@ RS_HD void settle(bool tsumo, int base, int dealer, int winner, int loser, int h
     *honba_comp = 300 * honba;
   } else {
     *honba_comp = 0;
+    #pragma unroll 1
     for (int s = 0; s < 4; s++) {
       if (s == winner) continue;
       const int share = (dealer_win || s == dealer) ? 2 * base : base;

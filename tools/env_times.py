@@ -15,6 +15,7 @@ from paper_2605_20577_b200.env import BatchEnv, EnvConfig, alloc_observations, o
 
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 4096
 launches = int(sys.argv[2]) if len(sys.argv) > 2 else 100
+no_flush = len(sys.argv) > 3 and sys.argv[3] == 'noflush'
 env = BatchEnv(n, EnvConfig(rule='no-red')).init(seed=0)
 env.rollout(300)
 obs = alloc_observations(n, env.device)
@@ -37,7 +38,8 @@ def q(xs, f):
 qs = collections.defaultdict(list)
 cyc_by = collections.defaultdict(list)
 for it in range(launches):
-    flush.fill_(it & 255)
+    if not no_flush:
+        flush.fill_(it & 255)
     torch.cuda.synchronize()
     env._L.rs_debug_rollout_cycles(env._h, 1, C.byref(ost), prof.data_ptr(), torch.cuda.current_stream().cuda_stream)
     torch.cuda.synchronize()
@@ -55,7 +57,7 @@ for it in range(launches):
     rc = cyc[:, 0].tolist()
     for e in range(n):
         cyc_by[cls_of(a[e], rs[e])].append(sc[e] + rc[e])
-print("n=%d, %d launches; times in us from the first warp's entry (mean over launches)" % (n, launches))
+print("L2 %s; " % ("warm (no flush)" if no_flush else "flushed") + "n=%d, %d launches; times in us from the first warp's entry (mean over launches)" % (n, launches))
 for name in ("entry", "first step", "end"):
     print("  %-10s " % name + "  ".join("p%s %6.2f" % (int(f * 100), st.mean(qs[(name, f)]))
                                         for f in (0.5, 0.9, 0.99, 1.0)))
