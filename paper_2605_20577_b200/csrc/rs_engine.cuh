@@ -265,10 +265,10 @@ struct Engine {
     h.w0 = h.w1 = h.w2 = h.w3 = h.w4 = 0;
     h.cm = h.cp = h.cs = h.cz = 0;
     const uint32_t* w32 = reinterpret_cast<const uint32_t*>(w);
-#pragma unroll
+#pragma unroll 1
     for (int r = 0; r < 3; r++) {
       const uint32_t q = w32[4 * r + i];
-#pragma unroll
+#pragma unroll 1
       for (int j = 0; j < 4; j++) deal_tile(h, (int)((q >> (8 * j)) & 255u));
     }
     deal_tile(h, w[48 + i]);
@@ -647,7 +647,7 @@ struct Engine {
 
   // ------------------------------------------------------ kyoku endings
   RS_HD rs_result_rec& result() const { return S.results[e]; }
-  RS_HD void begin_result(int kind) const {
+  RS_COLD void begin_result(int kind) const {
     rs_result_rec& r = result();
     r.kyoku = g.kyoku;
     r.honba = g.honba;
@@ -657,7 +657,7 @@ struct Engine {
     r.n_settlements = 0;
     r.tenpai_mask = 0;
   }
-  RS_HD void end_result() const {
+  RS_COLD void end_result() const {
     rs_result_rec& r = result();
     for (int s = 0; s < 4; s++) r.scores_after[s] = g.scores[s];
   }
@@ -671,7 +671,7 @@ struct Engine {
     g.queue = 0;
   }
   // engine.py:842-872
-  RS_HD void advance_round(bool dealer_repeat, bool reset_honba) {
+  RS_COLD void advance_round(bool dealer_repeat, bool reset_honba) {
     g.n_results++;
     g.drawn = -1;
     if (dealer_repeat && g.repeats >= C.renchan_cap) dealer_repeat = false;
@@ -702,6 +702,7 @@ struct Engine {
   }
   // engine.py:829-839
   RS_COLD void abort_kyoku(int kind) {
+    #pragma unroll 1
     for (int s = 0; s < 4; s++)
       if (hi::riichi(info(s))) { g.scores[s] += 1000; g.deposits -= 1; }
     begin_result(kind);
@@ -713,18 +714,22 @@ struct Engine {
   RS_COLD void exhaustive() {
     emit(EV_DRAW_END, -1, -1);
     int tmask = 0, n = 0;
+    #pragma unroll 1
     for (int s = 0; s < 4; s++)
       if (hi::shanten(info(s)) == 0) { tmask |= 1 << s; n++; }
     int d[4] = {0, 0, 0, 0};
     if (n > 0 && n < 4) {
       const int gain = 3000 / n, loss = 3000 / (4 - n);
+      #pragma unroll 1
       for (int s = 0; s < 4; s++) d[s] = ((tmask >> s) & 1) ? gain : -loss;
     }
+    #pragma unroll 1
     for (int s = 0; s < 4; s++) g.scores[s] += d[s];
     begin_result(RS_RES_EXHAUSTIVE);
     rs_result_rec& r = result();
     r.tenpai_mask = tmask;
     r.n_settlements = 1;
+    #pragma unroll 1
     for (int s = 0; s < 4; s++) r.deltas[0][s] = d[s];
     r.honba_component[0] = 0;
     r.deposits_claimed[0] = 0;
@@ -766,8 +771,11 @@ struct Engine {
     const int loser = g.call_from;
     const int nw = g.rn();
     int w4[3];
+    #pragma unroll 1
     for (int i = 0; i < nw; i++) w4[i] = g.rseat(i);
+    #pragma unroll 1
     for (int i = 1; i < nw; i++)
+      #pragma unroll 1
       for (int j = i; j > 0 && ((w4[j - 1] - loser) & 3) > ((w4[j] - loser) & 3); j--) {
         const int t = w4[j]; w4[j] = w4[j - 1]; w4[j - 1] = t;
       }
@@ -778,6 +786,7 @@ struct Engine {
     r.n_settlements = nw;
     const int dealer = g.dealer();
     bool dealer_won = false;
+    #pragma unroll 1
     for (int i = 0; i < nw; i++) {
       const int seat = w4[i];
       r.winners[i] = (int8_t)seat;
@@ -791,6 +800,7 @@ struct Engine {
       const int honba = i == 0 ? g.honba : 0, dep = i == 0 ? g.deposits : 0;
       int deltas[4], hc;
       settle(false, rd.base, dealer, seat, loser, honba, dep, deltas, &hc);
+      #pragma unroll 1
       for (int s = 0; s < 4; s++) { r.deltas[i][s] = deltas[s]; g.scores[s] += deltas[s]; }
       r.honba_component[i] = hc;
       r.deposits_claimed[i] = dep;
@@ -989,9 +999,11 @@ struct Engine {
   RS_COLD void check_four_kans() {
     if (C.rule != RS_RULE_RED) return;
     int total = 0, seats = 0;
+    #pragma unroll 1
     for (int s = 0; s < 4; s++) {
       const int nm = hi::nmelds(info(s));
       int c = 0;
+      #pragma unroll 1
       for (int i = 0; i < 4; i++)
         if (i < nm && mi::type(meld_info(s, i)) >= M_KAN_OPEN) c++;
       total += c;
@@ -1002,10 +1014,14 @@ struct Engine {
   // append a meld of sorted ids (melds.py:17-34)
   RS_HD void add_meld(int seat, Hand& h, int type, const int* ids, int nids, int called, int from) {
     int t[4];
+    #pragma unroll 1
     for (int i = 0; i < nids; i++) t[i] = ids[i];
+    #pragma unroll 1
     for (int i = 1; i < nids; i++)
+      #pragma unroll 1
       for (int j = i; j > 0 && t[j - 1] > t[j]; j--) { const int x = t[j]; t[j] = t[j - 1]; t[j - 1] = x; }
     uint32_t packed = 0;
+    #pragma unroll 1
     for (int i = 0; i < nids; i++) packed |= (uint32_t)t[i] << (8 * i);
     const int nm = hi::nmelds(h.info);
     RS_CHECK((unsigned)seat < 4u && (unsigned)nm < 4u && nids >= 3 && nids <= 4);
@@ -1032,6 +1048,7 @@ struct Engine {
     if (action == A_PON || action == A_KAN_OPEN) {
       const int need = action == A_PON ? 2 : 3;
       uint32_t nib = h.nibble(kind);
+      #pragma unroll 1
       for (int j = 0; j < need; j++) { const int b = ctz32(nib); nib &= nib - 1; ids[n++] = 4 * kind + b; }
     } else {
       int k0, k1;
@@ -1041,6 +1058,7 @@ struct Engine {
       ids[n++] = h.lowest_of_kind(k0);
       ids[n++] = h.lowest_of_kind(k1);
     }
+    #pragma unroll 1
     for (int j = 0; j < n; j++) hand_take(T, h, ids[j], tok());
     ids[n] = g.call_tile;
     const int type = action == A_PON ? M_PON : (action == A_KAN_OPEN ? M_KAN_OPEN : M_CHI);
@@ -1069,7 +1087,9 @@ struct Engine {
     Hand h = load_hand(bp, seat);
     int ids[4];
     uint32_t nib = h.nibble(kind);
+    #pragma unroll 1
     for (int j = 0; j < 4; j++) { ids[j] = 4 * kind + ctz32(nib); nib &= nib - 1; }
+    #pragma unroll 1
     for (int j = 0; j < 4; j++) hand_take(T, h, ids[j], tok());
     add_meld(seat, h, M_KAN_CLOSED, ids, 4, -1, -1);
     finish_hand(T, h);
@@ -1088,12 +1108,15 @@ struct Engine {
     Hand h = load_hand(bp, seat);
     const int tile = h.lowest_of_kind(kind);
     const int nm = hi::nmelds(h.info);
+    #pragma unroll 1
     for (int i = 0; i < 4; i++)
       if (i < nm) {
         const uint32_t mf = meld_info(seat, i), mt = meld_tiles(seat, i);
         if (mi::type(mf) == M_PON && ((mt & 255) >> 2) == kind) {
           int t[4] = {(int)(mt & 255), (int)((mt >> 8) & 255), (int)((mt >> 16) & 255), tile};
+          #pragma unroll 1
           for (int a = 1; a < 4; a++)
+            #pragma unroll 1
             for (int b = a; b > 0 && t[b - 1] > t[b]; b--) { const int x = t[b]; t[b] = t[b - 1]; t[b - 1] = x; }
           sword(bp, W_MELD + 2 * (4 * seat + i)) = (uint32_t)t[0] | ((uint32_t)t[1] << 8) | ((uint32_t)t[2] << 16) |
                                        ((uint32_t)t[3] << 24);
@@ -1202,13 +1225,16 @@ struct Engine {
   RS_COLD void terminal_rewards(float* r) const {  // game end only
     if (C.reward_scheme == RS_REWARD_RANK) {
       const double RR[4] = {1.0, 0.333, -0.333, -1.0};
+      #pragma unroll 1
       for (int s = 0; s < 4; s++) {
         int rank = 0;
+        #pragma unroll 1
         for (int t = 0; t < 4; t++)
           if (g.scores[t] > g.scores[s] || (g.scores[t] == g.scores[s] && t < s)) rank++;
         r[s] = (float)RR[rank];
       }
     } else {
+      #pragma unroll 1
       for (int s = 0; s < 4; s++) r[s] = (float)((double)(g.scores[s] - 25000) / 25000.0);
     }
   }
