@@ -509,6 +509,12 @@ struct Engine {
   // engine.py:386-390: the cheap shanten test inline, the yaku search cold
   RS_HOT bool can_tsumo(int seat, const Hand& h) const {
     if (hi::shanten(h.info) != -1) return false;
+    // a complete hand always has a reading (shanten -1 is exactly "some
+    // standard / seven-pairs / orphans form"), and every reading carries a
+    // yaku when the hand is in riichi, closed (menzen tsumo), drawn from the
+    // dead wall (rinshan) or the last live tile (haitei): yaku.py:239-310,
+    // :353-369 add those before any other; the search runs otherwise
+    if (hi::riichi(h.info) || hi::nmelds(h.info) == 0 || g.rinshan_pending || g.live() == 0) return true;
     return tsumo_has_yaku(seat, h);
   }
   RS_COLD bool tsumo_has_yaku(int seat, const Hand& h) const {
@@ -526,6 +532,9 @@ struct Engine {
     if (!((wt >> (tile >> 2)) & 1)) return false;
     if (hi::temp(inf) || hi::perm(inf)) return false;
     if (wt & sdword(bp, W_HRKIND + 2 * seat)) return false;
+    // the tile completes the hand (it is a wait), so a reading exists; riichi,
+    // chankan and houtei (last live tile) make every reading valid
+    if (hi::riichi(inf) || chankan || g.live() == 0) return true;
     return ron_has_yaku(seat, tile, chankan);
   }
   RS_COLD bool ron_has_yaku(int seat, int tile, bool chankan) const {
