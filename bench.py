@@ -63,6 +63,9 @@ def parse(argv=None):
     p.add_argument("--no-python-ref", action="store_true",
                    help="reference arm: skip timing the Python reference itself (baseline/_ref)")
     p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--e2e-autoreset", choices=("same", "next"), default="next",
+                   help="HostStepper auto-reset in the e2e leg: in the finishing step, or at the start of the next "
+                        "(the reference runner's order)")
     p.add_argument("--no-fused", action="store_true", help="skip the fused 100-step rollout timing")
     p.add_argument("--no-rows", action="store_true", help="skip the red / 1M-env extra rows")
     p.add_argument("--row-steps", type=int, default=20, help="timed K=1 launches per extra row")
@@ -659,7 +662,8 @@ def e2e_run(args, env, dev, world, obs_to_host: bool):
     n = env.n
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream(dev)
-    hs = HostStepper(env, autoreset=True, observe=True, policy=True, obs_to_host=obs_to_host)
+    autoreset = {"same": True, "next": "next"}[args.e2e_autoreset]
+    hs = HostStepper(env, autoreset=autoreset, observe=True, policy=True, obs_to_host=obs_to_host)
     env.random_actions(out=hs._act_dev)
     hs.actions.copy_(hs._act_dev.cpu())
     acts, nxt = hs.actions.numpy(), hs.next_actions.numpy()  # views of the pinned buffers
@@ -689,6 +693,9 @@ def e2e_run(args, env, dev, world, obs_to_host: bool):
     if not obs_to_host:
         res["api"] = ("HostStepper.step: one CUDA-graph replay per step; the fused step+autoreset+observe+policy "
                       "kernel reads the actions from and writes its results to pinned host memory")
+        res["autoreset"] = ("next step: a finished env starts its next game at the start of the following step, "
+                            "the reference runner's order (bench/runner.py:107-113)" if autoreset == "next" else
+                            "same step: a finished env starts its next game in the step that finishes it")
     hs.close()
     return res
 

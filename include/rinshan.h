@@ -315,6 +315,16 @@ int rs_step(rs_handle* h, const int32_t* actions_dev, const rs_step_out* out, vo
 /* bump the completion word (rs_set_done_flag) once every output of the
  * step is visible to the host */
 #define RS_STEP_SIGNAL 8
+/* instead of RS_STEP_AUTORESET, the reference runner's order
+ * (bench/runner.py:107-113, Gymnasium's next-step autoreset): a finished
+ * env starts its next game at the beginning of the following step, acts
+ * with its own policy stream there (random, or heuristic with
+ * RS_STEP_HEURISTIC; its host action is ignored) and steps.  The step that
+ * finishes an env leaves it finished (its outputs describe the final
+ * state, next action -1).  Per-env trajectories equal rs_rollout's.  Needs
+ * a policy output (next_actions or recs); exclusive with
+ * RS_STEP_AUTORESET. */
+#define RS_STEP_RESET_FIRST 16
 int rs_step_ex(rs_handle* h, const int32_t* actions_dev, int32_t flags, const rs_step_out* out,
                const rs_obs_out* obs, int32_t* next_actions_dev, void* stream);
 /* rs_step_ex with the per-env outputs and the next action (random, or

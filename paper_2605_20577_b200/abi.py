@@ -36,6 +36,7 @@ STEP_AUTORESET = 1
 STEP_OBSERVE = 2
 STEP_HEURISTIC = 4
 STEP_SIGNAL = 8
+STEP_RESET_FIRST = 16
 # rs_check_invariants bits (include/rinshan.h RS_INV_*)
 INV_SCORE_SUM = 1
 INV_TILES = 2

@@ -502,6 +502,13 @@ __global__ void __launch_bounds__(ROLL_BLOCK, ROLL_MINB) k_step(const __grid_con
     if (E.g.env_terminated || E.g.env_truncated) m.clear();
     else m = E.load_legal();
     r[0] = r[1] = r[2] = r[3] = 0.f;
+  } else if ((flags & RS_STEP_RESET_FIRST) && (E.g.env_terminated || E.g.env_truncated)) {
+    // runner.py:107-113: the finished env's next game, then its own policy
+    // draw and the step (the host action is ignored)
+    E.g.resets++;
+    E.init_game(derive_key(E.g.env_key, 2 + (uint64_t)E.g.resets), r);
+    const Mask115 lm = E.load_legal();
+    st = E.step((flags & RS_STEP_HEURISTIC) ? E.heuristic_action(lm) : E.random_action(lm), m, r);
   } else {
     st = E.step(action, m, r);
   }
@@ -1339,6 +1346,8 @@ int rs_step_ex(rs_handle* h, const int32_t* actions_dev, int32_t flags, const rs
                const rs_obs_out* obs, int32_t* next_actions_dev, void* stream) {
   if (!h || !actions_dev) return set_err(RS_E_ARG, "rs_step: null argument");
   if ((flags & RS_STEP_OBSERVE) && !obs) return set_err(RS_E_ARG, "RS_STEP_OBSERVE needs obs buffers");
+  if ((flags & RS_STEP_RESET_FIRST) && ((flags & RS_STEP_AUTORESET) || !next_actions_dev))
+    return set_err(RS_E_ARG, "RS_STEP_RESET_FIRST needs next_actions and excludes RS_STEP_AUTORESET");
   const DeviceScope device_scope(h->device);
   cudaStream_t st = (cudaStream_t)stream;
   rs_obs_out o{};
@@ -1359,6 +1368,8 @@ int rs_step_rec_out(rs_handle* h, const int32_t* actions, int32_t flags, rs_step
                     const rs_obs_out* obs, int32_t* next_actions, void* stream) {
   if (!h || !actions || !recs) return set_err(RS_E_ARG, "rs_step_rec_out: null argument");
   if ((flags & RS_STEP_OBSERVE) && !obs) return set_err(RS_E_ARG, "RS_STEP_OBSERVE needs obs buffers");
+  if ((flags & RS_STEP_RESET_FIRST) && (flags & RS_STEP_AUTORESET))
+    return set_err(RS_E_ARG, "RS_STEP_RESET_FIRST excludes RS_STEP_AUTORESET");
   const DeviceScope device_scope(h->device);
   cudaStream_t st = (cudaStream_t)stream;
   rs_obs_out o{};

@@ -211,7 +211,7 @@ class BatchEnv:
                   "rs_init_indexed")
         return self
 
-    def step(self, actions: torch.Tensor, *, autoreset: bool = False, observe: bool = False,
+    def step(self, actions: torch.Tensor, *, autoreset: bool | str = False, observe: bool = False,
              next_actions: torch.Tensor | None = None, out: abi.rs_step_out | None = None,
              next_policy: str = "random") -> "BatchEnv":
         """step(state, action) for every env (env/core.py:85-94): illegal ids
@@ -223,11 +223,20 @@ class BatchEnv:
         belong to the new game); `observe` fills `self.observe()`'s tensors
         for the current players; `next_actions` (int32[n]) receives the
         next action of `next_policy` ("random" or "heuristic"; -1 for
-        finished envs)."""
+        finished envs).  `autoreset="next"` (needs `next_actions`) instead
+        restarts an env finished by an earlier step at the start of this
+        one, where it acts with `next_policy` (its action is ignored): the
+        reference runner's order (bench/runner.py:107-113)."""
         actions = actions.to(device=self.device, dtype=torch.int32).contiguous()
         if actions.numel() != self.n:
             raise ValueError("need one action per env")
-        flags = (1 if autoreset else 0) | (2 if observe else 0) | (4 if _policy_id(next_policy) else 0)
+        if autoreset == "next":
+            if next_actions is None:
+                raise ValueError('autoreset="next" needs next_actions')
+            flags = abi.STEP_RESET_FIRST
+        else:
+            flags = abi.STEP_AUTORESET if autoreset else 0
+        flags |= (abi.STEP_OBSERVE if observe else 0) | (abi.STEP_HEURISTIC if _policy_id(next_policy) else 0)
         ost = None
         if observe:
             if self._obs is None:
@@ -373,6 +382,14 @@ class HostStepper:
     it to a device block and one copy moves the block (232 bytes per env)
     to the host inside the same graph (the kernel writing it over the host
     link directly was ~2x slower: small scattered stores).
+
+    `autoreset`: True resets a finished env in the step that finishes it
+    (its result shows the transition, its legal mask / observation / next
+    action the new game); "next" (with `policy`) keeps it finished until the
+    following step, which starts its next game, draws its action from its
+    policy stream (the host action is ignored) and steps it -- the
+    reference runner's order (bench/runner.py:107-113) and the same
+    trajectories as `BatchEnv.rollout`; False never resets.
     """
 
     BYTES_PER_ENV = 40
@@ -387,6 +404,10 @@ class HostStepper:
                 raise ValueError("obs_to_host needs observe=True")
             self._obs_host, self.observations = alloc_observations_block(n, pinned=True)
             self._obs_dev_buf, self._obs_dev = alloc_observations_block(n, pinned=False, device=dev)
+        if autoreset not in (True, False, "next"):
+            raise ValueError(f"bad autoreset {autoreset!r}")
+        if autoreset == "next" and not policy:
+            raise ValueError('autoreset="next" needs policy=True (a reset env acts with its own policy)')
         self.env = env
         self.n = n
         self.autoreset, self.observe, self.policy = autoreset, observe, policy
@@ -445,6 +466,12 @@ class HostStepper:
             self._graph = g
             self._stream = s
 
+    def _flags(self) -> int:
+        f = abi.STEP_OBSERVE if self.observe else 0
+        if self.autoreset == "next":
+            return f | abi.STEP_RESET_FIRST
+        return f | (abi.STEP_AUTORESET if self.autoreset else 0)
+
     def _rec_views(self, buf: torch.Tensor) -> dict:
         """views of an rs_step_rec[n] buffer (include/rinshan.h)"""
         n = self.n
@@ -484,7 +511,7 @@ class HostStepper:
         if self._packed:
             env = self.env
             ost = obs_struct(self._obs_target()) if self.observe else None
-            flags = (1 if self.autoreset else 0) | (2 if self.observe else 0)
+            flags = self._flags()
             if self.observations is None:
                 flags |= abi.STEP_SIGNAL  # the kernel's own stores complete the step
             check(env._L.rs_step_rec_out(env._h, self.actions.data_ptr(), flags, self._res_host.data_ptr(),
@@ -498,7 +525,7 @@ class HostStepper:
         if self.zero_copy != "none":
             env = self.env
             ost = obs_struct(self._obs_target()) if self.observe else None
-            flags = (1 if self.autoreset else 0) | (2 if self.observe else 0)
+            flags = self._flags()
             check(env._L.rs_step_ex(env._h, self.actions.data_ptr(), flags, C.byref(self._out),
                                     C.byref(ost) if ost is not None else None,
                                     self._dev_views["next_actions"].data_ptr() if self.policy else None,

@@ -251,10 +251,13 @@ def test_step_tensors_match_records():
 
 @pytest.mark.parametrize("zero_copy,order", ((True, "1"), (False, "1"), (True, "2")))
 @pytest.mark.parametrize("rule", RULES)
-def test_host_stepper_equals_fused_rollout(rule, zero_copy, order, monkeypatch):
+@pytest.mark.parametrize("autoreset", (True, "next"))
+def test_host_stepper_equals_fused_rollout(rule, zero_copy, order, autoreset, monkeypatch):
     """HostStepper (CUDA graph: actions in, fused step+autoreset+observe+
     policy, result block out -- through mapped pinned memory or explicit
-    copies) follows the same trajectories as k_rollout."""
+    copies) follows the same trajectories as k_rollout, with the reset in
+    the finishing step (autoreset=True) or in the next one (autoreset="next",
+    RS_STEP_RESET_FIRST: the runner's order, so finished envs match too)."""
     from paper_2605_20577_b200.env import HostStepper
 
     monkeypatch.setenv("RINSHAN_ORDER", order)  # "2": the env sort runs inside the captured graph
@@ -263,7 +266,7 @@ def test_host_stepper_equals_fused_rollout(rule, zero_copy, order, monkeypatch):
     a = BatchEnv(n, cfg).init(seed=9)
     b = BatchEnv(n, cfg).init(seed=9)
     a.rollout(steps)
-    hs = HostStepper(b, autoreset=True, observe=True, policy=True, zero_copy=zero_copy)
+    hs = HostStepper(b, autoreset=autoreset, observe=True, policy=True, zero_copy=zero_copy)
     first = torch.empty(n, dtype=torch.int32, device="cuda")
     b.random_actions(out=first)
     hs.actions.copy_(first.cpu())
@@ -273,11 +276,18 @@ def test_host_stepper_equals_fused_rollout(rule, zero_copy, order, monkeypatch):
         hs.step()
         hs.actions.copy_(hs.next_actions)
     torch.cuda.synchronize()
-    compared = 0
+    compared = finished = 0
     for i in range(0, n, 3):
         reca, recb = a.export(i), b.export(i)
-        if reca.env_terminated or reca.env_truncated:
+        done = reca.env_terminated or reca.env_truncated
+        if done and autoreset is True:
             continue  # b has already auto-reset this env
+        if done:  # "next": both finished, no next action drawn
+            finished += 1
+            assert not diff(projection(reca), projection(recb)), (i, diff(projection(reca), projection(recb))[:5])
+            assert recb.policy_counter == reca.policy_counter
+            assert hs.next_actions[i] == -1
+            continue
         assert recb.policy_counter == reca.policy_counter + 1
         compared += 1
         ra, rb = projection(reca), projection(recb)
@@ -289,6 +299,8 @@ def test_host_stepper_equals_fused_rollout(rule, zero_copy, order, monkeypatch):
             d["internal"].pop("env_terminated"); d["internal"].pop("env_truncated")
         assert not diff(ra, rb), (i, diff(ra, rb)[:5])
     assert compared > 50
+    if autoreset == "next":
+        assert b.export(0).resets == a.export(0).resets
 
 
 @pytest.mark.parametrize("rule", RULES)
