@@ -10,6 +10,8 @@
 // masks (+ a mask of ids counted twice), so a reading needs no arrays.
 #pragma once
 
+#include <cstddef>
+
 #include "../../include/rinshan.h"
 #include "rs_common.cuh"
 
@@ -445,14 +447,19 @@ RS_COLD bool score_win(const WinIn& w, Reading& best, bool first_only) {
 // yaku id (yakuman multiplicity for yakuman hands), the reading's totals and
 // the dora parts of the win context
 RS_HD void fill_win_rec(rs_win_rec& x, const Reading& rd, const WinIn& w) {
+  // ten zero words, then the han of the (few) yaku present
+  static_assert(offsetof(rs_win_rec, yaku_han) == 0 && alignof(rs_win_rec) >= 4 && sizeof(x.yaku_han) == 40,
+                "yaku_han: ten aligned words");
+  uint32_t* yh = reinterpret_cast<uint32_t*>(x.yaku_han);
 #pragma unroll 1
-  for (int id = 0; id < 40; id++) {
-    int han = 0;
-    if ((rd.mask >> id) & 1) {
-      if (rd.yakuman) han = ((rd.x2 >> id) & 1) ? 2 : 1;
-      else han = yaku_han_of(id, rd.form == 1 ? true : w.closed);
-    }
-    x.yaku_han[id] = (int8_t)han;
+  for (int i = 0; i < 10; i++) yh[i] = 0u;
+  uint64_t ym = rd.mask;
+  while (ym) {
+    const int id = ctz64(ym);
+    ym &= ym - 1;
+    RS_CHECK(id < 40);
+    x.yaku_han[id] = (int8_t)(rd.yakuman ? (((rd.x2 >> id) & 1) ? 2 : 1)
+                                         : yaku_han_of(id, rd.form == 1 ? true : w.closed));
   }
   x.yakuman = rd.yakuman;
   x.han = rd.han;
