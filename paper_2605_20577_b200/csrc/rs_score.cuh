@@ -372,29 +372,37 @@ RS_COLD bool score_win(const WinIn& w, Reading& best, bool first_only) {
     Counts base = w.conc;
     base.sub(p, 2);
     // enumerate set extractions (decompose.py:24-47): at each level take the
-    // lowest kind as a triplet (bit 0) or a run (bit 1)
+    // lowest kind as a triplet (bit clear) or a run (bit set); level d reads
+    // choice bit needed-1-d, so the choices sharing a prefix are contiguous
+    // and a level that fails skips all of them
     uint32_t decs[16];
     int nd = 0;
-    #pragma unroll 1
+#pragma unroll 1
     for (int choice = 0; choice < (1 << needed); choice++) {
       Counts c = base;
       int keys[4];
-      bool ok = true;
-      #pragma unroll 1
-      for (int d = 0; d < needed && ok; d++) {
+      int fail = -1;
+#pragma unroll 1
+      for (int d = 0; d < needed; d++) {
         const int i = c.lowest();
-        if (i >= 34) { ok = false; break; }
-        if (!((choice >> d) & 1)) {
-          if (c.get(i) >= 3) { c.sub(i, 3); keys[d] = 64 + i; }
-          else ok = false;
-        } else {
-          if (i < 27 && i % 9 <= 6 && c.get(i + 1) && c.get(i + 2)) {
+        bool ok = i < 34;
+        if (ok && !((choice >> (needed - 1 - d)) & 1)) {
+          ok = c.get(i) >= 3;
+          if (ok) { c.sub(i, 3); keys[d] = 64 + i; }
+        } else if (ok) {
+          ok = i < 27 && i % 9 <= 6 && c.get(i + 1) && c.get(i + 2);
+          if (ok) {
             c.sub(i, 1); c.sub(i + 1, 1); c.sub(i + 2, 1);
             keys[d] = i;
-          } else ok = false;
+          }
         }
+        if (!ok) { fail = d; break; }
       }
-      if (!ok || !c.empty()) continue;
+      if (fail >= 0) {
+        choice |= (1 << (needed - 1 - fail)) - 1;
+        continue;
+      }
+      if (!c.empty()) continue;
       // sorted(sets): insertion sort of <= 4 keys, packed 7 bits each
       #pragma unroll 1
       for (int a = 1; a < needed; a++)
