@@ -439,7 +439,10 @@ struct Engine {
   // ------------------------------------------------------ win evaluation
   // engine.py:345-375 (_win_context)
   // one out-of-line copy for its four callers (cold: win checks and settlements)
-  RS_COLD void win_input(int seat, const Hand& h, int win_tile, bool tsumo, bool chankan, WinIn& w) const {
+  // `value`: also the dora / ura / red counts (the settlement); the legality
+  // checks only ask whether a reading carries a yaku, which they never change
+  RS_COLD void win_input(int seat, const Hand& h, int win_tile, bool tsumo, bool chankan, WinIn& w,
+                         bool value = true) const {
     const uint32_t inf = h.info;
     w.conc.c[0] = nib_counts(h.w0);
     w.conc.c[1] = nib_counts(h.w1);
@@ -451,7 +454,7 @@ struct Engine {
     w.closed = true;
     Counts all = w.conc;
     int reds = 0;
-    if (C.rule == RS_RULE_RED) {
+    if (value && C.rule == RS_RULE_RED) {
       reds = (int)h.has(16) + (int)h.has(52) + (int)h.has(88);
       if (!tsumo && is_red_tile(win_tile)) reds++;
     }
@@ -464,7 +467,7 @@ struct Engine {
         w.mtype[i] = mi::type(mf);
         w.mbase[i] = (mt & 255) >> 2;
         if (w.mtype[i] != M_KAN_CLOSED) w.closed = false;
-        const int nt = mi::ntiles(mf);
+        const int nt = value ? mi::ntiles(mf) : 0;
         #pragma unroll 1
         for (int j = 0; j < 4; j++)
           if (j < nt) {
@@ -493,12 +496,12 @@ struct Engine {
     }
     // dora.py:9-26
     int dora = 0, ura = 0;
+    const int nd = value ? (int)g.dora_count : 0;
 #pragma unroll 1
-    for (int i = 0; i < 5; i++)
-      if (i < g.dora_count) {
-        dora += all.get(dora_kind(wall(122 + 2 * i) >> 2));
-        if (w.riichi) ura += all.get(dora_kind(wall(123 + 2 * i) >> 2));
-      }
+    for (int i = 0; i < nd; i++) {
+      dora += all.get(dora_kind(wall(122 + 2 * i) >> 2));
+      if (w.riichi) ura += all.get(dora_kind(wall(123 + 2 * i) >> 2));
+    }
     w.dora = dora;
     w.ura = ura;
     w.reds = reds;
@@ -519,7 +522,7 @@ struct Engine {
   }
   RS_COLD bool tsumo_has_yaku(int seat, const Hand& h) const {
     WinIn w;
-    win_input(seat, h, g.drawn, true, false, w);
+    win_input(seat, h, g.drawn, true, false, w, false);
     Reading r;
     return score_win(w, r, true);
   }
@@ -540,7 +543,7 @@ struct Engine {
   RS_COLD bool ron_has_yaku(int seat, int tile, bool chankan) const {
     const Hand h = load_hand(bp, seat);
     WinIn w;
-    win_input(seat, h, tile, false, chankan, w);
+    win_input(seat, h, tile, false, chankan, w, false);
     Reading r;
     return score_win(w, r, true);
   }
