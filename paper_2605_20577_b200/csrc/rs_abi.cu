@@ -460,12 +460,74 @@ __device__ __noinline__ void signal_done(const Done& d, uint32_t working, int la
 // the stream (e.g. a copy of the observations to the host)
 __global__ void k_signal(Done done) { signal_done(done, 0xFFFFFFFFu, (int)(threadIdx.x & 31)); }
 
+// Instruction warm-up for the win path (DESIGN §4 item 55): at small
+// batches a K=1 launch runs the scoring code (win input, the reading search,
+// settlement, the result record) on at most a few envs, after the L2 flush
+// that precedes every launch, so its instructions come from HBM one line at
+// a time (~40 K cycles for a win).  One extra CTA runs the two largest
+// single-copy (out-of-line) pieces at the start of the launch on a constant
+// closed riichi tsumo, one piece per warp so they are fetched in parallel
+// and ahead of any env (its scratch block in its own shared memory, nothing
+// written outside the CTA); by the time an env reaches a win or a yaku
+// check those lines are in L2.
+__device__ __noinline__ void warm_win_path(int piece, const Soa& S, const Tabs& T, const Cfg& C, uint8_t* scratch,
+                                           volatile int* sink) {
+  // 234m 567m 345p 678s 55z (+ the drawn 3m)
+  constexpr uint8_t tiles[14] = {4, 8, 12, 16, 20, 24, 48, 52, 56, 96, 100, 104, 128, 129};
+  if (piece == 0) {  // the reading search (the largest piece)
+    WinIn w;
+    for (int j = 0; j < 5; j++) w.conc.c[j] = 0;
+    for (int i = 0; i < 14; i++) w.conc.add(tiles[i] >> 2, 1);
+    w.nmelds = 0;
+    for (int m = 0; m < 4; m++) w.mtype[m] = w.mbase[m] = 0;
+    w.win_kind = 3;
+    w.tsumo = true;
+    w.seat_wind = 27;
+    w.round_wind = 27;
+    w.riichi = 1;
+    w.ippatsu = w.last_tile = w.rinshan = w.chankan = w.first_draw = false;
+    w.closed = true;
+    w.dora = w.ura = w.reds = 0;
+    w.double_yakuman = w.kazoe = false;
+    Reading rd;
+    score_win(w, rd, false);
+    *sink = rd.han + rd.fu;
+  } else if (piece == 1) {  // the win input of an engine over a zeroed block
+    for (int i = 0; i < (int)BLK_BYTES / 4; i++) reinterpret_cast<uint32_t*>(scratch)[i] = 0u;
+    Engine E(S, T, C, 0, scratch);
+    E.g = Game{};
+    E.g.dora_count = 1;
+    Hand h;
+    h.w0 = h.w1 = h.w2 = h.w3 = h.w4 = 0;
+    h.cm = h.cp = h.cs = h.cz = 0;
+    for (int i = 0; i < 14; i++) deal_tile(h, tiles[i]);
+    h.info = hi::set_riichi(hi::set_nconc(hi::set_riichi_index(0u, -1), 14), 1);
+    WinIn w;
+    E.win_input(0, h, 12, true, false, w);
+    *sink = w.dora + w.win_kind;
+  }
+}
+
+// the warm-up CTA's body: warp w runs piece w (piece 1's scratch block in
+// the CTA's dynamic shared memory when it fits)
+__device__ __forceinline__ void warm_cta(const Soa& S, const Tabs& T, const Cfg& C) {
+  __shared__ int s_sink;
+  const int wp = threadIdx.x >> 5;
+  const uint32_t need = wp == 1 ? BLK_BYTES : 0u;
+  if ((threadIdx.x & 31) == 0 && wp < 2 && need <= dyn_smem_bytes()) warm_win_path(wp, S, T, C, g_smem, &s_sink);
+}
+
 __global__ void __launch_bounds__(ROLL_BLOCK, ROLL_MINB) k_step(const __grid_constant__ Soa S, const __grid_constant__ DevTables D,
     const __grid_constant__ Cfg C, const int32_t* actions, int flags, rs_obs_out obs, int32_t* next_actions,
     StepOut out, int epw, int staged, int glog2, int check, rs_step_rec* recs, const int32_t* order,
-    uint8_t* kind_out, int prefetch, Done done) {
+    uint8_t* kind_out, int prefetch, Done done, int warm) {
   tables_begin(D, glog2);  // the action and header loads overlap the table copy
   const Tabs T{};
+  if (warm && blockIdx.x == gridDim.x - 1) {  // the warm-up CTA (no envs)
+    warm_cta(S, T, C);
+    tables_wait();
+    return;
+  }
   const int lane = threadIdx.x & 31;
   const int q = ((blockIdx.x * blockDim.x + threadIdx.x) >> 5) * epw + (lane >> glog2);
   const bool idle = (lane >> glog2) >= epw || q >= S.n;
@@ -620,15 +682,20 @@ __global__ void __launch_bounds__(ROLL_BLOCK, ROLL_MINB) k_rollout(const __grid_
                                                    uint64_t* digests, rs_obs_out dobs, StepOut out, int epw,
                                                    uint32_t* prof, int staged, int policy, int glog2,
                                                    int check, const int32_t* order, uint8_t* kind_out,
-                                                   int prefetch) {
+                                                   int prefetch, int warm) {
   const uint32_t g_entry = prof ? globaltimer_lo() : 0u;
   tables_begin(D, glog2);  // the first env tile's header loads overlap the copy
   const Tabs T{};
+  if (warm && blockIdx.x == gridDim.x - 1) {  // the warm-up CTA (no envs)
+    warm_cta(S, T, C);
+    tables_wait();
+    return;
+  }
   bool tables_ready = false;
   uint32_t g_staged = 0u;
   unsigned long long games = 0;
   const int lane = threadIdx.x & 31;
-  const int warps = (gridDim.x * blockDim.x) >> 5;
+  const int warps = ((gridDim.x - (warm ? 1 : 0)) * blockDim.x) >> 5;
   const int sub = lane & ((1 << glog2) - 1);  // the lane's index in its env's group
   const uint32_t gm = glog2 >= 5 ? 0xFFFFFFFFu : (((1u << (1 << glog2)) - 1u) << (lane - sub));
   // one stage slot per env, shared by the env's lane group
@@ -883,6 +950,7 @@ struct rs_handle {
   int cluster;
   int occ_cl_key[8], occ_cl_val[8];  // co-resident clusters per (block, smem)
   int prefetch;  // RINSHAN_PREFETCH: L1 prefetch of an env's lines before its step (prefetch_env)
+  int warm;      // RINSHAN_WARM (default 1): the win-path warm-up CTA at small batches (warm_win_path)
   // rs_set_done_flag: the step launches' completion word in mapped host
   // memory and its device-side counter / sequence
   uint32_t* done_flag = nullptr;
@@ -957,6 +1025,9 @@ Launch launch_at(rs_handle* h, int epw) {
   L.grid = (L.grid + L.cluster - 1) / L.cluster * L.cluster;
   return L;
 }
+// the win-path warm-up CTA (warm_win_path): lane-group launches (small
+// batches, where a launch holds few wins) without clusters
+int warm_of(const rs_handle* h, const Launch& L) { return h->warm && L.cluster <= 1 && L.glog2 > 0 ? 1 : 0; }
 // CTAs of the persistent grid: every resident CTA, or with clusters every
 // CTA of the clusters that fit at once (cudaOccupancyMaxActiveClusters)
 int persistent_ctas(rs_handle* h, const Launch& L) {
@@ -1293,6 +1364,8 @@ int rs_create(rs_handle** out, int64_t n_envs, const rs_config* cfg, int32_t dev
   // round 2: with the observer streams replaced by the 256-byte event ring, mode 2 (block + ring) is the
   // default: +1-1.7 % at 262 K-1 M envs, neutral at 4,096-64 K
   h->prefetch = prefetch_env_s ? std::max(0, std::min(2, atoi(prefetch_env_s))) : 2;
+  const char* warm_env_s = getenv("RINSHAN_WARM");
+  h->warm = warm_env_s ? (atoi(warm_env_s) != 0) : 1;
   const char* stage_env = getenv("RINSHAN_STAGE");
   h->stage_mode = stage_env ? std::max(0, std::min(2, atoi(stage_env))) : 0;
   const char* groups_env = getenv("RINSHAN_GROUPS");
@@ -1357,10 +1430,10 @@ int rs_step_ex(rs_handle* h, const int32_t* actions_dev, int32_t flags, const rs
     const int rc = order_envs(h, st);
     if (rc) return rc;
   }
-  CUDA_TRY(launch_tables(h, k_step, L.grid, L.block, L.smem, st, h->S, h->D, h->cfg, actions_dev, flags, o,
-                         next_actions_dev, step_out(h, out), L.epw, L.staged, L.glog2, h->check_steps,
+  CUDA_TRY(launch_tables(h, k_step, L.grid + warm_of(h, L), L.block, L.smem, st, h->S, h->D, h->cfg, actions_dev,
+                         flags, o, next_actions_dev, step_out(h, out), L.epw, L.staged, L.glog2, h->check_steps,
                          (rs_step_rec*)nullptr, L.ordered ? (const int32_t*)h->order : nullptr,
-                         L.ordered ? h->kind : nullptr, h->prefetch, done_of(h, L, flags)));
+                         L.ordered ? h->kind : nullptr, h->prefetch, done_of(h, L, flags), warm_of(h, L)));
   return finish_step_out(h, out, st);
 }
 
@@ -1379,10 +1452,10 @@ int rs_step_rec_out(rs_handle* h, const int32_t* actions, int32_t flags, rs_step
     const int rc = order_envs(h, st);
     if (rc) return rc;
   }
-  CUDA_TRY(launch_tables(h, k_step, L.grid, L.block, L.smem, st, h->S, h->D, h->cfg, actions, flags, o,
-                         next_actions, StepOut{}, L.epw, L.staged, L.glog2, h->check_steps, recs,
+  CUDA_TRY(launch_tables(h, k_step, L.grid + warm_of(h, L), L.block, L.smem, st, h->S, h->D, h->cfg, actions,
+                         flags, o, next_actions, StepOut{}, L.epw, L.staged, L.glog2, h->check_steps, recs,
                          L.ordered ? (const int32_t*)h->order : nullptr, L.ordered ? h->kind : nullptr,
-                         h->prefetch, done_of(h, L, flags)));
+                         h->prefetch, done_of(h, L, flags), warm_of(h, L)));
   return 0;
 }
 
@@ -1497,11 +1570,11 @@ int rs_rollout_policy(rs_handle* h, int32_t steps, int32_t policy, const rs_obs_
       if (tr.terminated) trt.terminated = tr.terminated + (size_t)t * n;
       if (tr.truncated) trt.truncated = tr.truncated + (size_t)t * n;
       if (tr.status) trt.status = tr.status + (size_t)t * n;
-      CUDA_TRY(launch_tables(h, kern, L.grid, L.block, L.smem, st, h->S, h->D, h->cfg, 1, ot, slots,
+      CUDA_TRY(launch_tables(h, kern, L.grid + warm_of(h, L), L.block, L.smem, st, h->S, h->D, h->cfg, 1, ot, slots,
                              actions_log ? actions_log + (size_t)t * n : nullptr,
                              actors_log ? actors_log + (size_t)t * n : nullptr, trt, stats_dev, digests_dev,
                              h->dig_obs, step_out(h, out), L.epw, nullptr, L.staged, policy, L.glog2,
-                             h->check_steps, (const int32_t*)h->order, h->kind, h->prefetch));
+                             h->check_steps, (const int32_t*)h->order, h->kind, h->prefetch, warm_of(h, L)));
     }
     return finish_step_out(h, out, st);
   }
@@ -1509,11 +1582,11 @@ int rs_rollout_policy(rs_handle* h, int32_t steps, int32_t policy, const rs_obs_
     const int rc = order_envs(h, st);
     if (rc) return rc;
   }
-  CUDA_TRY(launch_tables(h, kern, L.grid, L.block, L.smem, st, h->S, h->D, h->cfg, steps, o, obs ? obs_slots : 0,
-                         actions_log, actors_log, step_out(h, traj), stats_dev, digests_dev, h->dig_obs,
-                         step_out(h, out), L.epw, nullptr, L.staged, policy, L.glog2, h->check_steps,
+  CUDA_TRY(launch_tables(h, kern, L.grid + warm_of(h, L), L.block, L.smem, st, h->S, h->D, h->cfg, steps, o,
+                         obs ? obs_slots : 0, actions_log, actors_log, step_out(h, traj), stats_dev, digests_dev,
+                         h->dig_obs, step_out(h, out), L.epw, nullptr, L.staged, policy, L.glog2, h->check_steps,
                          L.ordered ? (const int32_t*)h->order : nullptr, L.ordered ? h->kind : nullptr,
-                         h->prefetch));
+                         h->prefetch, warm_of(h, L)));
   return finish_step_out(h, out, st);
 }
 
@@ -1530,7 +1603,7 @@ int rs_debug_rollout_cycles(rs_handle* h, int32_t steps, const rs_obs_out* obs, 
   CUDA_TRY(launch_tables(h, k_rollout<false>, L.grid, L.block, L.smem, st, h->S, h->D, h->cfg, steps, o, obs ? 1 : 0,
                          nullptr, nullptr, StepOut{}, nullptr, nullptr, rs_obs_out{}, StepOut{}, L.epw, prof_dev, L.staged,
                          (int)RS_POLICY_RANDOM, L.glog2, 0, (const int32_t*)nullptr, (uint8_t*)nullptr,
-                         h->prefetch));
+                         h->prefetch, 0));
   CUDA_TRY(cudaGetLastError());
   return 0;
 }
