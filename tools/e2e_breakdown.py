@@ -56,12 +56,12 @@ recs = torch.empty(n * 40, dtype=torch.uint8, device=dev)
 
 
 def step_dev():
-    env._L.rs_step_rec_out(env._h, acts.data_ptr(), 3, recs.data_ptr(), C.byref(ost), None, s.cuda_stream)
+    env._L.rs_step_rec_out(env._h, acts.data_ptr(), 18, recs.data_ptr(), C.byref(ost), None, s.cuda_stream)
     acts.copy_(recs.view(torch.int32).view(n, 10)[:, 8])
 
 
 res["step_dev"] = timed(step_dev)
-hs = HostStepper(env, autoreset=True, observe=True, policy=True)
+hs = HostStepper(env, autoreset="next", observe=True, policy=True)
 env.random_actions(out=hs._act_dev)
 hs.actions.copy_(hs._act_dev.cpu())
 def step_map():
@@ -83,7 +83,7 @@ def e2e():
 
 res["e2e"] = timed(e2e)
 hs.close()
-hs2 = HostStepper(env, autoreset=True, observe=True, policy=True, obs_to_host=True)
+hs2 = HostStepper(env, autoreset="next", observe=True, policy=True, obs_to_host=True)
 hs2.actions.copy_(hs.actions)
 a2, n2 = hs2.actions.numpy(), hs2.next_actions.numpy()
 

@@ -16,7 +16,7 @@ dev = torch.device("cuda", 0)
 flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
 env = BatchEnv(n, EnvConfig(rule="no-red"), device=dev).init(seed=0)
 env.rollout(300)
-hs = HostStepper(env, autoreset=True, observe=True, policy=True)
+hs = HostStepper(env, autoreset="next", observe=True, policy=True)
 env.random_actions(out=hs._act_dev)
 hs.actions.copy_(hs._act_dev.cpu())
 acts, nxt = hs.actions.numpy(), hs.next_actions.numpy()
