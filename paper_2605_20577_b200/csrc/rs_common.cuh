@@ -54,9 +54,10 @@ inline uint4 make_uint4(uint32_t x, uint32_t y, uint32_t z, uint32_t w) { return
 
 // Measured alternatives kept buildable (tools/build_variant.sh -D...):
 //   -DRS_AB_OFF_WIN16   observation window over 4 lanes instead of 8 / 16
-//   -DRS_CLAIM_LANES    opponents' claim checks on three lanes of the env's
-//                       group, combined by one warp reduction (2 % slower at
-//                       4,096 envs: the checks diverge per lane anyway)
+//   -DRS_NO_CLAIM_LANES the opponents' claim checks on every lane of the
+//                       env's group instead of one opponent per lane (lanes
+//                       1-3, combined by one warp reduction: the default
+//                       since the cold paths shrank, DESIGN §4 items 31, 56)
 //   -DRS_SWAP5          the deal's swap chain five swaps per load round
 //                       (neutral to -0.7 %: resets are not the launch tail)
 #if defined(RS_AB_OFF_WIN16)
@@ -64,10 +65,10 @@ inline uint4 make_uint4(uint32_t x, uint32_t y, uint32_t z, uint32_t w) { return
 #else
 #define RS_WIN16 1
 #endif
-#if defined(RS_CLAIM_LANES)
-#define RS_CLAIM_LANES_ON 1
-#else
+#if defined(RS_NO_CLAIM_LANES)
 #define RS_CLAIM_LANES_ON 0
+#else
+#define RS_CLAIM_LANES_ON 1
 #endif
 #if defined(RS_SWAP5)
 #define RS_SWAP5_ON 1
