@@ -37,6 +37,12 @@ STEP_OBSERVE = 2
 STEP_HEURISTIC = 4
 STEP_SIGNAL = 8
 STEP_RESET_FIRST = 16
+
+# status returns (include/rinshan.h; positive values are cudaError_t)
+RS_E_ARG = -1
+RS_E_TABLES = -2
+RS_E_STATE = -3
+RS_E_CORRUPT = -4
 # rs_check_invariants bits (include/rinshan.h RS_INV_*)
 INV_SCORE_SUM = 1
 INV_TILES = 2

@@ -105,3 +105,40 @@ def test_skip_action_leaves_envs_untouched(rule):
         ra.policy_counter = rb.policy_counter
         assert bytes(ra) == bytes(rb), i
     assert torch.equal(a_env.legal_bits, b.legal_bits)
+
+
+def test_reset_first_flag_validation():
+    """RS_STEP_RESET_FIRST needs a policy output and excludes
+    RS_STEP_AUTORESET (include/rinshan.h); BatchEnv.step(autoreset="next")
+    needs next_actions"""
+    from paper_2605_20577_b200 import abi
+
+    env = BatchEnv(8, EnvConfig()).init(seed=3)
+    acts = env.random_actions()
+    nxt = torch.empty(8, dtype=torch.int32, device="cuda")
+    L, h, s = env._L, env._h, torch.cuda.current_stream().cuda_stream
+    assert L.rs_step_ex(h, acts.data_ptr(), abi.STEP_RESET_FIRST | abi.STEP_AUTORESET, None, None, nxt.data_ptr(),
+                        s) == abi.RS_E_ARG
+    assert L.rs_step_ex(h, acts.data_ptr(), abi.STEP_RESET_FIRST, None, None, None, s) == abi.RS_E_ARG
+    with pytest.raises(ValueError):
+        env.step(acts, autoreset="next")
+    env.step(acts, autoreset="next", next_actions=nxt)  # valid
+    torch.cuda.synchronize()
+    env.close()
+
+
+@pytest.mark.parametrize("warm", ("0", "1"))
+def test_warm_cta_leaves_trajectories_unchanged(warm, monkeypatch):
+    """the win-path warm-up CTA (RINSHAN_WARM, small batches) writes nothing
+    an env can see: digests with and without it equal the oracle's"""
+    monkeypatch.setenv("RINSHAN_WARM", warm)
+    n, steps, seed = 512, 200, 77
+    env = BatchEnv(n, EnvConfig(rule="red")).init(seed=seed, index_base=0)
+    digests = torch.zeros(n, dtype=torch.int64, device="cuda")
+    for _ in range(steps):
+        env.rollout(1, digests=digests)
+    torch.cuda.synchronize()
+    got = [int(x) & ((1 << 64) - 1) for x in digests.cpu().tolist()]
+    env.close()
+    _, ref = O.run_shard(O.make_config(rule="red"), seed, 0, n, steps, digests=True)
+    assert got == ref
