@@ -1077,9 +1077,18 @@ int envs_per_warp(rs_handle* h) {
   return epw;
 }
 // `persistent` caps the grid at the resident CTAs (k_rollout walks env tiles)
+// `persistent`: the rollout's grid-stride loop over the resident CTAs only
+// when every CTA stages the tables (-DRS_TABLES_SMEM: one copy per CTA);
+// with the tables read through L1 one env group per warp and the hardware
+// block scheduler balancing the uneven steps is faster (DESIGN §4 item 57:
+// 1 M envs +7-8 %, 262 K +10 %)
 Launch step_launch(rs_handle* h, bool persistent) {
   Launch L = launch_at(h, envs_per_warp(h));
+#if defined(RS_TABLES_SMEM)
   if (persistent) L.grid = std::min(L.grid, persistent_ctas(h, L));
+#else
+  (void)persistent;
+#endif
   return L;
 }
 
