@@ -935,7 +935,7 @@ struct rs_handle {
   // env ordering (large batches): each stepping launch records the kind of
   // every env's next step; the next launch first sorts the envs by kind
   // (CUB radix sort, 2 key bits) so a warp's envs share a branch structure
-  int ordering;            // RINSHAN_ORDER: 0 off, 1 at >= 131072 envs (default), 2 always
+  int ordering;            // RINSHAN_ORDER: 0 off, 1 at >= 524288 envs (default), 2 always
   uint8_t* kind;           // [n] next-step kind per env (k_rollout / k_step write it)
   uint8_t* kind_sorted;    // [n] sort scratch
   int32_t* iota;           // [n] 0..n-1
@@ -1013,11 +1013,11 @@ Launch launch_at(rs_handle* h, int epw) {
   L.glog2 = 0;
   if (h->groups)
     while ((epw << (L.glog2 + 1)) <= 32) L.glog2++;
-  // measured on B200, final build (tools/order_thresh.sh; 100 launches from
-  // fresh games / 50 after 300 steps): 262 K envs +9 % / +42 %, 131 K +6 % /
-  // +16 %, 64 K -12 % / -10 % (the sort's launches cost more than the
-  // divergence saved below ~100 K envs)
-  L.ordered = h->ordering == 2 || (h->ordering == 1 && h->n >= (1 << 17));
+  // measured on B200, round-2 final build with the batch-sized grid (50
+  // launches after 200 steps, sorted vs not): 1 M envs +4.3 %, 512 K +2.4 %,
+  // 262 K -2.2 %, 131 K -10 % (round 1's persistent grid gained from the
+  // sort down to 131 K: it bound each thread to a fixed list of envs)
+  L.ordered = h->ordering == 2 || (h->ordering == 1 && h->n >= (1 << 19));
   L.smem = L.staged ? smem_staged(L.block, L.block / 32 * epw, L.glog2) : smem_for(L.block, L.glog2);
   L.ctas = resident_ctas(h, L.block, L.smem);
   L.grid = warp_grid(h, epw, L.block, 0);
