@@ -935,7 +935,7 @@ struct rs_handle {
   // env ordering (large batches): each stepping launch records the kind of
   // every env's next step; the next launch first sorts the envs by kind
   // (CUB radix sort, 2 key bits) so a warp's envs share a branch structure
-  int ordering;            // RINSHAN_ORDER: 0 off, 1 at >= 524288 envs (default), 2 always
+  int ordering;            // RINSHAN_ORDER: 0 off, 1 at >= 131072 envs (default), 2 always
   uint8_t* kind;           // [n] next-step kind per env (k_rollout / k_step write it)
   uint8_t* kind_sorted;    // [n] sort scratch
   int32_t* iota;           // [n] 0..n-1
@@ -1013,11 +1013,12 @@ Launch launch_at(rs_handle* h, int epw) {
   L.glog2 = 0;
   if (h->groups)
     while ((epw << (L.glog2 + 1)) <= 32) L.glog2++;
-  // measured on B200, round-2 final build with the batch-sized grid (50
-  // launches after 200 steps, sorted vs not): 1 M envs +4.3 %, 512 K +2.4 %,
-  // 262 K -2.2 %, 131 K -10 % (round 1's persistent grid gained from the
-  // sort down to 131 K: it bound each thread to a fixed list of envs)
-  L.ordered = h->ordering == 2 || (h->ordering == 1 && h->n >= (1 << 19));
+  // measured on B200, round-2 final build with the batch-sized grid, K=1
+  // launches at the plateau (launches 800-1200 from fresh games,
+  // tools/drift_probe.py; unsorted envs drift apart for ~800 steps, sorted
+  // ones hold): 262 K envs sorted 355 vs 468 us, 131 K 205 vs 250 us, 64 K
+  // 138 vs 141 us, 16 K 75 vs 66 us
+  L.ordered = h->ordering == 2 || (h->ordering == 1 && h->n >= (1 << 17));
   L.smem = L.staged ? smem_staged(L.block, L.block / 32 * epw, L.glog2) : smem_for(L.block, L.glog2);
   L.ctas = resident_ctas(h, L.block, L.smem);
   L.grid = warp_grid(h, epw, L.block, 0);
