@@ -560,19 +560,21 @@ __global__ void __launch_bounds__(ROLL_BLOCK, ROLL_MINB) k_step(const __grid_con
   // yet); its outputs describe its current state with zero rewards
   const bool skip = action == RS_ACTION_SKIP;
   int st = 0;
-  if (skip) {
-    if (E.g.env_terminated || E.g.env_truncated) m.clear();
-    else m = E.load_legal();
-    r[0] = r[1] = r[2] = r[3] = 0.f;
-  } else if ((flags & RS_STEP_RESET_FIRST) && (E.g.env_terminated || E.g.env_truncated)) {
+  int act = action;
+  if (!skip && (flags & RS_STEP_RESET_FIRST) && (E.g.env_terminated || E.g.env_truncated)) {
     // runner.py:107-113: the finished env's next game, then its own policy
     // draw and the step (the host action is ignored)
     E.g.resets++;
     E.init_game(derive_key(E.g.env_key, 2 + (uint64_t)E.g.resets), r);
     const Mask115 lm = E.load_legal();
-    st = E.step((flags & RS_STEP_HEURISTIC) ? E.heuristic_action(lm) : E.random_action(lm), m, r);
+    act = (flags & RS_STEP_HEURISTIC) ? E.heuristic_action(lm) : E.random_action(lm);
+  }
+  if (skip) {
+    if (E.g.env_terminated || E.g.env_truncated) m.clear();
+    else m = E.load_legal();
+    r[0] = r[1] = r[2] = r[3] = 0.f;
   } else {
-    st = E.step(action, m, r);
+    st = E.step(act, m, r);  // one inlined copy of the transition (cold code, §4 item 49)
   }
   const int term = E.g.env_terminated, trunc = E.g.env_truncated;
   bool dirty = !skip && st != RS_STATUS_CONTRACT;
