@@ -1009,6 +1009,9 @@ Launch launch_at(rs_handle* h, int epw) {
   L.epw = epw;
   const int64_t warps = (h->n + epw - 1) / epw;
   L.block = warps * 32 >= (int64_t)h->num_sms * ROLL_BLOCK ? ROLL_BLOCK : BLOCK;
+  // large batches (the batch-sized grid, item 57): 128-thread CTAs give the
+  // block scheduler finer units (131 K +1.7 %, 262 K +4.2 %, 1 M +2.0 %)
+  if (h->n >= (1 << 17)) L.block = BLOCK;
   if (h->block_override > 0) L.block = h->block_override;
   L.staged = h->stage_mode == 2 || (h->stage_mode == 1 && epw < 32);
   // idle lanes join their env as a lane group (not with the stage: one slot per lane)
