@@ -2,7 +2,7 @@
 # profiling tool: build_variant.sh NAME "-DFOO=1 ..." -> build_variants/NAME.so from the current csrc
 set -e
 name=$1; shift
-rm -rf /tmp/vb_$name && mkdir -p /tmp/vb_$name/p /tmp/vb_$name/include
+rm -rf /tmp/vb_$name && mkdir -p /tmp/vb_$name/p /tmp/vb_$name/include /root/repo/build_variants
 cp /root/repo/include/rinshan.h /tmp/vb_$name/include/
 cp -r /root/repo/paper_2605_20577_b200/csrc /tmp/vb_$name/p/csrc
 cd /tmp/vb_$name/p/csrc
