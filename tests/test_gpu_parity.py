@@ -398,3 +398,30 @@ def test_host_stepper_observations_to_host(zero_copy):
         for k, v in dev_obs.items():
             assert torch.equal(host_obs[k], v.cpu()), (t, k)
     hs.close()
+
+
+@pytest.mark.parametrize("policy", ("random", "heuristic"))
+def test_step_reset_first_equals_rollout(policy):
+    """BatchEnv.step(autoreset="next") (RS_STEP_RESET_FIRST through rs_step_ex)
+    with the next actions fed back equals the fused rollout of the same
+    policy env for env, finished envs included (the runner's order)"""
+    n, steps = 256, 160
+    cfg = EnvConfig(rule="red")
+    a = BatchEnv(n, cfg).init(seed=5)
+    b = BatchEnv(n, cfg).init(seed=5)
+    a.rollout(steps, policy=policy)
+    acts = b.heuristic_actions() if policy == "heuristic" else b.random_actions()
+    nxt = torch.empty(n, dtype=torch.int32, device="cuda")
+    for _ in range(steps):
+        b.step(acts, autoreset="next", next_actions=nxt, next_policy=policy)
+        acts, nxt = nxt, acts
+    torch.cuda.synchronize()
+    for i in range(0, n, 5):
+        ra, rb = a.export(i), b.export(i)
+        pa, pb = projection(ra), projection(rb)
+        if not (ra.env_terminated or ra.env_truncated) and policy == "random":
+            # b has already drawn its next action from the policy stream
+            assert rb.policy_counter == ra.policy_counter + 1
+            for d in (pa, pb):
+                d["internal"].pop("policy_counter", None)
+        assert not diff(pa, pb), (i, diff(pa, pb)[:5])
