@@ -323,7 +323,8 @@ int rs_step(rs_handle* h, const int32_t* actions_dev, const rs_step_out* out, vo
  * finishes an env leaves it finished (its outputs describe the final
  * state, next action -1).  Per-env trajectories equal rs_rollout's.  Needs
  * a policy output (next_actions or recs); exclusive with
- * RS_STEP_AUTORESET. */
+ * RS_STEP_AUTORESET.  An env whose action is RS_ACTION_SKIP is left
+ * untouched (not reset). */
 #define RS_STEP_RESET_FIRST 16
 int rs_step_ex(rs_handle* h, const int32_t* actions_dev, int32_t flags, const rs_step_out* out,
                const rs_obs_out* obs, int32_t* next_actions_dev, void* stream);
