@@ -513,8 +513,11 @@ __device__ __noinline__ void warm_win_path(int piece, const Soa& S, const Tabs& 
 __device__ __forceinline__ void warm_cta(const Soa& S, const Tabs& T, const Cfg& C) {
   __shared__ int s_sink;
   const int wp = threadIdx.x >> 5;
-  const uint32_t need = wp == 1 ? BLK_BYTES : 0u;
-  if ((threadIdx.x & 31) == 0 && wp < 2 && need <= dyn_smem_bytes()) warm_win_path(wp, S, T, C, g_smem, &s_sink);
+  // piece 1's scratch block after the staged tables (-DRS_TABLES_SMEM: their
+  // bulk copy lands first; WALL_SLOT_OFF is 0 otherwise)
+  const uint32_t need = wp == 1 ? (uint32_t)WALL_SLOT_OFF + BLK_BYTES : 0u;
+  if ((threadIdx.x & 31) == 0 && wp < 2 && need <= dyn_smem_bytes())
+    warm_win_path(wp, S, T, C, g_smem + WALL_SLOT_OFF, &s_sink);
 }
 
 __global__ void __launch_bounds__(ROLL_BLOCK, ROLL_MINB) k_step(const __grid_constant__ Soa S, const __grid_constant__ DevTables D,
@@ -524,8 +527,8 @@ __global__ void __launch_bounds__(ROLL_BLOCK, ROLL_MINB) k_step(const __grid_con
   tables_begin(D, glog2);  // the action and header loads overlap the table copy
   const Tabs T{};
   if (warm && blockIdx.x == gridDim.x - 1) {  // the warm-up CTA (no envs)
-    warm_cta(S, T, C);
     tables_wait();
+    warm_cta(S, T, C);
     return;
   }
   const int lane = threadIdx.x & 31;
@@ -689,8 +692,8 @@ __global__ void __launch_bounds__(ROLL_BLOCK, ROLL_MINB) k_rollout(const __grid_
   tables_begin(D, glog2);  // the first env tile's header loads overlap the copy
   const Tabs T{};
   if (warm && blockIdx.x == gridDim.x - 1) {  // the warm-up CTA (no envs)
-    warm_cta(S, T, C);
     tables_wait();
+    warm_cta(S, T, C);
     return;
   }
   bool tables_ready = false;
@@ -1362,9 +1365,19 @@ int rs_create(rs_handle** out, int64_t n_envs, const rs_config* cfg, int32_t dev
   const void* kernels[] = {(const void*)k_init, (const void*)k_step, (const void*)k_policy,
                            (const void*)k_observe, (const void*)k_rollout<false>, (const void*)k_rollout<true>,
                            (const void*)k_import, (const void*)k_autoreset, (const void*)k_check};
-  for (const void* k : kernels)
-    if ((err = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_staged(ROLL_BLOCK, ROLL_BLOCK))))
+  // the largest launch (the stage mode's slots) may exceed the opt-in limit
+  // in a -DRS_TABLES_SMEM build (tables + scratch + 256 slots): allow what
+  // the device allows; a launch that needs more fails at launch
+  int optin = 0;
+  if ((err = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device)))
+    return cleanup(err, "device query");
+  for (const void* k : kernels) {
+    cudaFuncAttributes fa{};
+    if ((err = cudaFuncGetAttributes(&fa, k))) return cleanup(err, "cudaFuncGetAttributes");
+    const int want = std::min(smem_staged(ROLL_BLOCK, ROLL_BLOCK), optin - (int)fa.sharedSizeBytes);
+    if ((err = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, want)))
       return cleanup(err, "cudaFuncSetAttribute");
+  }
   if ((err = cudaDeviceGetAttribute(&h->num_sms, cudaDevAttrMultiProcessorCount, device)))
     return cleanup(err, "device query");
   for (int i = 0; i < 16; i++) h->occ_key[i] = h->occ_val[i] = 0;
