@@ -91,3 +91,18 @@ def test_create_rejects_bad_config_without_gpu():
                         kazoe=0, double_yakuman=0, agari_yame=1, renchan_cap=32)
     assert L.rs_create(C.byref(h), 16, C.byref(cfg), 0) != 0
     assert L.rs_state_bytes(None) == 976
+
+
+def test_python_constants_match_the_header():
+    """abi.py's step flags and status codes are the header's #defines"""
+    from paper_2605_20577_b200 import abi
+
+    text = (Path(__file__).resolve().parent.parent / "include" / "rinshan.h").read_text()
+    defs = {m.group(1): int(m.group(2).strip("()").replace("-2147483647 - 1", str(-2**31)))
+            for m in re.finditer(r"#define (RS_(?:STEP|E)_[A-Z_]+) (\(?-?[0-9]+\)?)", text)}
+    want = {"RS_STEP_AUTORESET": abi.STEP_AUTORESET, "RS_STEP_OBSERVE": abi.STEP_OBSERVE,
+            "RS_STEP_HEURISTIC": abi.STEP_HEURISTIC, "RS_STEP_SIGNAL": abi.STEP_SIGNAL,
+            "RS_STEP_RESET_FIRST": abi.STEP_RESET_FIRST, "RS_E_ARG": abi.RS_E_ARG,
+            "RS_E_TABLES": abi.RS_E_TABLES, "RS_E_STATE": abi.RS_E_STATE, "RS_E_CORRUPT": abi.RS_E_CORRUPT}
+    for name, value in want.items():
+        assert defs[name] == value, name
