@@ -513,6 +513,27 @@ __device__ __noinline__ void warm_win_path(int piece, const Soa& S, const Tabs& 
 __device__ __forceinline__ void warm_cta(const Soa& S, const Tabs& T, const Cfg& C) {
   __shared__ int s_sink;
   const int wp = threadIdx.x >> 5;
+#if defined(__CUDA_ARCH__)
+  if (wp == 2 && grp_size() >= 4) {
+    // the reset's deal (deal_group, the lane-group path): every lane of the
+    // warp, one scratch block + identity wall per lane group, after the
+    // tables; it runs ~7 us into a reset, so the warm copy gets ahead
+    const int G = grp_size(), grp = (threadIdx.x & 31) / G, sub = grp_sub();
+    const uint32_t base = (uint32_t)WALL_SLOT_OFF + (uint32_t)grp * 1024u;
+    if (base + 1024u <= dyn_smem_bytes()) {
+      uint8_t* bp = g_smem + base;
+      uint8_t* w = bp + 768;
+      for (int i = sub; i < (int)BLK_BYTES / 4; i += G) reinterpret_cast<uint32_t*>(bp)[i] = 0u;
+      for (int i = sub; i < 36; i += G) reinterpret_cast<uint32_t*>(w)[i] = 0x03020100u + 0x04040404u * (uint32_t)i;
+      __syncwarp(grp_mask());
+      Engine E(S, T, C, 0, bp);
+      E.g = Game{};
+      E.deal_group(w, 0);
+      if (sub == 0) s_sink = (int)reinterpret_cast<const uint32_t*>(bp)[W_HINFO];
+    }
+    return;
+  }
+#endif
   // piece 1's scratch block after the staged tables (-DRS_TABLES_SMEM: their
   // bulk copy lands first; WALL_SLOT_OFF is 0 otherwise)
   const uint32_t need = wp == 1 ? (uint32_t)WALL_SLOT_OFF + BLK_BYTES : 0u;

@@ -282,7 +282,7 @@ struct Engine {
   // lane group of 4+: lane sub builds seat sub & 3 (the four deals' table
   // lookups in parallel instead of one seat after the other); the waits of
   // a 13-tile tenpai deal (rare) are then scanned by the whole group
-  RS_HD void deal_group(const uint8_t* w, int dealer) {
+  RS_COLD void deal_group(const uint8_t* w, int dealer) {  // one copy (warm_cta warms it)
     const int sub = grp_sub();
     const uint32_t gm = grp_mask();
     const int s = sub & 3;
